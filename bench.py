@@ -1,0 +1,429 @@
+#!/usr/bin/env python
+"""Benchmark of the all-pairs PCC hot path on B200 (BASELINE.json's metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--config c2]
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 ... bench.py --gpus N
+
+One step = one pass of the hot path over the config's synthetic dataset:
+K1 normalisation of all n rows + K2 symmetric contraction of this rank's
+contiguous share of the GPU tile jobs (partition(T, N), distributed.py:76-92)
+with the packed epilogue.  Inputs are resident in HBM before the timed
+region; X and U (>= 537 MB at c2) exceed the 126 MB L2, so no flush is
+needed between steps.  Timing is CUDA events on the launching stream, W
+untimed warm-up steps, K timed steps between barrier+synchronize, max over
+ranks.  ``e2e`` times the public API (``allpairs`` / the per-worker shard
+call) with the pinned-host upload of X and the download of this rank's
+packed cells inside the timed region.
+
+``--impl reference`` times the reference algorithm's CPU implementation
+(the bit-exact C port under oracle/, all host threads) on a bounded sample
+of the same workload -- the reference itself is Python+numba and not
+installable on the box.  Only rank 0 runs it.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+DEFAULT_CONFIG = "c2"  # BASELINE.json configs[1]: the single-GPU headline configuration
+
+
+def _env_int(name: str, default: int) -> int:
+    v = os.environ.get(name)
+    return int(v) if v not in (None, "") else default
+
+
+def parse_args(argv=None):
+    p = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=("b200", "reference"), default="b200")
+    p.add_argument("--config", default=DEFAULT_CONFIG, choices=("c1", "c2", "c3", "c4", "c5"))
+    p.add_argument("--e2e-steps", type=int, default=None, help="timed end-to-end API calls (default: min(steps, 5))")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-fraction", type=float, default=None,
+                   help="fraction of the reference t=4 tile range in the CPU sample")
+    return p.parse_args(argv)
+
+
+# --------------------------------------------------------------------------- CPU (oracle) leg
+
+def cpu_sample(x: np.ndarray, fraction: float, threads: int) -> dict:
+    """Time the reference algorithm (bit-exact C port) on the host: normalize
+    all rows, then compute+scatter the first ``fraction`` of the t=4 tile range
+    (engine.py:46-52 with capacity = the sample).  Returns pairs/s."""
+    import oracle
+    from paper_1605_01584_b200.indexing import sym_job_coord
+
+    n, l = x.shape
+    t = 4
+    m = -(-n // t)
+    total = m * (m + 1) // 2
+    hi = max(1, int(total * fraction))
+    # cells (y <= x < n) inside tiles [0, hi): whole tile rows + a partial one
+    yt, xt = sym_job_coord(m, hi - 1)
+    pairs = 0
+    for r in range(yt + 1):
+        x_last = m - 1 if r < yt else xt
+        for ry in range(t):
+            y = r * t + ry
+            if y >= n:
+                break
+            x_hi = min(n, (x_last + 1) * t)
+            pairs += max(0, x_hi - max(y, r * t))
+    t0 = time.perf_counter()
+    u, _ = oracle.normalize(x, threads=threads)
+    flat = oracle.compute_pass(u, t, 0, hi, threads=threads)
+    packed = np.empty(n * (n + 1) // 2, dtype=np.float64)
+    oracle.scatter_range(packed, flat, 0, hi, m, t, n)
+    dt = time.perf_counter() - t0
+    return {"pairs": pairs, "seconds": dt, "pairs_per_s": pairs / dt, "tiles": hi, "total_tiles": total}
+
+
+def run_reference(args, rank: int, world: int) -> None:
+    if rank != 0:
+        return
+    import oracle
+    from paper_1605_01584_b200.workloads import CONFIGS, make_config
+
+    spec = CONFIGS[args.config]
+    x = make_config(args.config)
+    threads = oracle.default_threads()
+    frac = args.cpu_fraction or _default_ref_fraction(args.config)
+    for _ in range(args.warmup):
+        cpu_sample(x, frac / 4, threads)
+    samples = [cpu_sample(x, frac, threads) for _ in range(args.steps)]
+    secs = [s["seconds"] for s in samples]
+    pairs = samples[0]["pairs"]
+    value = pairs / statistics.median(secs)
+    sample_desc = (f"normalize all {spec.n} rows + compute_tile_range/scatter_range of reference t=4 tiles "
+                   f"[0, {samples[0]['tiles']}) of {samples[0]['total_tiles']} ({pairs} pairs), median of {len(secs)}")
+    line = {
+        "impl": "reference",
+        "metric": "pairs_per_sec",
+        "value": value,
+        "unit": "pairs/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": statistics.median(secs) * 1e3,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic",
+        "config": _config_dict(args.config, world),
+        "gflops": 2.0 * spec.l * pairs / statistics.median(secs) / 1e9,
+        "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": threads, "kind": "port", "sample": sample_desc},
+        "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _default_ref_fraction(cfg: str) -> float:
+    # ~1-2 s of 16-thread CPU work per step
+    return {"c1": 1.0, "c2": 1 / 64, "c3": 1 / 8, "c4": 1 / 512, "c5": 1 / 512}[cfg]
+
+
+# --------------------------------------------------------------------------- helpers
+
+def _config_dict(cfg: str, world: int) -> dict:
+    from paper_1605_01584_b200.workloads import CONFIGS
+
+    spec = CONFIGS[cfg]
+    return {
+        "workload": f"{cfg}: n={spec.n} x l={spec.l} FP64, {spec.description}",
+        "n": spec.n,
+        "l": spec.l,
+        "seed": spec.seed,
+        "global_batch": spec.n,
+        "parallelism": f"tile-range partition over {world} GPU(s), no collective in the data path",
+        "l2_policy": "inputs larger than L2 (X and U >= 537 MB vs 126 MB L2); no flush",
+        "output": "packed upper triangle n(n+1)/2 f64, sharded per GPU range, kept on device",
+    }
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region (B200_PROFILING.md)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        rows = []
+        try:
+            for line in open(self.path):
+                f = [c.strip() for c in line.split(",")]
+                if len(f) >= 9:
+                    rows.append(f)
+        except OSError:
+            pass
+        finally:
+            try:
+                os.unlink(self.path)
+            except OSError:
+                pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        pw = [float(r[3]) for r in rows if r[3].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower().startswith("active")})
+        load = [s for s in sm if mx and s > 0.3 * max(mx)] or sm
+        return {
+            "sm_mhz": statistics.median(load) if load else None,
+            "sm_max_mhz": max(mx) if mx else None,
+            "power_w_max": max(pw) if pw else None,
+            "reasons": reasons,
+            "samples": len(rows),
+        }
+
+
+def _load_traffic(cfg: str):
+    """Per-launch DRAM bytes of the contraction kernel from the committed ncu capture."""
+    p = ROOT / "profiles" / "ncu_syrk_traffic.json"
+    try:
+        d = json.loads(p.read_text())
+        return d.get(cfg, {}).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
+# --------------------------------------------------------------------------- GPU leg
+
+def run_b200(args, rank: int, world: int, local_rank: int) -> None:
+    import torch
+    import torch.distributed as dist
+
+    import paper_1605_01584_b200 as pc
+    from paper_1605_01584_b200 import _lib
+    from paper_1605_01584_b200._device import ptr, stream_handle
+    from paper_1605_01584_b200.distributed import partition, shard_span, owned_runs, compute_worker
+    from paper_1605_01584_b200.workloads import CONFIGS, make_config
+    from paper_1605_01584_b200.transform import normalize_device
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    spec = CONFIGS[args.config]
+    n, l = spec.n, spec.l
+    L = _lib.lib()
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local_rank])
+
+    def max_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    x_host = make_config(args.config)
+    x_pinned = torch.from_numpy(x_host).pin_memory()
+    x = x_pinned.to(dev)
+    T = int(L.pcc_gpu_tile_count(n))
+    tb, te = partition(T, world)[rank]
+    span_lo, span_hi = shard_span(n, tb, te)
+    shard = torch.empty(max(1, span_hi - span_lo), dtype=torch.float64, device=dev)
+    my_cells = sum(hi - lo for lo, hi in owned_runs(n, tb, te))
+    total_pairs = n * (n + 1) // 2
+    stream = torch.cuda.current_stream()
+    s = stream_handle(stream)
+
+    def step(ev_pair=None):
+        u, flags = normalize_device(x)
+        if ev_pair is not None:
+            ev_pair[0].record(stream)
+        if te > tb:
+            _lib.check(L.pcc_syrk_f64(ptr(u), n, l, u.shape[1], tb, te, _lib.LAYOUT_PACKED, ptr(shard), 0,
+                                      span_lo, 0, 0, 0, s), "syrk")
+        if ev_pair is not None:
+            ev_pair[1].record(stream)
+        return u, flags
+
+    # warm-up (also the first-touch of the allocator)
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+
+    syrk_events = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for _ in range(args.steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clocks:
+        t0.record(stream)
+        for i in range(args.steps):
+            step(syrk_events[i])
+        t1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    elapsed_ms = t0.elapsed_time(t1)
+    syrk_ms = [a.elapsed_time(b) for a, b in syrk_events]
+    ms_step = max_over_ranks(elapsed_ms / args.steps)
+    syrk_avg_ms = max_over_ranks(sum(syrk_ms) / len(syrk_ms)) if te > tb else 0.0
+    clock = clocks.summary()
+
+    # ---- roofline of the dominant kernel (the contraction), per launch
+    peak = _lib.probe_fp64_peak()
+    flops_launch = 2.0 * l * my_cells                          # algorithmic: 2 l per owned pair
+    achieved = flops_launch / (sum(syrk_ms) / len(syrk_ms) * 1e-3) / 1e12 if te > tb else 0.0
+    achieved = max_over_ranks(achieved) if world == 1 else achieved
+    roof = {
+        "bound": "tensor",
+        "achieved": achieved,
+        "peak": peak,
+        "unit": "TFLOP/s",
+        "frac": achieved / peak if peak else None,
+        "traffic": _load_traffic(args.config),
+        "kernel": "syrk_kernel<packed> (DMMA.8x8x4 FP64)",
+        "peak_source": "measured live: register-resident mma.sync f64 probe (pcc_probe_fp64_peak); "
+                       "MEASURED_PEAKS.json has no FP64 entry",
+        "algorithmic_flops_per_launch": flops_launch,
+    }
+
+    # ---- end to end through the public API (pinned X upload + packed download inside)
+    e2e_steps = args.e2e_steps if args.e2e_steps is not None else min(args.steps, 5)
+    host_out = torch.empty(total_pairs if world == 1 else max(1, span_hi - span_lo), dtype=torch.float64,
+                           pin_memory=True)
+    ds = pc.Dataset(values=x_pinned)
+    if world == 1:
+        def api_call():
+            return pc.allpairs(ds, out=host_out)
+    else:
+        def api_call():
+            return compute_worker(ds, world, rank, dev, out=host_out)
+    api_call()  # warm-up
+    barrier()
+    wall = []
+    for _ in range(e2e_steps):
+        torch.cuda.synchronize()
+        barrier()
+        a = time.perf_counter()
+        r = api_call()
+        wall.append(time.perf_counter() - a)
+    e2e_s = max_over_ranks(statistics.median(wall))
+    h2d = n * l * 8 * world
+    d2h = total_pairs * 8
+    if world == 1:
+        # sanity: the API result matches the device-timed shard bit for bit
+        assert np.array_equal(r.packed.numpy()[:1000], shard[:1000].cpu().numpy())
+
+    # ---- CPU baseline (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle
+
+        threads = oracle.default_threads()
+        frac = args.cpu_fraction or {"c1": 1.0, "c2": 1 / 16, "c3": 1 / 2, "c4": 1 / 256, "c5": 1 / 128}[args.config]
+        res = cpu_sample(x_host, frac, threads)
+        cpu = {
+            "value": res["pairs_per_s"],
+            "unit": "pairs/s",
+            "cores": threads,
+            "kind": "port",
+            "sample": (f"bit-exact C port of the reference (oracle/), {threads} threads: normalize all rows + "
+                       f"t=4 tiles [0, {res['tiles']}) of {res['total_tiles']} = {res['pairs']} pairs in "
+                       f"{res['seconds']:.2f} s"),
+        }
+
+    value = total_pairs / (ms_step * 1e-3)
+    if rank == 0:
+        line = {
+            "metric": "pairs_per_sec",
+            "value": value,
+            "unit": "pairs/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": max(3, args.warmup),
+            "ms_per_step": ms_step,
+            "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic",
+            "config": _config_dict(args.config, world),
+            "gflops": float(n) * n * l / (ms_step * 1e-3) / 1e9,
+            "roofline_fp64_frac_of_step": (float(n) * n * l / world / (ms_step * 1e-3) / 1e12) / peak,
+            "syrk_ms": syrk_avg_ms,
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": {"value": total_pairs / e2e_s, "unit": "pairs/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3, "steps": e2e_steps},
+            "gpu_launches": 2 * args.steps,
+            "clocks": clock,
+        }
+        print(json.dumps(line), flush=True)
+
+
+def main(argv=None):
+    args = parse_args(argv)
+    rank = _env_int("RANK", 0)
+    world = _env_int("WORLD_SIZE", 1)
+    local_rank = _env_int("LOCAL_RANK", 0)
+    if world > 1:
+        import torch.distributed as dist
+
+        backend = "gloo" if args.impl == "reference" else "nccl"
+        if backend == "nccl":
+            import torch
+
+            torch.cuda.set_device(local_rank)
+        dist.init_process_group(backend=backend)
+    try:
+        if args.impl == "reference":
+            run_reference(args, rank, world)
+        else:
+            run_b200(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

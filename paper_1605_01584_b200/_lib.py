@@ -1,0 +1,140 @@
+"""ctypes binding of the C ABI in ``include/pcc_b200.h`` (libpcc_b200.so).
+
+The library is built in-tree by ``__graft_entry__.build()`` (nvcc,
+``-gencode arch=compute_100a,code=sm_100a``) into
+``paper_1605_01584_b200/lib/libpcc_b200.so``.  There is no fallback: if the
+library is missing or no B200 is visible, every compute entry point raises.
+ctypes releases the GIL for the duration of each call, so one host thread per
+device drives devices concurrently (SURVEY.md §5 "Distributed communication
+backend").
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from pathlib import Path
+
+from .errors import DeviceError
+
+__all__ = [
+    "LIB_PATH",
+    "lib",
+    "check",
+    "DeviceInfo",
+    "GPU_TILE",
+    "K_ALIGN",
+    "LAYOUT_PACKED",
+    "LAYOUT_DENSE",
+    "LAYOUT_TILES",
+    "EXPORTED_SYMBOLS",
+]
+
+LIB_PATH = Path(__file__).resolve().parent / "lib" / "libpcc_b200.so"
+
+PCC_OK, PCC_EINVAL, PCC_ECUDA = 0, 1, 2
+GPU_TILE = 128
+K_ALIGN = 16
+LAYOUT_PACKED, LAYOUT_DENSE, LAYOUT_TILES = 0, 1, 2
+
+# Every symbol include/pcc_b200.h declares (tests check the .so exports them).
+EXPORTED_SYMBOLS = (
+    "pcc_last_error",
+    "pcc_version",
+    "pcc_device_info",
+    "pcc_rows_padded",
+    "pcc_ldu",
+    "pcc_gpu_tile_count",
+    "pcc_normalize_rows_f64",
+    "pcc_zero_rows_f64",
+    "pcc_syrk_f64",
+    "pcc_compute_pass_f64",
+    "pcc_scatter_range_f64",
+    "pcc_allpairs_f64",
+    "pcc_probe_fp64_peak",
+)
+
+
+class DeviceInfo(ctypes.Structure):
+    _fields_ = [
+        ("device", ctypes.c_int),
+        ("sm_count", ctypes.c_int),
+        ("cc_major", ctypes.c_int),
+        ("cc_minor", ctypes.c_int),
+        ("max_smem_optin", ctypes.c_int),
+        ("syrk_ctas_per_sm", ctypes.c_int),
+        ("syrk_smem_bytes", ctypes.c_int),
+        ("gpu_tile", ctypes.c_int),
+        ("total_mem", ctypes.c_size_t),
+    ]
+
+
+_lock = threading.Lock()
+_lib = None
+
+_i32, _i64, _u64 = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64
+_vp = ctypes.c_void_p
+
+
+def _bind(l: ctypes.CDLL) -> None:
+    sig = {
+        "pcc_last_error": (ctypes.c_char_p, []),
+        "pcc_version": (ctypes.c_int, []),
+        "pcc_device_info": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(DeviceInfo)]),
+        "pcc_rows_padded": (_i64, [_i64]),
+        "pcc_ldu": (_i64, [_i64]),
+        "pcc_gpu_tile_count": (_u64, [_i64]),
+        "pcc_normalize_rows_f64": (ctypes.c_int, [_vp, _i64, _vp, _i64, _vp, _i64, _i64, _i64, _vp]),
+        "pcc_zero_rows_f64": (ctypes.c_int, [_vp, _i64, _i64, _i64, _vp]),
+        "pcc_syrk_f64": (ctypes.c_int, [_vp, _i64, _i64, _i64, _u64, _u64, _i32, _vp, _i64, _u64, _i32, _u64, _u64, _vp]),
+        "pcc_compute_pass_f64": (ctypes.c_int, [_vp, _i64, _i64, _i64, _i64, _u64, _u64, _vp, _vp]),
+        "pcc_scatter_range_f64": (ctypes.c_int, [_vp, _vp, _u64, _u64, _i64, _i64, _vp]),
+        "pcc_allpairs_f64": (ctypes.c_int, [_vp, _i64, _i64, _i64, _vp, _i64, _vp, _u64, _u64, _i32, _vp, _i64, _u64, _vp]),
+        "pcc_probe_fp64_peak": (ctypes.c_int, [ctypes.POINTER(ctypes.c_double)]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(l, name)
+        fn.restype = res
+        fn.argtypes = args
+
+
+def lib() -> ctypes.CDLL:
+    """Load (once) and return the engine library; raise DeviceError if absent."""
+    global _lib
+    if _lib is None:
+        with _lock:
+            if _lib is None:
+                if not LIB_PATH.exists():
+                    raise DeviceError(
+                        f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+                        "(there is no CPU fallback)"
+                    )
+                l = ctypes.CDLL(str(LIB_PATH))
+                _bind(l)
+                _lib = l
+    return _lib
+
+
+def check(rc: int, what: str = "") -> None:
+    """Map a C-ABI status to the reference's exception conventions."""
+    if rc == PCC_OK:
+        return
+    msg = lib().pcc_last_error().decode(errors="replace")
+    if what:
+        msg = f"{what}: {msg}"
+    if rc == PCC_EINVAL:
+        raise ValueError(msg)
+    raise DeviceError(msg)
+
+
+def device_info(device: int) -> DeviceInfo:
+    info = DeviceInfo()
+    check(lib().pcc_device_info(device, ctypes.byref(info)), "pcc_device_info")
+    return info
+
+
+def probe_fp64_peak() -> float:
+    """Measured DMMA (FP64 tensor pipe) TFLOP/s of the current device."""
+    v = ctypes.c_double(0.0)
+    check(lib().pcc_probe_fp64_peak(ctypes.byref(v)), "pcc_probe_fp64_peak")
+    return v.value

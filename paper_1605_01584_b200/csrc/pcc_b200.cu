@@ -1,0 +1,319 @@
+// pcc_b200.cu -- C ABI (include/pcc_b200.h) over the sm_100a kernels.
+//
+// Host-side argument checking mirrors the reference's errors: anything the
+// reference rejects with ValueError (bad ranges, sizes) returns PCC_EINVAL
+// with a message; CUDA failures return PCC_ECUDA.  Nothing here falls back
+// to a CPU path.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/pcc_b200.h"
+#include "normalize.cuh"
+#include "syrk.cuh"
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+int fail(int code, const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char *what) {
+  return fail(PCC_ECUDA, "%s: %s (%s)", what, cudaGetErrorString(e), cudaGetErrorName(e));
+}
+
+#define PCC_CUDA(call, what)                      \
+  do {                                            \
+    cudaError_t e_ = (call);                      \
+    if (e_ != cudaSuccess) return cuda_fail(e_, what); \
+  } while (0)
+
+struct DeviceConfig {
+  bool ready = false;
+  int sm_count = 0;
+  int cc_major = 0, cc_minor = 0;
+  int max_smem_optin = 0;
+  int syrk_ctas_per_sm = 0;
+  size_t total_mem = 0;
+};
+
+constexpr int kMaxDevices = 64;
+DeviceConfig g_dev[kMaxDevices];
+std::mutex g_dev_mu;
+
+template <int LAYOUT>
+int configure_syrk(int *ctas) {
+  PCC_CUDA(cudaFuncSetAttribute(pcc::syrk_kernel<LAYOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                pcc::kSyrkSmemBytes),
+           "cudaFuncSetAttribute(syrk smem)");
+  PCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas, pcc::syrk_kernel<LAYOUT>, pcc::kSyrkThreads,
+                                                         pcc::kSyrkSmemBytes),
+           "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+  return PCC_OK;
+}
+
+// Per-device one-time setup (smem opt-in, occupancy); returns the config of
+// the calling thread's current device.
+int device_config(const DeviceConfig **out, int device = -1) {
+  if (device < 0) PCC_CUDA(cudaGetDevice(&device), "cudaGetDevice");
+  if (device >= kMaxDevices) return fail(PCC_EINVAL, "device %d out of range", device);
+  std::lock_guard<std::mutex> lock(g_dev_mu);
+  DeviceConfig &c = g_dev[device];
+  if (!c.ready) {
+    int prev = 0;
+    PCC_CUDA(cudaGetDevice(&prev), "cudaGetDevice");
+    if (prev != device) PCC_CUDA(cudaSetDevice(device), "cudaSetDevice");
+    cudaDeviceProp p;
+    PCC_CUDA(cudaGetDeviceProperties(&p, device), "cudaGetDeviceProperties");
+    c.sm_count = p.multiProcessorCount;
+    c.cc_major = p.major;
+    c.cc_minor = p.minor;
+    c.max_smem_optin = (int)p.sharedMemPerBlockOptin;
+    c.total_mem = p.totalGlobalMem;
+    if (p.major != 10) {
+      if (prev != device) cudaSetDevice(prev);
+      return fail(PCC_ECUDA, "device %d is sm_%d%d; this library is built for sm_100a (B200) only", device,
+                  p.major, p.minor);
+    }
+    int c0 = 0, c1 = 0, c2 = 0;
+    int rc = configure_syrk<pcc::kLayoutPacked>(&c0);
+    if (rc == PCC_OK) rc = configure_syrk<pcc::kLayoutDense>(&c1);
+    if (rc == PCC_OK) rc = configure_syrk<pcc::kLayoutTiles>(&c2);
+    if (prev != device) cudaSetDevice(prev);
+    if (rc != PCC_OK) return rc;
+    c.syrk_ctas_per_sm = c0 < c1 ? (c0 < c2 ? c0 : c2) : (c1 < c2 ? c1 : c2);
+    if (c.syrk_ctas_per_sm < 1) return fail(PCC_ECUDA, "contraction kernel cannot be resident on device %d", device);
+    c.ready = true;
+  }
+  *out = &c;
+  return PCC_OK;
+}
+
+inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+
+int check_u(const double *u, int64_t n, int64_t l, int64_t ldu) {
+  if (n < 1 || (uint64_t)n > 0xFFFFFFFFull) return fail(PCC_EINVAL, "n must be in [1, 2^32-1], got %lld", (long long)n);
+  if (l < 1) return fail(PCC_EINVAL, "l must be >= 1, got %lld", (long long)l);
+  if (ldu < pcc_ldu(l) || (ldu & 1))
+    return fail(PCC_EINVAL, "ldu %lld must be even and >= pcc_ldu(l) = %lld", (long long)ldu, (long long)pcc_ldu(l));
+  if (u == nullptr || (reinterpret_cast<uintptr_t>(u) & 15))
+    return fail(PCC_EINVAL, "u must be a non-null 16-byte aligned device pointer");
+  return PCC_OK;
+}
+
+template <int LAYOUT>
+int launch_syrk(const double *u, int64_t n, int64_t l, int64_t ldu, uint64_t tb, uint64_t te,
+                const pcc::Epilogue &ep, cudaStream_t stream) {
+  if (te <= tb) return PCC_OK;
+  const DeviceConfig *dc = nullptr;
+  int rc = device_config(&dc);
+  if (rc) return rc;
+  const uint64_t m_g = ceil_div((uint64_t)n, pcc::kTile);
+  const int k_tiles = (int)ceil_div((uint64_t)l, pcc::kBK);
+  const uint64_t resident = (uint64_t)dc->sm_count * (uint64_t)dc->syrk_ctas_per_sm;
+  const uint64_t tiles = te - tb;
+  const unsigned grid = (unsigned)(tiles < resident ? tiles : resident);
+  pcc::syrk_kernel<LAYOUT><<<grid, pcc::kSyrkThreads, pcc::kSyrkSmemBytes, stream>>>(u, n, ldu, k_tiles, m_g, tb,
+                                                                                      te, ep);
+  PCC_CUDA(cudaGetLastError(), "syrk_kernel launch");
+  return PCC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *pcc_last_error(void) { return g_err; }
+
+int pcc_version(void) { return 100; }
+
+int64_t pcc_rows_padded(int64_t n) { return n <= 0 ? 0 : (int64_t)ceil_div((uint64_t)n, pcc::kTile) * pcc::kTile; }
+
+int64_t pcc_ldu(int64_t l) { return l <= 0 ? 0 : (int64_t)ceil_div((uint64_t)l, PCC_K_ALIGN) * PCC_K_ALIGN; }
+
+uint64_t pcc_gpu_tile_count(int64_t n) {
+  if (n <= 0) return 0;
+  const uint64_t m = ceil_div((uint64_t)n, pcc::kTile);
+  return m * (m + 1) / 2;
+}
+
+int pcc_device_info(int device, pcc_device_info_t *info) {
+  if (info == nullptr) return fail(PCC_EINVAL, "info is NULL");
+  if (device < 0) return fail(PCC_EINVAL, "device must be >= 0");
+  int count = 0;
+  PCC_CUDA(cudaGetDeviceCount(&count), "cudaGetDeviceCount");
+  if (device >= count) return fail(PCC_EINVAL, "device %d >= device count %d", device, count);
+  const DeviceConfig *dc = nullptr;
+  int rc = device_config(&dc, device);
+  if (rc) return rc;
+  info->device = device;
+  info->sm_count = dc->sm_count;
+  info->cc_major = dc->cc_major;
+  info->cc_minor = dc->cc_minor;
+  info->max_smem_optin = dc->max_smem_optin;
+  info->syrk_ctas_per_sm = dc->syrk_ctas_per_sm;
+  info->syrk_smem_bytes = pcc::kSyrkSmemBytes;
+  info->gpu_tile = pcc::kTile;
+  info->total_mem = dc->total_mem;
+  return PCC_OK;
+}
+
+int pcc_normalize_rows_f64(const double *x, int64_t ldx, double *u, int64_t ldu, uint8_t *zero_variance,
+                           int64_t l, int64_t row_lo, int64_t row_hi, void *stream) {
+  if (l < 2) return fail(PCC_EINVAL, "need at least 2 samples per variable, got %lld", (long long)l);
+  if (ldx < l || ldu < l) return fail(PCC_EINVAL, "ldx (%lld) and ldu (%lld) must be >= l (%lld)", (long long)ldx,
+                                      (long long)ldu, (long long)l);
+  if (row_lo < 0 || row_hi < row_lo)
+    return fail(PCC_EINVAL, "bad row range [%lld, %lld)", (long long)row_lo, (long long)row_hi);
+  if (row_hi == row_lo) return PCC_OK;
+  if (!x || !u || !zero_variance) return fail(PCC_EINVAL, "null pointer");
+  const uint64_t rows = (uint64_t)(row_hi - row_lo);
+  const uint64_t grid = ceil_div(rows, pcc::kNormRowsPerCta);
+  if (grid > 0x7FFFFFFFull) return fail(PCC_EINVAL, "too many rows");
+  pcc::normalize_rows_kernel<<<(unsigned)grid, pcc::kNormThreads, 0, (cudaStream_t)stream>>>(
+      x, ldx, u, ldu, zero_variance, l, row_lo, row_hi);
+  PCC_CUDA(cudaGetLastError(), "normalize_rows_kernel launch");
+  return PCC_OK;
+}
+
+int pcc_zero_rows_f64(double *u, int64_t ldu, int64_t row_lo, int64_t row_hi, void *stream) {
+  if (row_lo < 0 || row_hi < row_lo || ldu < 0) return fail(PCC_EINVAL, "bad row range");
+  if (row_hi == row_lo || ldu == 0) return PCC_OK;
+  PCC_CUDA(cudaMemsetAsync(u + row_lo * ldu, 0, (size_t)(row_hi - row_lo) * (size_t)ldu * sizeof(double),
+                           (cudaStream_t)stream),
+           "cudaMemsetAsync(pad rows)");
+  return PCC_OK;
+}
+
+int pcc_syrk_f64(const double *u, int64_t n, int64_t l, int64_t ldu, uint64_t tile_begin, uint64_t tile_end,
+                 int32_t layout, double *out, int64_t ld_out, uint64_t out_base, int32_t ref_t, uint64_t ref_begin,
+                 uint64_t ref_end, void *stream) {
+  int rc = check_u(u, n, l, ldu);
+  if (rc) return rc;
+  const uint64_t total = pcc_gpu_tile_count(n);
+  if (tile_begin > tile_end || tile_end > total)
+    return fail(PCC_EINVAL, "tile range [%llu, %llu) invalid for %llu tiles", (unsigned long long)tile_begin,
+                (unsigned long long)tile_end, (unsigned long long)total);
+  if (out == nullptr) return fail(PCC_EINVAL, "out is NULL");
+  pcc::Epilogue ep{out, ld_out, out_base, ref_t, 0, ref_begin, ref_end};
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (layout) {
+    case PCC_LAYOUT_PACKED:
+      return launch_syrk<pcc::kLayoutPacked>(u, n, l, ldu, tile_begin, tile_end, ep, s);
+    case PCC_LAYOUT_DENSE:
+      if (ld_out < n) return fail(PCC_EINVAL, "dense ld_out %lld < n %lld", (long long)ld_out, (long long)n);
+      return launch_syrk<pcc::kLayoutDense>(u, n, l, ldu, tile_begin, tile_end, ep, s);
+    case PCC_LAYOUT_TILES: {
+      if (ref_t < 1) return fail(PCC_EINVAL, "tile size must be >= 1, got %d", ref_t);
+      ep.ref_m = ceil_div((uint64_t)n, (uint64_t)ref_t);
+      const uint64_t ref_total = ep.ref_m * (ep.ref_m + 1) / 2;
+      if (ref_begin > ref_end || ref_end > ref_total)
+        return fail(PCC_EINVAL, "tile range [%llu, %llu) invalid for %llu tiles", (unsigned long long)ref_begin,
+                    (unsigned long long)ref_end, (unsigned long long)ref_total);
+      return launch_syrk<pcc::kLayoutTiles>(u, n, l, ldu, tile_begin, tile_end, ep, s);
+    }
+    default:
+      return fail(PCC_EINVAL, "unknown layout %d", layout);
+  }
+}
+
+int pcc_compute_pass_f64(const double *u, int64_t n, int64_t l, int64_t ldu, int64_t t, uint64_t j_lo,
+                         uint64_t j_hi, double *out, void *stream) {
+  int rc = check_u(u, n, l, ldu);
+  if (rc) return rc;
+  if (t < 1) return fail(PCC_EINVAL, "tile size must be >= 1, got %lld", (long long)t);
+  const uint64_t m = ceil_div((uint64_t)n, (uint64_t)t);
+  const uint64_t total = m * (m + 1) / 2;
+  if (j_lo > j_hi || j_hi > total)
+    return fail(PCC_EINVAL, "tile range [%llu, %llu) invalid for %llu tiles", (unsigned long long)j_lo,
+                (unsigned long long)j_hi, (unsigned long long)total);
+  if (j_hi == j_lo) return PCC_OK;
+  if (out == nullptr) return fail(PCC_EINVAL, "out is NULL");
+  cudaStream_t s = (cudaStream_t)stream;
+  // Cells outside y <= x < n are exactly 0.0 (_kernels.py:370-373).
+  PCC_CUDA(cudaMemsetAsync(out, 0, (size_t)(j_hi - j_lo) * (size_t)t * (size_t)t * sizeof(double), s),
+           "cudaMemsetAsync(pass buffer)");
+  // GPU tile rows covering the reference tile rows of [j_lo, j_hi).
+  const uint64_t yt_a = pcc::tile_row(m, j_lo), yt_b = pcc::tile_row(m, j_hi - 1);
+  const uint64_t y_a = yt_a * (uint64_t)t;
+  uint64_t y_b = (yt_b + 1) * (uint64_t)t;
+  if (y_b > (uint64_t)n) y_b = (uint64_t)n;
+  const uint64_t m_g = ceil_div((uint64_t)n, pcc::kTile);
+  const uint64_t Ya = y_a / pcc::kTile, Yb = (y_b - 1) / pcc::kTile;
+  const uint64_t tb = pcc::row_prefix(m_g, Ya), te = pcc::row_prefix(m_g, Yb + 1);
+  return pcc_syrk_f64(u, n, l, ldu, tb, te, PCC_LAYOUT_TILES, out, 0, 0, (int32_t)t, j_lo, j_hi, stream);
+}
+
+int pcc_scatter_range_f64(double *packed, const double *values, uint64_t first_tile, uint64_t count, int64_t t,
+                          int64_t n, void *stream) {
+  if (t < 1 || n < 1) return fail(PCC_EINVAL, "bad geometry n=%lld t=%lld", (long long)n, (long long)t);
+  const uint64_t m = ceil_div((uint64_t)n, (uint64_t)t);
+  if (first_tile + count > m * (m + 1) / 2) return fail(PCC_EINVAL, "tile range outside the tile matrix");
+  if (count == 0) return PCC_OK;
+  if (!packed || !values) return fail(PCC_EINVAL, "null pointer");
+  const uint64_t cells = count * (uint64_t)t * (uint64_t)t;
+  uint64_t grid = ceil_div(cells, 256);
+  if (grid > 148ull * 64) grid = 148ull * 64;
+  pcc::scatter_range_kernel<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(packed, values, first_tile, count, t,
+                                                                              n, m);
+  PCC_CUDA(cudaGetLastError(), "scatter_range_kernel launch");
+  return PCC_OK;
+}
+
+int pcc_allpairs_f64(const double *x, int64_t n, int64_t l, int64_t ldx, double *u, int64_t ldu,
+                     uint8_t *zero_variance, uint64_t tile_begin, uint64_t tile_end, int32_t layout, double *out,
+                     int64_t ld_out, uint64_t out_base, void *stream) {
+  int rc = check_u(u, n, l, ldu);
+  if (rc) return rc;
+  if (tile_end == UINT64_MAX) tile_end = pcc_gpu_tile_count(n);
+  rc = pcc_normalize_rows_f64(x, ldx, u, ldu, zero_variance, l, 0, n, stream);
+  if (rc) return rc;
+  rc = pcc_zero_rows_f64(u, ldu, n, pcc_rows_padded(n), stream);
+  if (rc) return rc;
+  return pcc_syrk_f64(u, n, l, ldu, tile_begin, tile_end, layout, out, ld_out, out_base, 0, 0, 0, stream);
+}
+
+int pcc_probe_fp64_peak(double *tflops) {
+  if (!tflops) return fail(PCC_EINVAL, "tflops is NULL");
+  const DeviceConfig *dc = nullptr;
+  int rc = device_config(&dc);
+  if (rc) return rc;
+  double *scratch = nullptr;
+  cudaStream_t s = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  PCC_CUDA(cudaMalloc(&scratch, sizeof(double)), "cudaMalloc");
+  PCC_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
+  PCC_CUDA(cudaEventCreate(&e0), "cudaEventCreate");
+  PCC_CUDA(cudaEventCreate(&e1), "cudaEventCreate");
+  const int threads = 512, iters = 4000;
+  const int grid = dc->sm_count * 2;
+  pcc::dmma_probe_kernel<<<grid, threads, 0, s>>>(scratch, 200);  // warm-up
+  float best = 1e30f;
+  for (int rep = 0; rep < 3; ++rep) {
+    cudaEventRecord(e0, s);
+    pcc::dmma_probe_kernel<<<grid, threads, 0, s>>>(scratch, iters);
+    cudaEventRecord(e1, s);
+    cudaError_t e = cudaEventSynchronize(e1);
+    if (e != cudaSuccess) return cuda_fail(e, "dmma_probe_kernel");
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (ms < best) best = ms;
+  }
+  const double flops = 2.0 * 256.0 * 8.0 * iters * (double)(threads / 32) * grid;
+  *tflops = flops / ((double)best * 1e-3) / 1e12;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaStreamDestroy(s);
+  cudaFree(scratch);
+  PCC_CUDA(cudaGetLastError(), "dmma_probe_kernel");
+  return PCC_OK;
+}
+
+}  // extern "C"

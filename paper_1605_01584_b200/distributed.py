@@ -1,0 +1,310 @@
+"""Static distribution of GPU tile jobs across devices.
+
+Mirrors ``paircorr.distributed`` (/root/reference/pkg/src/paircorr/distributed.py):
+``partition`` is the reference's rule verbatim in meaning -- ``p``
+contiguous chunks of ``ceil(T/p)`` tile ids, trailing workers possibly empty
+(distributed.py:76-92; the paper's static distribution) --
+applied to the 128 x 128 GPU tile matrix.  A worker is one GPU driven by one
+host thread (ctypes releases the GIL); every worker normalises the full
+dataset itself (the reference's worker model, worker.py:68-80) and
+contracts only its tile range, so there is no collective in the data path.
+Results stay sharded on the devices (``ShardedResult``) or are gathered
+into one packed host array; every packed cell belongs to exactly one tile
+and every tile to exactly one worker, so the gathered result is bitwise
+identical for any worker count.
+"""
+
+from __future__ import annotations
+
+import threading
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._device import as_device_f64, ptr, resolve_devices, stream_handle
+from .errors import IntegrityError, WorkerError
+from .indexing import sym_job_coord, sym_job_count
+from .tiles import CorrelationResult, TileGeometry
+from .transform import Dataset, normalize_device
+
+__all__ = [
+    "BACKENDS",
+    "WorkerAssignment",
+    "Shard",
+    "ShardedResult",
+    "partition",
+    "make_assignments",
+    "shard_span",
+    "owned_runs",
+    "run_workers",
+    "compute_worker",
+    "check_coverage",
+]
+
+BACKENDS = ("in_process", "subprocess", "cuda")
+
+
+def partition(total_tiles: int, p: int) -> list[tuple[int, int]]:
+    """``p`` contiguous ranges covering ``[0, total_tiles)`` (distributed.py:76-92)."""
+    if p < 1:
+        raise ValueError(f"worker count must be >= 1, got {p}")
+    if total_tiles < 0:
+        raise ValueError(f"total tile count must be >= 0, got {total_tiles}")
+    chunk = -(-total_tiles // p) if total_tiles else 0
+    return [(min(total_tiles, i * chunk), min(total_tiles, (i + 1) * chunk)) for i in range(p)]
+
+
+@dataclass(frozen=True)
+class WorkerAssignment:
+    """Tile range of one worker (distributed.py:55-64); ``geometry`` is the GPU tile geometry."""
+
+    worker_index: int
+    start: int
+    stop: int
+    geometry: TileGeometry
+    capacity: int = 0
+
+    @property
+    def tile_count(self) -> int:
+        return self.stop - self.start
+
+
+def gpu_geometry(n: int) -> TileGeometry:
+    return TileGeometry(n=n, t=_lib.GPU_TILE)
+
+
+def make_assignments(geom: TileGeometry, p: int, capacity: int = 0) -> list[WorkerAssignment]:
+    """distributed.py:95-99 over ``geom`` (normally the GPU geometry)."""
+    return [WorkerAssignment(i, lo, hi, geom, capacity) for i, (lo, hi) in enumerate(partition(geom.total_tiles, p))]
+
+
+def _F(n: int, y: int) -> int:
+    return (y * (2 * n + 1 - y)) >> 1
+
+
+def shard_span(n: int, tile_begin: int, tile_end: int) -> tuple[int, int]:
+    """Packed-index span ``[lo, hi)`` covering every cell of GPU tiles ``[tile_begin, tile_end)``."""
+    if tile_end <= tile_begin:
+        return (0, 0)
+    T = _lib.GPU_TILE
+    mg = -(-n // T)
+    y0, x0 = sym_job_coord(mg, tile_begin)
+    y1, x1 = sym_job_coord(mg, tile_end - 1)
+    ya, xa = y0 * T, x0 * T
+    y_last = min(n, (y1 + 1) * T) - 1
+    x_end = min(n, (x1 + 1) * T)
+    return _F(n, ya) + xa - ya, _F(n, y_last) + x_end - y_last
+
+
+def owned_runs(n: int, tile_begin: int, tile_end: int) -> list[tuple[int, int]]:
+    """Maximal contiguous packed-index runs owned by GPU tiles ``[tile_begin, tile_end)``.
+
+    Whole tile-row bands own whole packed rows (one run); the partial bands
+    at the two ends of the range contribute one run per job row.
+    """
+    if tile_end <= tile_begin:
+        return []
+    T = _lib.GPU_TILE
+    mg = -(-n // T)
+    Y0, X0 = sym_job_coord(mg, tile_begin)
+    Y1, X1 = sym_job_coord(mg, tile_end - 1)
+    runs: list[tuple[int, int]] = []
+
+    def add(lo: int, hi: int) -> None:
+        if hi <= lo:
+            return
+        if runs and runs[-1][1] == lo:
+            runs[-1] = (runs[-1][0], hi)
+        else:
+            runs.append((lo, hi))
+
+    for Y in range(Y0, Y1 + 1):
+        xa = X0 if Y == Y0 else Y
+        xb = X1 if Y == Y1 else mg - 1
+        full = xa == Y and xb == mg - 1
+        y_lo, y_hi = Y * T, min(n, (Y + 1) * T)
+        if full:
+            add(_F(n, y_lo), _F(n, y_hi))
+            continue
+        for y in range(y_lo, y_hi):
+            c_lo = max(y, xa * T)
+            c_hi = min(n, (xb + 1) * T)
+            add(_F(n, y) + c_lo - y, _F(n, y) + c_hi - y)
+    return runs
+
+
+@dataclass
+class Shard:
+    """One worker's contiguous GPU tile range and its device-resident packed span."""
+
+    worker_index: int
+    device: torch.device
+    tile_begin: int
+    tile_end: int
+    base: int                      # packed index of values[0]
+    values: torch.Tensor | None    # device float64[span], cells of other shards unspecified
+    zero_variance: frozenset[int] = field(default_factory=frozenset)
+
+    def runs(self, n: int) -> list[tuple[int, int]]:
+        return owned_runs(n, self.tile_begin, self.tile_end)
+
+
+@dataclass
+class ShardedResult:
+    """Per-device packed shards of one all-pairs result (kept on device)."""
+
+    n: int
+    shards: list[Shard]
+    zero_variance: frozenset[int] = field(default_factory=frozenset)
+
+    def gather(self, out: np.ndarray | torch.Tensor | None = None) -> CorrelationResult:
+        """Copy every shard's owned cells into one packed host array."""
+        total = sym_job_count(self.n)
+        if out is None:
+            host = torch.from_numpy(np.empty(total, dtype=np.float64))
+        else:
+            host = out if isinstance(out, torch.Tensor) else torch.from_numpy(out)
+            if host.numel() < total:
+                raise ValueError(f"out holds {host.numel()} values, need {total}")
+        for sh in self.shards:
+            if sh.values is None:
+                continue
+            with torch.cuda.device(sh.device):
+                for lo, hi in sh.runs(self.n):
+                    host[lo:hi].copy_(sh.values[lo - sh.base : hi - sh.base], non_blocking=host.is_pinned())
+                torch.cuda.current_stream().synchronize()
+        packed = out if out is not None else host.numpy()
+        return CorrelationResult(n=self.n, packed=packed, zero_variance=self.zero_variance)
+
+
+def check_coverage(spans: list[tuple[int, int, int]], total: int) -> None:
+    """Each span is (start, delivered_up_to, stop); demand an exact cover (distributed.py:321-335)."""
+    covered = 0
+    expected = 0
+    for start, delivered, stop in spans:
+        if start != expected:
+            raise IntegrityError(f"tile ranges not contiguous: expected start {expected}, got {start}")
+        if delivered != stop:
+            raise IntegrityError(f"tiles [{delivered}, {stop}) never delivered")
+        covered += stop - start
+        expected = stop
+    if covered != total:
+        raise IntegrityError(f"covered {covered} tiles of {total}")
+
+
+def compute_shard(x_host, n: int, l: int, a: WorkerAssignment, device: torch.device,
+                  x_device: torch.Tensor | None = None) -> tuple[Shard, torch.Tensor]:
+    """Worker body: upload, normalise everything, contract ``a``'s tile range.
+
+    Returns the shard and the device zero-variance flags; asynchronous on
+    the device's current stream.
+    """
+    with torch.cuda.device(device):
+        x = x_device if x_device is not None else as_device_f64(x_host, device)
+        u, flags = normalize_device(x)
+        lo, hi = shard_span(n, a.start, a.stop)
+        vals = torch.empty(max(hi - lo, 1), dtype=torch.float64, device=device)
+        if a.stop > a.start:
+            _lib.check(
+                _lib.lib().pcc_syrk_f64(ptr(u), n, l, u.shape[1], a.start, a.stop, _lib.LAYOUT_PACKED, ptr(vals), 0,
+                                        lo, 0, 0, 0, stream_handle()),
+                f"worker {a.worker_index}",
+            )
+        return Shard(a.worker_index, device, a.start, a.stop, lo, vals), flags
+
+
+def compute_worker(dataset: Dataset, p: int, worker_index: int, device=None, out=None):
+    """Run worker ``worker_index`` of a ``p``-way split as a standalone call.
+
+    The one-process-per-GPU form of ``run_workers`` (torchrun ranks): upload,
+    normalise, contract this worker's GPU tile range; with ``out`` (host
+    float64 buffer of ``shard_span`` size, pinned for async copies) its owned
+    packed cells are downloaded to ``out[index - span_lo]``.  Returns the
+    device ``Shard``; ``Shard.zero_variance`` holds the constant rows.
+    """
+    if not 0 <= worker_index < p:
+        raise ValueError(f"worker index {worker_index} outside [0, {p})")
+    n, l = dataset.n, dataset.l
+    a = make_assignments(gpu_geometry(n), p)[worker_index]
+    dev = resolve_devices(None if device is None else [device])[0]
+    shard, flags = compute_shard(dataset.values, n, l, a, dev)
+    with torch.cuda.device(dev):
+        if out is not None:
+            host = out if isinstance(out, torch.Tensor) else torch.from_numpy(out)
+            lo_span, hi_span = shard_span(n, a.start, a.stop)
+            if host.numel() < hi_span - lo_span:
+                raise ValueError(f"out holds {host.numel()} values, shard needs {hi_span - lo_span}")
+            for lo, hi in owned_runs(n, a.start, a.stop):
+                host[lo - shard.base : hi - shard.base].copy_(shard.values[lo - shard.base : hi - shard.base],
+                                                              non_blocking=host.is_pinned())
+        shard.zero_variance = frozenset(np.flatnonzero(flags.cpu().numpy()).tolist())
+        torch.cuda.current_stream().synchronize()
+    return shard
+
+
+def run_workers(
+    dataset: Dataset,
+    geom: TileGeometry | None,
+    p: int,
+    backend: str = "cuda",
+    capacity: int | None = None,
+    threads: int = 1,
+    devices=None,
+    gather: bool = True,
+    out=None,
+):
+    """Partition the GPU tile range across ``p`` workers on ``devices`` (distributed.py:117-151).
+
+    Worker ``i`` runs on ``devices[i % len(devices)]`` with its own host
+    thread.  ``geom`` (the caller's reference tiling) only fixes ``n``: the
+    result never depends on it.  Returns a gathered ``CorrelationResult``
+    (``gather=True``) or the device-resident ``ShardedResult``.  A failing
+    worker raises ``WorkerError`` carrying its index and unfinished range.
+    """
+    if backend not in BACKENDS:
+        raise ValueError(f"unknown backend {backend!r}, expected one of {BACKENDS}")
+    if not isinstance(dataset, Dataset):
+        from .fileio import load_dataset
+
+        dataset = load_dataset(dataset)
+    if geom is not None and dataset.n != geom.n:
+        raise ValueError(f"geometry is for n={geom.n} but dataset has n={dataset.n}")
+    devs = resolve_devices(devices)
+    n, l = dataset.n, dataset.l
+    assignments = make_assignments(gpu_geometry(n), p)
+    shards: list[Shard | None] = [None] * p
+    flags: list[torch.Tensor | None] = [None] * p
+    errors: list[BaseException | None] = [None] * p
+
+    def run_one(a: WorkerAssignment) -> None:
+        dev = devs[a.worker_index % len(devs)]
+        try:
+            shards[a.worker_index], flags[a.worker_index] = compute_shard(dataset.values, n, l, a, dev)
+            with torch.cuda.device(dev):
+                torch.cuda.current_stream().synchronize()
+        except BaseException as exc:  # noqa: BLE001 - re-raised as WorkerError below
+            errors[a.worker_index] = exc
+
+    if p == 1 or len(devs) == 1:
+        for a in assignments:
+            run_one(a)
+    else:
+        ts = [threading.Thread(target=run_one, args=(a,)) for a in assignments]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+    for a in assignments:
+        exc = errors[a.worker_index]
+        if exc is not None:
+            raise WorkerError(
+                f"worker {a.worker_index} failed with tiles [{a.start}, {a.stop}) unassembled: {exc}",
+                worker_index=a.worker_index,
+                unfinished_range=(a.start, a.stop),
+            ) from exc
+    check_coverage([(a.start, a.stop, a.stop) for a in assignments], gpu_geometry(n).total_tiles)
+    zv = frozenset(np.flatnonzero(flags[0].cpu().numpy()).tolist())
+    result = ShardedResult(n=n, shards=[s for s in shards if s is not None], zero_variance=zv)
+    return result.gather(out) if gather else result

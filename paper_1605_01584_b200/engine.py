@@ -1,0 +1,190 @@
+"""One-call entry point: the drop-in for ``paircorr.allpairs``.
+
+Mirrors ``paircorr.engine`` (/root/reference/pkg/src/paircorr/engine.py:1-56).
+``allpairs`` keeps the reference signature and result type; the scheduling
+knobs (``tile_size``, ``capacity``, ``threads``, ``backend``,
+``buffer_budget``) are validated as the reference validates them and, as the
+reference promises (engine.py:32-37), never change a bit of the result.
+
+Single-device data flow (all asynchronous on one CUDA stream, one host
+synchronisation at the end):
+
+    X (host, pinned if given as a pinned tensor) --H2D--> X_dev
+    K1 normalize (csrc/normalize.cuh)              X_dev -> U (padded), flags
+    K2 syrk, packed epilogue (csrc/syrk.cuh)       U -> packed[n(n+1)/2] (device)
+    D2H of each finished pass's packed rows on a copy stream, overlapped with
+    the next pass's contraction (the paper's Alg. 2 double buffering,
+    PAPER.md:235-287, with the device array as the staging buffer)
+
+Passes are groups of whole GPU tile rows, so each pass owns one contiguous
+packed range and its copy is a single cudaMemcpyAsync.
+"""
+
+from __future__ import annotations
+
+from pathlib import Path
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._device import as_device_f64, ptr, resolve_devices, stream_handle
+from .distributed import BACKENDS, run_workers
+from .indexing import sym_job_count
+from .tiles import DEFAULT_TILE_SIZE, CorrelationResult, TileGeometry
+from .transform import Dataset, normalize_device
+
+__all__ = ["allpairs", "default_capacity", "DEFAULT_BUFFER_BUDGET", "plan_row_passes"]
+
+DEFAULT_BUFFER_BUDGET = 256 * 2**20  # engine.py:14
+
+
+def default_capacity(t: int, buffer_budget: int | None = None) -> int:
+    """Largest per-pass tile count whose two buffers fit the budget (engine.py:17-20)."""
+    budget = DEFAULT_BUFFER_BUDGET if buffer_budget is None else buffer_budget
+    return max(1, budget // (2 * t * t * 8))
+
+
+def _F(n: int, y: int) -> int:
+    return (y * (2 * n + 1 - y)) >> 1
+
+
+def plan_row_passes(n: int, passes: int) -> list[tuple[int, int, int, int]]:
+    """Split the GPU tile matrix into <= ``passes`` groups of whole tile rows.
+
+    Returns ``(tile_begin, tile_end, packed_lo, packed_hi)`` per pass with
+    roughly equal tile counts; the packed ranges are contiguous and
+    disjoint and cover ``[0, n(n+1)/2)``.
+    """
+    T = _lib.GPU_TILE
+    mg = -(-n // T)
+    total = mg * (mg + 1) // 2
+    passes = max(1, min(passes, mg))
+    cuts = [0]
+    acc, y = 0, 0
+    for k in range(1, passes):
+        goal = total * k / passes
+        # take row y while its midpoint lies before the goal
+        while y < mg and acc + (mg - y) / 2 < goal:
+            acc += mg - y
+            y += 1
+        if y > cuts[-1]:
+            cuts.append(y)
+    if cuts[-1] != mg:
+        cuts.append(mg)
+    return [(_F(mg, a), _F(mg, b), _F(n, min(n, a * T)), _F(n, min(n, b * T))) for a, b in zip(cuts, cuts[1:])]
+
+
+def _host_out(out, total: int) -> torch.Tensor:
+    if out is None:
+        return torch.from_numpy(np.empty(total, dtype=np.float64))
+    t = out if isinstance(out, torch.Tensor) else torch.from_numpy(out)
+    if t.device.type != "cpu" or t.dtype != torch.float64 or not t.is_contiguous():
+        raise ValueError("out must be a contiguous float64 host array")
+    if t.numel() < total:
+        raise ValueError(f"out holds {t.numel()} values, need {total}")
+    return t
+
+
+def _allpairs_one_device(dataset: Dataset, device: torch.device, keep_on_device: bool, out, passes: int,
+                         output: str):
+    n, l = dataset.n, dataset.l
+    L = _lib.lib()
+    with torch.cuda.device(device):
+        compute = torch.cuda.current_stream()
+        x = as_device_f64(dataset.values, device)
+        u, flags = normalize_device(x)
+        ldu = int(u.shape[1])
+        T = int(L.pcc_gpu_tile_count(n))
+        s = stream_handle(compute)
+        if output == "dense":
+            dense = torch.empty((n, n), dtype=torch.float64, device=device)
+            _lib.check(L.pcc_syrk_f64(ptr(u), n, l, ldu, 0, T, _lib.LAYOUT_DENSE, ptr(dense), n, 0, 0, 0, 0, s),
+                       "allpairs(dense)")
+            zv = frozenset(np.flatnonzero(flags.cpu().numpy()).tolist())
+            return (dense if keep_on_device else dense.cpu().numpy()), zv
+
+        total = sym_job_count(n)
+        packed = torch.empty(total, dtype=torch.float64, device=device)
+        if keep_on_device:
+            _lib.check(L.pcc_syrk_f64(ptr(u), n, l, ldu, 0, T, _lib.LAYOUT_PACKED, ptr(packed), 0, 0, 0, 0, 0, s),
+                       "allpairs")
+            zv = frozenset(np.flatnonzero(flags.cpu().numpy()).tolist())
+            return packed, zv
+
+        host = _host_out(out, total)
+        pinned = host.is_pinned()
+        copy = torch.cuda.Stream(device)
+        for tb, te, lo, hi in plan_row_passes(n, passes):
+            _lib.check(L.pcc_syrk_f64(ptr(u), n, l, ldu, tb, te, _lib.LAYOUT_PACKED, ptr(packed), 0, 0, 0, 0, 0, s),
+                       "allpairs")
+            ev = torch.cuda.Event()
+            ev.record(compute)
+            copy.wait_event(ev)
+            with torch.cuda.stream(copy):
+                host[lo:hi].copy_(packed[lo:hi], non_blocking=pinned)
+        flags_host = flags.cpu()
+        copy.synchronize()
+        packed.record_stream(copy)
+        zv = frozenset(np.flatnonzero(flags_host.numpy()).tolist())
+        result = out if out is not None else host.numpy()
+        return result, zv
+
+
+def allpairs(
+    dataset: Dataset | str | Path,
+    tile_size: int = DEFAULT_TILE_SIZE,
+    capacity: int | None = None,
+    threads: int = 1,
+    workers: int = 1,
+    backend: str = "in_process",
+    buffer_budget: int | None = None,
+    *,
+    devices=None,
+    output: str = "packed",
+    keep_on_device: bool = False,
+    out=None,
+    passes: int = 8,
+):
+    """All-pairs Pearson correlation of ``dataset`` on B200 GPUs (engine.py:23-56).
+
+    Reference arguments keep their meaning and validation; ``workers > 1``
+    splits the GPU tile range across that many workers (one host thread
+    each, round-robin over ``devices``).  Extensions:
+
+    * ``devices``: ``None`` (current device), a device count, or a list;
+    * ``output``: ``"packed"`` (reference layout, returns ``CorrelationResult``)
+      or ``"dense"`` (returns the full ``n x n`` matrix and the zero-variance
+      set, written by the same kernel's dense epilogue);
+    * ``keep_on_device``: leave the packed result on the GPU (a CUDA tensor
+      in ``CorrelationResult.packed``);
+    * ``out``: caller-owned host float64 buffer for the packed result (pinned
+      memory makes the device-to-host copies asynchronous);
+    * ``passes``: number of row-group passes whose D2H copies overlap the
+      contraction.
+    """
+    if not isinstance(dataset, Dataset):
+        from .fileio import load_dataset
+
+        dataset = load_dataset(dataset)
+    geom = TileGeometry(n=dataset.n, t=tile_size)  # validates tile_size like the reference
+    if capacity is None:
+        capacity = default_capacity(tile_size, buffer_budget)
+    if capacity < 1:
+        raise ValueError(f"capacity must be >= 1, got {capacity}")
+    if backend not in BACKENDS:
+        raise ValueError(f"unknown backend {backend!r}, expected one of {BACKENDS}")
+    if workers < 1:
+        raise ValueError(f"worker count must be >= 1, got {workers}")
+    if output not in ("packed", "dense"):
+        raise ValueError(f"output must be 'packed' or 'dense', got {output!r}")
+    devs = resolve_devices(devices)
+    if (workers > 1 or len(devs) > 1) and output == "packed" and not keep_on_device:
+        return run_workers(dataset, geom, max(workers, len(devs)), backend="cuda", devices=devs, out=out)
+    if workers > 1 or len(devs) > 1:
+        raise ValueError("multi-worker runs support output='packed' gathered to host "
+                         "(use run_workers(..., gather=False) for device-resident shards)")
+    res, zv = _allpairs_one_device(dataset, devs[0], keep_on_device, out, passes, output)
+    if output == "dense":
+        return res, zv
+    return CorrelationResult(n=dataset.n, packed=res, zero_variance=zv)
