@@ -41,7 +41,7 @@ extern "C" {
 #define PCC_GPU_TILE 128
 /* U's row padding: ldu must be >= pcc_ldu(l) (multiple of PCC_K_ALIGN) and
  * U must have pcc_rows_padded(n) rows, the pad rows/columns zero. */
-#define PCC_K_ALIGN 16
+#define PCC_K_ALIGN 32
 
 /* Output layouts of pcc_syrk_f64. */
 #define PCC_LAYOUT_PACKED 0 /* upper triangle in job-id order: out[F(y)+x-y - out_base] (tiles.py:93-99) */
@@ -116,6 +116,15 @@ int pcc_zero_rows_f64(double *u, int64_t ldu, int64_t row_lo, int64_t row_hi, vo
 int pcc_syrk_f64(const double *u, int64_t n, int64_t l, int64_t ldu, uint64_t tile_begin,
                  uint64_t tile_end, int32_t layout, double *out, int64_t ld_out, uint64_t out_base,
                  int32_t ref_t, uint64_t ref_begin, uint64_t ref_end, void *stream);
+
+/* Same as pcc_syrk_f64 with an explicit contraction kernel shape (0 = the
+ * production default; 1..4 = the alternatives measured in DESIGN.md).  Every
+ * shape computes each cell with the same K order, so all variants produce
+ * bitwise identical results; this entry point exists for tuning. */
+int pcc_syrk_f64_variant(int32_t variant, const double *u, int64_t n, int64_t l, int64_t ldu,
+                         uint64_t tile_begin, uint64_t tile_end, int32_t layout, double *out,
+                         int64_t ld_out, uint64_t out_base, int32_t ref_t, uint64_t ref_begin,
+                         uint64_t ref_end, void *stream);
 
 /* Replaces _kernels.compute_tile_range(u, out, n, t, m, j_lo, j_hi, base)
  * (_kernels.py:351-373) with base = j_lo: fills out[0 .. (j_hi-j_lo)*t*t)

@@ -34,7 +34,7 @@ LIB_PATH = Path(__file__).resolve().parent / "lib" / "libpcc_b200.so"
 
 PCC_OK, PCC_EINVAL, PCC_ECUDA = 0, 1, 2
 GPU_TILE = 128
-K_ALIGN = 16
+K_ALIGN = 32
 LAYOUT_PACKED, LAYOUT_DENSE, LAYOUT_TILES = 0, 1, 2
 
 # Every symbol include/pcc_b200.h declares (tests check the .so exports them).
@@ -48,6 +48,7 @@ EXPORTED_SYMBOLS = (
     "pcc_normalize_rows_f64",
     "pcc_zero_rows_f64",
     "pcc_syrk_f64",
+    "pcc_syrk_f64_variant",
     "pcc_compute_pass_f64",
     "pcc_scatter_range_f64",
     "pcc_allpairs_f64",
@@ -87,6 +88,7 @@ def _bind(l: ctypes.CDLL) -> None:
         "pcc_normalize_rows_f64": (ctypes.c_int, [_vp, _i64, _vp, _i64, _vp, _i64, _i64, _i64, _vp]),
         "pcc_zero_rows_f64": (ctypes.c_int, [_vp, _i64, _i64, _i64, _vp]),
         "pcc_syrk_f64": (ctypes.c_int, [_vp, _i64, _i64, _i64, _u64, _u64, _i32, _vp, _i64, _u64, _i32, _u64, _u64, _vp]),
+        "pcc_syrk_f64_variant": (ctypes.c_int, [_i32, _vp, _i64, _i64, _i64, _u64, _u64, _i32, _vp, _i64, _u64, _i32, _u64, _u64, _vp]),
         "pcc_compute_pass_f64": (ctypes.c_int, [_vp, _i64, _i64, _i64, _i64, _u64, _u64, _vp, _vp]),
         "pcc_scatter_range_f64": (ctypes.c_int, [_vp, _vp, _u64, _u64, _i64, _i64, _vp]),
         "pcc_allpairs_f64": (ctypes.c_int, [_vp, _i64, _i64, _i64, _vp, _i64, _vp, _u64, _u64, _i32, _vp, _i64, _u64, _vp]),

@@ -41,6 +41,7 @@ struct DeviceConfig {
   int cc_major = 0, cc_minor = 0;
   int max_smem_optin = 0;
   int syrk_ctas_per_sm = 0;
+  int variant_ctas[16] = {0};
   size_t total_mem = 0;
 };
 
@@ -48,15 +49,89 @@ constexpr int kMaxDevices = 64;
 DeviceConfig g_dev[kMaxDevices];
 std::mutex g_dev_mu;
 
-template <int LAYOUT>
-int configure_syrk(int *ctas) {
-  PCC_CUDA(cudaFuncSetAttribute(pcc::syrk_kernel<LAYOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                pcc::kSyrkSmemBytes),
+// Contraction kernel shapes.  Variant 0 is the production default (TMA +
+// mbarrier ring); the others are kept for the measured comparison in
+// DESIGN.md (pcc_syrk_f64_variant) and only instantiated for the packed
+// layout.
+using V0 = pcc::SyrkCfg<2, 4, 8, 4, 16, 6>;  // TMA + mbarrier, 8 warps 64x32, BK 16 x 6 stages  (default)
+using V1 = pcc::SyrkCfg<2, 4, 8, 4, 16, 4>;  // cp.async + __syncthreads, 8 warps 64x32, BK 16 x 4
+using V2 = pcc::SyrkCfg<4, 4, 4, 4, 16, 4>;  // cp.async, 16 warps 32x32
+using V3 = pcc::SyrkCfg<2, 4, 8, 4, 32, 3>;  // cp.async, BK 32 x 3
+using V4 = pcc::SyrkCfg<4, 2, 4, 8, 16, 4>;  // cp.async, 8 warps 32x64
+using V5 = pcc::SyrkCfg<2, 4, 8, 4, 8, 12>;  // TMA, BK 8 x 12 stages
+using V6 = pcc::SyrkCfg<2, 4, 8, 4, 16, 7>;  // TMA, BK 16 x 7 stages
+using V7 = pcc::SyrkCfg<2, 4, 8, 4, 32, 3>;  // TMA, BK 32 x 3 stages
+using V8 = pcc::SyrkCfg<4, 2, 4, 8, 16, 6>;  // TMA, 8 warps 32x64
+constexpr int kNumVariants = 9;
+
+template <class C, int LAYOUT>
+int configure_tma_one(int *ctas) {
+  using TL = pcc::TmaLayout<C>;
+  PCC_CUDA(cudaFuncSetAttribute(pcc::syrk_tma_kernel<C, LAYOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                TL::kSmemBytes),
+           "cudaFuncSetAttribute(syrk_tma smem)");
+  PCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas, pcc::syrk_tma_kernel<C, LAYOUT>, TL::kThreads,
+                                                         TL::kSmemBytes),
+           "cudaOccupancyMaxActiveBlocksPerMultiprocessor(tma)");
+  return PCC_OK;
+}
+
+template <class C>
+int configure_tma_variant(int *ctas) {
+  int c0 = 0, c1 = 0, c2 = 0;
+  int rc = configure_tma_one<C, pcc::kLayoutPacked>(&c0);
+  if (rc == PCC_OK) rc = configure_tma_one<C, pcc::kLayoutDense>(&c1);
+  if (rc == PCC_OK) rc = configure_tma_one<C, pcc::kLayoutTiles>(&c2);
+  *ctas = c0 < c1 ? (c0 < c2 ? c0 : c2) : (c1 < c2 ? c1 : c2);
+  return rc;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+int encode_umap(const double *u, int64_t ldu, int64_t rows, CUtensorMap *map) {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  static cudaError_t once_err = cudaSuccess;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void *p = nullptr;
+    once_err = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q);
+    if (once_err == cudaSuccess && q == cudaDriverEntryPointSuccess) fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  if (fn == nullptr) return fail(PCC_ECUDA, "cuTensorMapEncodeTiled unavailable (%s)", cudaGetErrorString(once_err));
+  const cuuint64_t dims[2] = {(cuuint64_t)ldu, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)ldu * sizeof(double)};
+  const cuuint32_t box[2] = {(cuuint32_t)pcc::kSlab, (cuuint32_t)pcc::kTile};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(u), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(PCC_ECUDA, "cuTensorMapEncodeTiled failed (CUresult %d)", (int)r);
+  return PCC_OK;
+}
+
+template <class C, int LAYOUT>
+int configure_one(int *ctas) {
+  PCC_CUDA(cudaFuncSetAttribute(pcc::syrk_kernel<C, LAYOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                C::kSmemBytes),
            "cudaFuncSetAttribute(syrk smem)");
-  PCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas, pcc::syrk_kernel<LAYOUT>, pcc::kSyrkThreads,
-                                                         pcc::kSyrkSmemBytes),
+  PCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas, pcc::syrk_kernel<C, LAYOUT>, C::kThreads,
+                                                         C::kSmemBytes),
            "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
   return PCC_OK;
+}
+
+template <class C>
+int configure_variant(int *ctas) {
+  int c0 = 0, c1 = 0, c2 = 0;
+  int rc = configure_one<C, pcc::kLayoutPacked>(&c0);
+  if (rc == PCC_OK) rc = configure_one<C, pcc::kLayoutDense>(&c1);
+  if (rc == PCC_OK) rc = configure_one<C, pcc::kLayoutTiles>(&c2);
+  *ctas = c0 < c1 ? (c0 < c2 ? c0 : c2) : (c1 < c2 ? c1 : c2);
+  return rc;
 }
 
 // Per-device one-time setup (smem opt-in, occupancy); returns the config of
@@ -82,14 +157,20 @@ int device_config(const DeviceConfig **out, int device = -1) {
       return fail(PCC_ECUDA, "device %d is sm_%d%d; this library is built for sm_100a (B200) only", device,
                   p.major, p.minor);
     }
-    int c0 = 0, c1 = 0, c2 = 0;
-    int rc = configure_syrk<pcc::kLayoutPacked>(&c0);
-    if (rc == PCC_OK) rc = configure_syrk<pcc::kLayoutDense>(&c1);
-    if (rc == PCC_OK) rc = configure_syrk<pcc::kLayoutTiles>(&c2);
+    int rc = configure_tma_variant<V0>(&c.variant_ctas[0]);
+    if (rc == PCC_OK) rc = configure_one<V1, pcc::kLayoutPacked>(&c.variant_ctas[1]);
+    if (rc == PCC_OK) rc = configure_one<V2, pcc::kLayoutPacked>(&c.variant_ctas[2]);
+    if (rc == PCC_OK) rc = configure_one<V3, pcc::kLayoutPacked>(&c.variant_ctas[3]);
+    if (rc == PCC_OK) rc = configure_one<V4, pcc::kLayoutPacked>(&c.variant_ctas[4]);
+    if (rc == PCC_OK) rc = configure_tma_one<V5, pcc::kLayoutPacked>(&c.variant_ctas[5]);
+    if (rc == PCC_OK) rc = configure_tma_one<V6, pcc::kLayoutPacked>(&c.variant_ctas[6]);
+    if (rc == PCC_OK) rc = configure_tma_one<V7, pcc::kLayoutPacked>(&c.variant_ctas[7]);
+    if (rc == PCC_OK) rc = configure_tma_one<V8, pcc::kLayoutPacked>(&c.variant_ctas[8]);
     if (prev != device) cudaSetDevice(prev);
     if (rc != PCC_OK) return rc;
-    c.syrk_ctas_per_sm = c0 < c1 ? (c0 < c2 ? c0 : c2) : (c1 < c2 ? c1 : c2);
-    if (c.syrk_ctas_per_sm < 1) return fail(PCC_ECUDA, "contraction kernel cannot be resident on device %d", device);
+    c.syrk_ctas_per_sm = c.variant_ctas[0];
+    for (int v = 0; v < kNumVariants; ++v)
+      if (c.variant_ctas[v] < 1) return fail(PCC_ECUDA, "contraction variant %d cannot be resident on device %d", v, device);
     c.ready = true;
   }
   *out = &c;
@@ -108,22 +189,59 @@ int check_u(const double *u, int64_t n, int64_t l, int64_t ldu) {
   return PCC_OK;
 }
 
+template <class C, int LAYOUT>
+int launch_cfg(const double *u, int64_t n, int64_t l, int64_t ldu, uint64_t tb, uint64_t te, const pcc::Epilogue &ep,
+               cudaStream_t stream, int ctas_per_sm, int sm_count) {
+  const uint64_t m_g = ceil_div((uint64_t)n, pcc::kTile);
+  const int k_tiles = (int)ceil_div((uint64_t)l, C::BK);
+  const uint64_t resident = (uint64_t)sm_count * (uint64_t)ctas_per_sm;
+  const uint64_t tiles = te - tb;
+  const unsigned grid = (unsigned)(tiles < resident ? tiles : resident);
+  pcc::syrk_kernel<C, LAYOUT><<<grid, C::kThreads, C::kSmemBytes, stream>>>(u, n, ldu, k_tiles, m_g, tb, te, ep);
+  PCC_CUDA(cudaGetLastError(), "syrk_kernel launch");
+  return PCC_OK;
+}
+
+template <class C, int LAYOUT>
+int launch_tma_cfg(const double *u, int64_t n, int64_t l, int64_t ldu, uint64_t tb, uint64_t te,
+                   const pcc::Epilogue &ep, cudaStream_t stream, int ctas_per_sm, int sm_count) {
+  using TL = pcc::TmaLayout<C>;
+  CUtensorMap map;
+  int rc = encode_umap(u, ldu, pcc_rows_padded(n), &map);
+  if (rc) return rc;
+  const uint64_t m_g = ceil_div((uint64_t)n, pcc::kTile);
+  const int k_tiles = (int)ceil_div((uint64_t)l, C::BK);
+  const uint64_t resident = (uint64_t)sm_count * (uint64_t)ctas_per_sm;
+  const uint64_t tiles = te - tb;
+  const unsigned grid = (unsigned)(tiles < resident ? tiles : resident);
+  pcc::syrk_tma_kernel<C, LAYOUT><<<grid, TL::kThreads, TL::kSmemBytes, stream>>>(map, n, k_tiles, m_g, tb, te, ep);
+  PCC_CUDA(cudaGetLastError(), "syrk_tma_kernel launch");
+  return PCC_OK;
+}
+
 template <int LAYOUT>
 int launch_syrk(const double *u, int64_t n, int64_t l, int64_t ldu, uint64_t tb, uint64_t te,
-                const pcc::Epilogue &ep, cudaStream_t stream) {
+                const pcc::Epilogue &ep, cudaStream_t stream, int variant = 0) {
   if (te <= tb) return PCC_OK;
   const DeviceConfig *dc = nullptr;
   int rc = device_config(&dc);
   if (rc) return rc;
-  const uint64_t m_g = ceil_div((uint64_t)n, pcc::kTile);
-  const int k_tiles = (int)ceil_div((uint64_t)l, pcc::kBK);
-  const uint64_t resident = (uint64_t)dc->sm_count * (uint64_t)dc->syrk_ctas_per_sm;
-  const uint64_t tiles = te - tb;
-  const unsigned grid = (unsigned)(tiles < resident ? tiles : resident);
-  pcc::syrk_kernel<LAYOUT><<<grid, pcc::kSyrkThreads, pcc::kSyrkSmemBytes, stream>>>(u, n, ldu, k_tiles, m_g, tb,
-                                                                                      te, ep);
-  PCC_CUDA(cudaGetLastError(), "syrk_kernel launch");
-  return PCC_OK;
+  const int sms = dc->sm_count;
+  const int *vc = dc->variant_ctas;
+  if (variant == 0) return launch_tma_cfg<V0, LAYOUT>(u, n, l, ldu, tb, te, ep, stream, vc[0], sms);
+  if (LAYOUT != pcc::kLayoutPacked)
+    return fail(PCC_EINVAL, "contraction variant %d is only built for the packed layout", variant);
+  switch (variant) {
+    case 1: return launch_cfg<V1, pcc::kLayoutPacked>(u, n, l, ldu, tb, te, ep, stream, vc[1], sms);
+    case 2: return launch_cfg<V2, pcc::kLayoutPacked>(u, n, l, ldu, tb, te, ep, stream, vc[2], sms);
+    case 3: return launch_cfg<V3, pcc::kLayoutPacked>(u, n, l, ldu, tb, te, ep, stream, vc[3], sms);
+    case 4: return launch_cfg<V4, pcc::kLayoutPacked>(u, n, l, ldu, tb, te, ep, stream, vc[4], sms);
+    case 5: return launch_tma_cfg<V5, pcc::kLayoutPacked>(u, n, l, ldu, tb, te, ep, stream, vc[5], sms);
+    case 6: return launch_tma_cfg<V6, pcc::kLayoutPacked>(u, n, l, ldu, tb, te, ep, stream, vc[6], sms);
+    case 7: return launch_tma_cfg<V7, pcc::kLayoutPacked>(u, n, l, ldu, tb, te, ep, stream, vc[7], sms);
+    case 8: return launch_tma_cfg<V8, pcc::kLayoutPacked>(u, n, l, ldu, tb, te, ep, stream, vc[8], sms);
+    default: return fail(PCC_EINVAL, "unknown contraction variant %d (0..%d)", variant, kNumVariants - 1);
+  }
 }
 
 }  // namespace
@@ -159,7 +277,7 @@ int pcc_device_info(int device, pcc_device_info_t *info) {
   info->cc_minor = dc->cc_minor;
   info->max_smem_optin = dc->max_smem_optin;
   info->syrk_ctas_per_sm = dc->syrk_ctas_per_sm;
-  info->syrk_smem_bytes = pcc::kSyrkSmemBytes;
+  info->syrk_smem_bytes = pcc::TmaLayout<V0>::kSmemBytes;
   info->gpu_tile = pcc::kTile;
   info->total_mem = dc->total_mem;
   return PCC_OK;
@@ -195,6 +313,13 @@ int pcc_zero_rows_f64(double *u, int64_t ldu, int64_t row_lo, int64_t row_hi, vo
 int pcc_syrk_f64(const double *u, int64_t n, int64_t l, int64_t ldu, uint64_t tile_begin, uint64_t tile_end,
                  int32_t layout, double *out, int64_t ld_out, uint64_t out_base, int32_t ref_t, uint64_t ref_begin,
                  uint64_t ref_end, void *stream) {
+  return pcc_syrk_f64_variant(0, u, n, l, ldu, tile_begin, tile_end, layout, out, ld_out, out_base, ref_t, ref_begin,
+                              ref_end, stream);
+}
+
+int pcc_syrk_f64_variant(int32_t variant, const double *u, int64_t n, int64_t l, int64_t ldu, uint64_t tile_begin,
+                         uint64_t tile_end, int32_t layout, double *out, int64_t ld_out, uint64_t out_base,
+                         int32_t ref_t, uint64_t ref_begin, uint64_t ref_end, void *stream) {
   int rc = check_u(u, n, l, ldu);
   if (rc) return rc;
   const uint64_t total = pcc_gpu_tile_count(n);
@@ -206,10 +331,10 @@ int pcc_syrk_f64(const double *u, int64_t n, int64_t l, int64_t ldu, uint64_t ti
   cudaStream_t s = (cudaStream_t)stream;
   switch (layout) {
     case PCC_LAYOUT_PACKED:
-      return launch_syrk<pcc::kLayoutPacked>(u, n, l, ldu, tile_begin, tile_end, ep, s);
+      return launch_syrk<pcc::kLayoutPacked>(u, n, l, ldu, tile_begin, tile_end, ep, s, variant);
     case PCC_LAYOUT_DENSE:
       if (ld_out < n) return fail(PCC_EINVAL, "dense ld_out %lld < n %lld", (long long)ld_out, (long long)n);
-      return launch_syrk<pcc::kLayoutDense>(u, n, l, ldu, tile_begin, tile_end, ep, s);
+      return launch_syrk<pcc::kLayoutDense>(u, n, l, ldu, tile_begin, tile_end, ep, s, variant);
     case PCC_LAYOUT_TILES: {
       if (ref_t < 1) return fail(PCC_EINVAL, "tile size must be >= 1, got %d", ref_t);
       ep.ref_m = ceil_div((uint64_t)n, (uint64_t)ref_t);
@@ -217,7 +342,7 @@ int pcc_syrk_f64(const double *u, int64_t n, int64_t l, int64_t ldu, uint64_t ti
       if (ref_begin > ref_end || ref_end > ref_total)
         return fail(PCC_EINVAL, "tile range [%llu, %llu) invalid for %llu tiles", (unsigned long long)ref_begin,
                     (unsigned long long)ref_end, (unsigned long long)ref_total);
-      return launch_syrk<pcc::kLayoutTiles>(u, n, l, ldu, tile_begin, tile_end, ep, s);
+      return launch_syrk<pcc::kLayoutTiles>(u, n, l, ldu, tile_begin, tile_end, ep, s, variant);
     }
     default:
       return fail(PCC_EINVAL, "unknown layout %d", layout);

@@ -33,17 +33,28 @@
 
 namespace pcc {
 
-constexpr int kTile = 128;
-constexpr int kBK = 16;
-constexpr int kStages = 4;
-constexpr int kSyrkThreads = 256;
-constexpr int kSlab = 8;
-constexpr int kSlabsPerStage = kBK / kSlab;
-constexpr int kOperandDoubles = kSlabsPerStage * kTile * kSlab;  // 2048
-constexpr int kStageDoubles = 2 * kOperandDoubles;                // A + B
-constexpr int kSyrkSmemBytes = kStages * kStageDoubles * (int)sizeof(double);
+constexpr int kTile = 128;  // GPU tile edge (PCC_GPU_TILE)
+constexpr int kSlab = 8;    // doubles per smem row-slab (one DMMA k8 pair)
 
 enum : int { kLayoutPacked = 0, kLayoutDense = 1, kLayoutTiles = 2 };
+
+// Kernel shape: WARPS_M x WARPS_N warps, each owning MI x NI DMMA 8x8
+// accumulators (CTA tile 128 x 128), K staged BK doubles per stage through
+// a STAGES-deep cp.async ring.
+template <int WARPS_M_, int WARPS_N_, int MI_, int NI_, int BK_, int STAGES_>
+struct SyrkCfg {
+  static constexpr int WARPS_M = WARPS_M_, WARPS_N = WARPS_N_, MI = MI_, NI = NI_, BK = BK_, STAGES = STAGES_;
+  static constexpr int kThreads = 32 * WARPS_M * WARPS_N;
+  static constexpr int kSlabs = BK / kSlab;
+  static constexpr int kOpDoubles = kSlabs * kTile * kSlab;
+  static constexpr int kStageDoubles = 2 * kOpDoubles;
+  static constexpr int kSmemBytes = STAGES * kStageDoubles * (int)sizeof(double);
+  static constexpr int kChunksPerRow = BK / 2;                 // 16-byte chunks
+  static constexpr int kRowsPerPass = kThreads / kChunksPerRow;
+  static constexpr int kPasses = kTile / kRowsPerPass;
+  static_assert(WARPS_M * MI * 8 == kTile && WARPS_N * NI * 8 == kTile, "CTA tile must be 128 x 128");
+  static_assert(BK % kSlab == 0 && kThreads % kChunksPerRow == 0 && kTile % kRowsPerPass == 0, "bad shape");
+};
 
 struct Epilogue {
   double *out;
@@ -56,8 +67,8 @@ struct Epilogue {
 };
 
 template <int LAYOUT>
-__device__ __forceinline__ void store_cell(const Epilogue &ep, uint64_t n, uint64_t y, uint64_t x,
-                                           uint64_t packed_row_base, double v) {
+__device__ __forceinline__ void store_cell(const Epilogue &ep, uint64_t y, uint64_t x, uint64_t packed_row_base,
+                                           double v) {
   if (LAYOUT == kLayoutPacked) {
     ep.out[packed_row_base + x] = v;
   } else if (LAYOUT == kLayoutDense) {
@@ -72,23 +83,23 @@ __device__ __forceinline__ void store_cell(const Epilogue &ep, uint64_t n, uint6
   }
 }
 
-template <int LAYOUT>
-__global__ void __launch_bounds__(kSyrkThreads, 1)
+template <class C, int LAYOUT>
+__global__ void __launch_bounds__(C::kThreads, 1)
 syrk_kernel(const double *__restrict__ u, int64_t n, int64_t ldu, int k_tiles, uint64_t m_g,
             uint64_t tile_begin, uint64_t tile_end, Epilogue ep) {
   extern __shared__ __align__(128) double smem[];
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
-  const int wm = warp >> 2, wn = warp & 3;
+  const int wm = warp / C::WARPS_N, wn = warp % C::WARPS_N;
   const int g = lane >> 2, tig = lane & 3;
   const uint32_t smem_base = smem_u32(smem);
 
-  // Copy assignment: 2 x 1024 16-byte chunks per stage; thread tid owns
-  // chunk q = tid % 8 of rows tid/8 + 32 i (i < 4) for both operands.
-  const int cq = tid & 7;
-  const int crow = tid >> 3;
+  // Copy assignment: thread tid owns 16-byte chunk q = tid % (BK/2) of rows
+  // tid / (BK/2) + kRowsPerPass * i, for both operands.
+  const int cq = tid % C::kChunksPerRow;
+  const int crow = tid / C::kChunksPerRow;
   const uint32_t copy_soff =
-      (uint32_t)(((cq >> 2) * kTile * kSlab + crow * kSlab + (cq & 3) * 2) * sizeof(double));
+      (uint32_t)((((cq >> 2) * kTile + crow) * kSlab + (cq & 3) * 2) * sizeof(double));
 
   for (uint64_t J = tile_begin + blockIdx.x; J < tile_end; J += gridDim.x) {
     const uint64_t Y = tile_row(m_g, J);
@@ -97,56 +108,56 @@ syrk_kernel(const double *__restrict__ u, int64_t n, int64_t ldu, int k_tiles, u
     const double *gb = u + (int64_t)(X * kTile + crow) * ldu + cq * 2;
 
     auto load_stage = [&](int slot, int kt) {
-      const uint32_t s = smem_base + (uint32_t)(slot * kStageDoubles * sizeof(double)) + copy_soff;
-      const int64_t k0 = (int64_t)kt * kBK;
+      const uint32_t s = smem_base + (uint32_t)(slot * C::kStageDoubles * sizeof(double)) + copy_soff;
+      const int64_t k0 = (int64_t)kt * C::BK;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int64_t roff = (int64_t)(32 * i) * ldu + k0;
-        cp_async_16(s + (uint32_t)(32 * i * kSlab * sizeof(double)), ga + roff);
-        cp_async_16(s + (uint32_t)((kOperandDoubles + 32 * i * kSlab) * sizeof(double)), gb + roff);
+      for (int i = 0; i < C::kPasses; ++i) {
+        const int64_t roff = (int64_t)(C::kRowsPerPass * i) * ldu + k0;
+        const uint32_t so = (uint32_t)(C::kRowsPerPass * i * kSlab * sizeof(double));
+        cp_async_16(s + so, ga + roff);
+        cp_async_16(s + so + (uint32_t)(C::kOpDoubles * sizeof(double)), gb + roff);
       }
     };
 
-    double acc[8][4][2];
+    double acc[C::MI][C::NI][2];
 #pragma unroll
-    for (int mi = 0; mi < 8; ++mi)
+    for (int mi = 0; mi < C::MI; ++mi)
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+      for (int ni = 0; ni < C::NI; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
 
 #pragma unroll
-    for (int s = 0; s < kStages - 1; ++s) {
+    for (int s = 0; s < C::STAGES - 1; ++s) {
       if (s < k_tiles) load_stage(s, s);
       cp_async_commit();
     }
 
     for (int kt = 0; kt < k_tiles; ++kt) {
-      cp_async_wait<kStages - 2>();
+      cp_async_wait<C::STAGES - 2>();
       __syncthreads();
-      const int nk = kt + kStages - 1;
-      if (nk < k_tiles) load_stage(nk % kStages, nk);
+      const int nk = kt + C::STAGES - 1;
+      if (nk < k_tiles) load_stage(nk % C::STAGES, nk);
       cp_async_commit();
 
-      const double *sA = smem + (kt % kStages) * kStageDoubles;
-      const double *sB = sA + kOperandDoubles;
+      const double *sA = smem + (kt % C::STAGES) * C::kStageDoubles + (wm * C::MI * 8 + g) * kSlab + tig * 2;
+      const double *sB = smem + (kt % C::STAGES) * C::kStageDoubles + C::kOpDoubles + (wn * C::NI * 8 + g) * kSlab +
+                         tig * 2;
 #pragma unroll
-      for (int slab = 0; slab < kSlabsPerStage; ++slab) {
-        double2 a[8], b[4];
+      for (int slab = 0; slab < C::kSlabs; ++slab) {
+        double2 a[C::MI], b[C::NI];
 #pragma unroll
-        for (int mi = 0; mi < 8; ++mi)
-          a[mi] = *reinterpret_cast<const double2 *>(sA + slab * kTile * kSlab +
-                                                     (wm * 64 + mi * 8 + g) * kSlab + tig * 2);
+        for (int mi = 0; mi < C::MI; ++mi)
+          a[mi] = *reinterpret_cast<const double2 *>(sA + slab * kTile * kSlab + mi * 8 * kSlab);
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni)
-          b[ni] = *reinterpret_cast<const double2 *>(sB + slab * kTile * kSlab +
-                                                     (wn * 32 + ni * 8 + g) * kSlab + tig * 2);
+        for (int ni = 0; ni < C::NI; ++ni)
+          b[ni] = *reinterpret_cast<const double2 *>(sB + slab * kTile * kSlab + ni * 8 * kSlab);
 #pragma unroll
-        for (int mi = 0; mi < 8; ++mi)
+        for (int mi = 0; mi < C::MI; ++mi)
 #pragma unroll
-          for (int ni = 0; ni < 4; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], a[mi].x, b[ni].x);
+          for (int ni = 0; ni < C::NI; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], a[mi].x, b[ni].x);
 #pragma unroll
-        for (int mi = 0; mi < 8; ++mi)
+        for (int mi = 0; mi < C::MI; ++mi)
 #pragma unroll
-          for (int ni = 0; ni < 4; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], a[mi].y, b[ni].y);
+          for (int ni = 0; ni < C::NI; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], a[mi].y, b[ni].y);
       }
     }
     cp_async_wait<0>();
@@ -154,19 +165,177 @@ syrk_kernel(const double *__restrict__ u, int64_t n, int64_t ldu, int k_tiles, u
 
     // Fused epilogue: cells y <= x < n straight from the accumulators.
     const uint64_t un = (uint64_t)n;
-    const uint64_t y0 = Y * kTile + wm * 64 + g;
-    const uint64_t x0 = X * kTile + wn * 32 + 2 * tig;
+    const uint64_t y0 = Y * kTile + wm * C::MI * 8 + g;
+    const uint64_t x0 = X * kTile + wn * C::NI * 8 + 2 * tig;
 #pragma unroll
-    for (int mi = 0; mi < 8; ++mi) {
+    for (int mi = 0; mi < C::MI; ++mi) {
       const uint64_t y = y0 + mi * 8;
       if (y >= un) continue;
       const uint64_t prb = (LAYOUT == kLayoutPacked) ? row_prefix(un, y) - y - ep.out_base : 0;
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni) {
+      for (int ni = 0; ni < C::NI; ++ni) {
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const uint64_t x = x0 + ni * 8 + e;
-          if (x >= y && x < un) store_cell<LAYOUT>(ep, un, y, x, prb, acc[mi][ni][e]);
+          if (x >= y && x < un) store_cell<LAYOUT>(ep, y, x, prb, acc[mi][ni][e]);
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// TMA + mbarrier variant.  U's row bands stream into a STAGES-deep shared
+// ring with TMA (cp.async.bulk.tensor.2d: one 8-double x 128-row box per
+// operand slab, completion counted in bytes on the slot's "full" mbarrier).
+// Thread 0 doubles as the producer: before each K step it tops the ring up
+// to kAhead steps in front of its own warp (blocking only when the ring is
+// empty), following the CTA's tile sequence across tile boundaries, so the
+// next tile's first stages land while the epilogue runs.  Every warp waits
+// on "full", runs its DMMA slab(s) and releases the slot with one arrive on
+// the slot's "empty" mbarrier.  There is no block-wide barrier in the K
+// loop; warps drift within the ring's slack.
+template <class C>
+struct TmaLayout {
+  static constexpr int kBarOffset = C::kSmemBytes;  // 2 * STAGES mbarriers after the ring
+  static constexpr int kSmemBytes = C::kSmemBytes + 2 * C::STAGES * 8;
+  static constexpr int kThreads = C::kThreads;
+  static constexpr int kAhead = C::STAGES / 2;  // producer lead over warp 0, in K steps
+  static constexpr uint32_t kStageBytes = (uint32_t)(C::kStageDoubles * sizeof(double));
+  static constexpr uint32_t kSlabBytes = (uint32_t)(kTile * kSlab * sizeof(double));
+};
+
+template <class C, int LAYOUT>
+__global__ void __launch_bounds__(C::kThreads, 1)
+syrk_tma_kernel(const __grid_constant__ CUtensorMap umap, int64_t n, int k_tiles, uint64_t m_g, uint64_t tile_begin,
+                uint64_t tile_end, Epilogue ep) {
+  using TL = TmaLayout<C>;
+  extern __shared__ __align__(1024) double smem[];
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const uint32_t smem_base = smem_u32(smem);
+  const uint32_t full0 = smem_base + TL::kBarOffset;
+  const uint32_t empty0 = full0 + C::STAGES * 8;
+  constexpr int kWarps = C::WARPS_M * C::WARPS_N;
+
+  if (tid == 0) {
+    tma_prefetch_desc(&umap);
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, kWarps);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  // Producer cursor (meaningful in thread 0 only): next K step to load.
+  const uint64_t first = tile_begin + blockIdx.x;
+  const uint64_t my_tiles = first < tile_end ? (tile_end - first + gridDim.x - 1) / gridDim.x : 0;
+  const uint64_t total_steps = my_tiles * (uint64_t)k_tiles;
+  uint64_t p_step = 0;
+  int p_kt = 0, p_stage = 0;
+  uint32_t p_phase = 0;
+  uint64_t p_J = first;
+  int32_t p_ya = 0, p_xb = 0;
+  if (tid == 0 && my_tiles) {
+    const uint64_t Y = tile_row(m_g, p_J);
+    p_ya = (int32_t)(Y * kTile);
+    p_xb = (int32_t)((p_J + Y - row_prefix(m_g, Y)) * kTile);
+  }
+  // Issue loads while the cursor is less than `want` steps ahead; block on a
+  // busy slot only if the consumer would otherwise find the ring empty.
+  auto produce = [&](uint64_t c_step) {
+    while (p_step < total_steps && p_step < c_step + TL::kAhead) {
+      const uint32_t empty = empty0 + 8 * p_stage;
+      if (p_step > c_step) {
+        if (!mbar_try_wait(empty, p_phase ^ 1)) break;
+      } else {
+        mbar_wait(empty, p_phase ^ 1);
+      }
+      const uint32_t full = full0 + 8 * p_stage;
+      mbar_arrive_expect_tx(full, TL::kStageBytes);
+      const uint32_t dst = smem_base + (uint32_t)p_stage * TL::kStageBytes;
+#pragma unroll
+      for (int slab = 0; slab < C::kSlabs; ++slab) {
+        const int32_t k0 = p_kt * C::BK + slab * kSlab;
+        tma_load_2d(dst + slab * TL::kSlabBytes, &umap, k0, p_ya, full);
+        tma_load_2d(dst + (uint32_t)(C::kOpDoubles * sizeof(double)) + slab * TL::kSlabBytes, &umap, k0, p_xb, full);
+      }
+      ++p_step;
+      if (++p_stage == C::STAGES) {
+        p_stage = 0;
+        p_phase ^= 1;
+      }
+      if (++p_kt == k_tiles && p_step < total_steps) {
+        p_kt = 0;
+        p_J += gridDim.x;
+        const uint64_t Y = tile_row(m_g, p_J);
+        p_ya = (int32_t)(Y * kTile);
+        p_xb = (int32_t)((p_J + Y - row_prefix(m_g, Y)) * kTile);
+      }
+    }
+  };
+
+  const int wm = warp / C::WARPS_N, wn = warp % C::WARPS_N;
+  const int g = lane >> 2, tig = lane & 3;
+  uint64_t c_step = 0;
+  int stage = 0;
+  uint32_t phase = 0;
+  for (uint64_t J = first; J < tile_end; J += gridDim.x) {
+    const uint64_t Y = tile_row(m_g, J);
+    const uint64_t X = J + Y - row_prefix(m_g, Y);
+
+    double acc[C::MI][C::NI][2];
+#pragma unroll
+    for (int mi = 0; mi < C::MI; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < C::NI; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+
+    for (int kt = 0; kt < k_tiles; ++kt, ++c_step) {
+      if (tid == 0) produce(c_step);
+      mbar_wait(full0 + 8 * stage, phase);
+      const double *sA = smem + stage * C::kStageDoubles + (wm * C::MI * 8 + g) * kSlab + tig * 2;
+      const double *sB = smem + stage * C::kStageDoubles + C::kOpDoubles + (wn * C::NI * 8 + g) * kSlab + tig * 2;
+#pragma unroll
+      for (int slab = 0; slab < C::kSlabs; ++slab) {
+        double2 a[C::MI], b[C::NI];
+#pragma unroll
+        for (int mi = 0; mi < C::MI; ++mi)
+          a[mi] = *reinterpret_cast<const double2 *>(sA + slab * kTile * kSlab + mi * 8 * kSlab);
+#pragma unroll
+        for (int ni = 0; ni < C::NI; ++ni)
+          b[ni] = *reinterpret_cast<const double2 *>(sB + slab * kTile * kSlab + ni * 8 * kSlab);
+#pragma unroll
+        for (int mi = 0; mi < C::MI; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < C::NI; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], a[mi].x, b[ni].x);
+#pragma unroll
+        for (int mi = 0; mi < C::MI; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < C::NI; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], a[mi].y, b[ni].y);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty0 + 8 * stage);
+      if (++stage == C::STAGES) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+
+    const uint64_t un = (uint64_t)n;
+    const uint64_t y0 = Y * kTile + wm * C::MI * 8 + g;
+    const uint64_t x0 = X * kTile + wn * C::NI * 8 + 2 * tig;
+#pragma unroll
+    for (int mi = 0; mi < C::MI; ++mi) {
+      const uint64_t y = y0 + mi * 8;
+      if (y >= un) continue;
+      const uint64_t prb = (LAYOUT == kLayoutPacked) ? row_prefix(un, y) - y - ep.out_base : 0;
+#pragma unroll
+      for (int ni = 0; ni < C::NI; ++ni) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const uint64_t x = x0 + ni * 8 + e;
+          if (x >= y && x < un) store_cell<LAYOUT>(ep, y, x, prb, acc[mi][ni][e]);
         }
       }
     }

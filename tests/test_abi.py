@@ -1,0 +1,78 @@
+"""The C-ABI library (libpcc_b200.so) loads without a GPU, exports exactly what
+include/pcc_b200.h declares, its pure helpers compute the documented
+geometry, device entry points fail loudly (status + message) when no GPU is
+present, and the shipped SASS uses the FP64 tensor pipe."""
+
+import ctypes
+import re
+import shutil
+import subprocess
+
+import pytest
+import torch
+
+from paper_1605_01584_b200 import _lib
+
+from conftest import ROOT
+
+HEADER = ROOT / "include" / "pcc_b200.h"
+
+
+def header_symbols():
+    text = HEADER.read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return set(re.findall(r"\b(pcc_[a-z0-9_]+)\s*\(", text))
+
+
+def test_header_and_binding_agree():
+    assert header_symbols() == set(_lib.EXPORTED_SYMBOLS)
+
+
+def test_library_exports_every_declared_symbol():
+    lib = ctypes.CDLL(str(_lib.LIB_PATH))
+    for name in header_symbols():
+        assert hasattr(lib, name), name
+    out = subprocess.run(["nm", "-D", "--defined-only", str(_lib.LIB_PATH)], capture_output=True, text=True)
+    if out.returncode == 0:
+        exported = set(re.findall(r"\b(pcc_[a-z0-9_]+)\b", out.stdout))
+        assert header_symbols() <= exported
+
+
+def test_pure_helpers():
+    L = _lib.lib()
+    assert L.pcc_version() >= 100
+    assert L.pcc_ldu(1) == 32 and L.pcc_ldu(32) == 32 and L.pcc_ldu(33) == 64 and L.pcc_ldu(1531) == 1536
+    assert L.pcc_rows_padded(1) == 128 and L.pcc_rows_padded(128) == 128 and L.pcc_rows_padded(10007) == 10112
+    for n, T in [(1, 1), (128, 1), (129, 3), (2000, 136), (16384, 8256), (10007, 3160), (32768, 32896),
+                 (65536, 131328)]:
+        assert L.pcc_gpu_tile_count(n) == T  # T at T_g=128
+
+
+def test_invalid_arguments_rejected_before_any_device_work():
+    L = _lib.lib()
+    with pytest.raises(ValueError, match="samples"):
+        _lib.check(L.pcc_normalize_rows_f64(None, 1, None, 1, None, 1, 0, 1, None))
+    with pytest.raises(ValueError, match="ldu"):
+        _lib.check(L.pcc_syrk_f64(None, 10, 17, 16, 0, 1, 0, None, 0, 0, 0, 0, 0, None))
+    with pytest.raises(ValueError, match="n must be"):
+        _lib.check(L.pcc_syrk_f64(None, 0, 17, 32, 0, 1, 0, None, 0, 0, 0, 0, 0, None))
+    with pytest.raises(ValueError, match="tile size"):
+        _lib.check(L.pcc_compute_pass_f64(ctypes.c_void_p(16), 10, 5, 16, 0, 0, 1, None, None))
+    assert L.pcc_last_error()
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU failure mode")
+def test_device_calls_fail_loudly_without_gpu():
+    info = _lib.DeviceInfo()
+    rc = _lib.lib().pcc_device_info(0, ctypes.byref(info))
+    assert rc != 0 and _lib.lib().pcc_last_error()
+
+
+@pytest.mark.skipif(shutil.which("cuobjdump") is None and not shutil.os.path.exists("/usr/local/cuda/bin/cuobjdump"),
+                    reason="no cuobjdump")
+def test_sass_is_sm100a_and_uses_dmma():
+    exe = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    sass = subprocess.run([exe, "-sass", str(_lib.LIB_PATH)], capture_output=True, text=True).stdout
+    assert "sm_100a" in sass
+    assert "DMMA.8x8x4" in sass          # FP64 tensor pipe in the contraction
+    assert "LDGSTS" in sass              # cp.async operand staging

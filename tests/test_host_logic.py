@@ -1,0 +1,291 @@
+"""Host-side logic of the drop-in (no GPU): bijection, geometry, partition,
+pass planning, shard ownership, host scatter, result/file containers and
+the loud-failure contract."""
+
+import json
+import math
+
+import numpy as np
+import pytest
+import torch
+from hypothesis import given, settings
+from hypothesis import strategies as st
+
+import oracle
+import paper_1605_01584_b200 as pc
+from paper_1605_01584_b200.distributed import owned_runs, partition, shard_span
+from paper_1605_01584_b200.engine import plan_row_passes
+from paper_1605_01584_b200.tiles import _scatter_host
+
+from conftest import GOLDEN, random_values, triangle_walk
+
+
+# --- bijection (indexing.py) ------------------------------------------------
+
+def test_row_prefix_and_examples():
+    assert pc.row_prefix(4, 0) == 0 and pc.row_prefix(4, 4) == 10 and pc.row_prefix(4, 2) == 7
+    assert pc.sym_job_id(4, 0, 0) == 0 and pc.sym_job_id(4, 1, 2) == 5 and pc.sym_job_id(4, 3, 3) == 9
+    assert pc.sym_job_coord(4, 5) == pc.Coord(1, 2)
+    assert pc.nonsym_job_id(4, 1, 2) == 6 and pc.nonsym_job_coord(4, 15) == pc.Coord(3, 3)
+    for bad in [(4, -1), (4, 5), (0, 0)]:
+        with pytest.raises(ValueError):
+            pc.row_prefix(*bad)
+    with pytest.raises(ValueError):
+        pc.sym_job_id(4, 2, 1)
+    with pytest.raises(ValueError):
+        pc.sym_job_coord(4, 10)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 7, 16, 33, 64])
+def test_bijection_exhaustive(n):
+    walk = triangle_walk(n)
+    for j, (y, x) in enumerate(walk):
+        assert pc.sym_job_id(n, y, x) == j
+        assert tuple(pc.sym_job_coord(n, j)) == (y, x)
+    ys, xs = pc.sym_job_coords(n, np.arange(len(walk), dtype=np.uint64))
+    assert [(int(a), int(b)) for a, b in zip(ys, xs)] == walk
+    assert np.array_equal(pc.sym_job_ids(n, ys, xs), np.arange(len(walk), dtype=np.uint64))
+
+
+def test_bijection_matches_reference_golden_at_scale():
+    z = np.load(GOLDEN / "bijection.npz")
+    for n in (10**4, 10**5, 10**6, 2**31 + 7, 2**32 - 1):
+        ids, y, x = z[f"n{n}/ids"], z[f"n{n}/y"], z[f"n{n}/x"]
+        gy, gx = pc.sym_job_coords(n, ids)
+        assert np.array_equal(gy, y) and np.array_equal(gx, x)
+        for j, yy, xx in list(zip(ids, y, x))[:200]:
+            assert tuple(pc.sym_job_coord(n, int(j))) == (int(yy), int(xx))
+    for m, j, y in z["tile_row"]:
+        assert pc.sym_job_coord(int(m), int(j)).y == int(y)
+
+
+def _row_bisect(n, j):
+    lo, hi = 0, n - 1
+    while lo < hi:
+        mid = (lo + hi + 1) // 2
+        if pc.row_prefix(n, mid) <= j:
+            lo = mid
+        else:
+            hi = mid - 1
+    return lo
+
+
+@given(st.integers(1, 2**20), st.data())
+@settings(max_examples=300, deadline=None)
+def test_bijection_roundtrip_property(n, data):
+    j = data.draw(st.integers(0, n * (n + 1) // 2 - 1))
+    y, x = pc.sym_job_coord(n, j)
+    assert y == _row_bisect(n, j) and y <= x < n
+    assert pc.sym_job_id(n, y, x) == j
+
+
+def test_max_n_boundaries():
+    n = pc.MAX_N
+    total = pc.sym_job_count(n)
+    assert total == n * (n + 1) // 2 < 2**64
+    assert pc.sym_job_coord(n, total - 1) == pc.Coord(n - 1, n - 1)
+    assert pc.sym_job_coord(n, 0) == pc.Coord(0, 0)
+    with pytest.raises(ValueError):
+        pc.sym_job_count(n + 1)
+
+
+# --- geometry, partition, passes ---------------------------------------------
+
+@pytest.mark.parametrize("n,t,m", [(1, 1, 1), (2, 2, 1), (3, 2, 2), (4, 2, 2), (5, 2, 3), (128, 4, 32), (10, 3, 4)])
+def test_geometry(n, t, m):
+    g = pc.TileGeometry(n=n, t=t)
+    assert g.m == m and g.total_tiles == m * (m + 1) // 2 and g.job_count == n * (n + 1) // 2
+    with pytest.raises(ValueError):
+        pc.TileGeometry(n=0, t=2)
+    with pytest.raises(ValueError):
+        pc.TileGeometry(n=4, t=0)
+
+
+def test_partition_matches_reference_golden():
+    ref = json.loads((GOLDEN / "partition.json").read_text())
+    for key, ranges in ref.items():
+        T, p = map(int, key.split(","))
+        assert [list(r) for r in partition(T, p)] == ranges
+    with pytest.raises(ValueError):
+        partition(5, 0)
+    with pytest.raises(ValueError):
+        partition(-1, 2)
+
+
+def test_plan_passes():
+    plan = pc.plan_passes(3, 20, 5)
+    assert plan.passes == ((3, 8), (8, 13), (13, 18), (18, 20)) and plan.total == 17
+    assert pc.plan_passes(4, 4, 3).passes == ()
+    with pytest.raises(ValueError):
+        pc.plan_passes(0, 5, 0)
+    with pytest.raises(ValueError):
+        pc.plan_passes(5, 4, 1)
+
+
+@pytest.mark.parametrize("n", [1, 127, 128, 129, 2000, 10007, 16384, 65536])
+@pytest.mark.parametrize("passes", [1, 3, 8, 64])
+def test_row_passes_cover_packed_and_tiles(n, passes):
+    ps = plan_row_passes(n, passes)
+    mg = -(-n // 128)
+    assert ps[0][0] == 0 and ps[-1][1] == mg * (mg + 1) // 2
+    assert ps[0][2] == 0 and ps[-1][3] == n * (n + 1) // 2
+    for a, b in zip(ps, ps[1:]):
+        assert a[1] == b[0] and a[3] == b[2]
+    assert all(p[1] > p[0] and p[3] > p[2] for p in ps)
+
+
+@pytest.mark.parametrize("n", [1, 5, 128, 129, 300, 1000])
+@pytest.mark.parametrize("p", [1, 2, 3, 7])
+def test_owned_runs_partition_the_packed_triangle(n, p):
+    mg = -(-n // 128)
+    T = mg * (mg + 1) // 2
+    total = n * (n + 1) // 2
+    cover = np.zeros(total, dtype=np.int32)
+    for lo_t, hi_t in partition(T, p):
+        span = shard_span(n, lo_t, hi_t)
+        for lo, hi in owned_runs(n, lo_t, hi_t):
+            assert span[0] <= lo < hi <= span[1]
+            cover[lo:hi] += 1
+    assert (cover == 1).all()
+
+
+def test_owned_runs_equal_cell_enumeration():
+    n = 300  # 3 GPU tile rows, 6 tiles
+    mg = 3
+    for tb in range(6):
+        for te in range(tb + 1, 7):
+            expect = set()
+            for J in range(tb, te):
+                Y, X = pc.sym_job_coord(mg, J)
+                for y in range(Y * 128, min(n, Y * 128 + 128)):
+                    for x in range(max(y, X * 128), min(n, X * 128 + 128)):
+                        expect.add(pc.sym_job_id(n, y, x))
+            got = set()
+            for lo, hi in owned_runs(n, tb, te):
+                got.update(range(lo, hi))
+            assert got == expect, (tb, te)
+
+
+# --- results, scatter, containers -------------------------------------------
+
+def test_host_scatter_matches_oracle(rng):
+    x = random_values(rng, 23, 7, special_rows=True)
+    u, _ = oracle.normalize(x)
+    for t in (1, 2, 3, 4, 8):
+        g = pc.TileGeometry(n=23, t=t)
+        flat = oracle.compute_pass(u, t, 0, g.total_tiles)
+        ref = np.full(g.job_count, np.nan)
+        oracle.scatter_range(ref, flat, 0, g.total_tiles, g.m, t, 23)
+        got = np.full(g.job_count, np.nan)
+        _scatter_host(got, flat, 0, g.total_tiles, g)
+        assert np.array_equal(got, ref, equal_nan=True)
+        # pass-by-pass through the public scatter_pass, with per-block fallback
+        res = pc.empty_result(23)
+        cut = g.total_tiles // 2
+        blocks = pc.BlockList(pc.TileBlock(j, flat[j * t * t:(j + 1) * t * t]) for j in range(cut))
+        pc.scatter(blocks, g, res)
+        b2 = pc.BlockList(pc.TileBlock(j, flat[j * t * t:(j + 1) * t * t]) for j in range(cut, g.total_tiles))
+        b2.flat = flat[cut * t * t:]
+        pc.scatter_pass(b2, g, res)
+        assert np.array_equal(res.packed, ref)
+
+
+def test_scatter_errors():
+    g = pc.TileGeometry(n=4, t=2)
+    res = pc.empty_result(4)
+    blk = pc.TileBlock(0, np.zeros(4))
+    with pytest.raises(pc.IntegrityError):
+        pc.scatter([blk, pc.TileBlock(0, np.zeros(4))], g, res)
+    with pytest.raises(ValueError):
+        pc.scatter([pc.TileBlock(3, np.zeros(4))], g, res)
+    with pytest.raises(ValueError):
+        pc.scatter([pc.TileBlock(0, np.zeros(3))], g, res)
+
+
+def test_correlation_result_get_and_dense():
+    packed = np.arange(10, dtype=np.float64)
+    r = pc.CorrelationResult(n=4, packed=packed)
+    assert r.get(1, 2) == r.get(2, 1) == 5.0
+    d = r.to_dense()
+    assert np.array_equal(d, d.T) and d[3, 3] == 9.0
+    with pytest.raises(ValueError):
+        r.get(0, 4)
+    with pytest.raises(ValueError):
+        r.get(-1, 0)
+
+
+def test_dataset_validation():
+    with pytest.raises(pc.DataError):
+        pc.Dataset(values=np.array([[np.nan, 1.0]]))
+    with pytest.raises(pc.DataError):
+        pc.Dataset(values=np.array([[np.inf, 1.0], [0.0, 2.0]]))
+    with pytest.raises(pc.DataError):
+        pc.Dataset(values=np.array([[1.0]]))
+    with pytest.raises(pc.DataError):
+        pc.Dataset(values=np.zeros((0, 5)))
+    with pytest.raises(pc.DataError):
+        pc.Dataset(values=np.zeros((2, 3)), ids=["only-one"])
+    with pytest.raises(pc.DataError):
+        pc.Dataset(values=np.zeros(3))
+    with pytest.raises(pc.DataError):
+        pc.Dataset(values=torch.tensor([[1.0, float("nan")]]))
+    d = pc.Dataset(values=[[1, 2, 3]])
+    assert d.values.dtype == np.float64 and d.n == 1 and d.l == 3
+
+
+def test_estimate_cost():
+    assert pc.estimate_cost(1, 1) == 6 and pc.estimate_cost(2, 10) == 130
+    for n, l in [(10**6, 999_983), (12345, 678)]:
+        assert pc.estimate_cost(n, l) == (10 * l * n + l * n * (n + 1)) // 2
+    with pytest.raises(ValueError):
+        pc.estimate_cost(0, 5)
+
+
+def test_file_roundtrip(tmp_path, rng):
+    x = random_values(rng, 9, 5)
+    pc.save_dataset(tmp_path / "d.lpcc", pc.Dataset(values=x))
+    assert np.array_equal(pc.load_dataset(tmp_path / "d.lpcc").values, x)
+    packed, zv = oracle.allpairs(x)
+    r = pc.CorrelationResult(n=9, packed=packed, zero_variance=frozenset({2, 5}))
+    pc.save_result(tmp_path / "r.lpcr", r)
+    back = pc.load_result(tmp_path / "r.lpcr")
+    assert np.array_equal(back.packed, packed) and back.zero_variance == {2, 5}
+    for i, j in [(0, 0), (3, 7), (8, 1)]:
+        assert pc.query_pair(tmp_path / "r.lpcr", i, j) == r.get(i, j)
+    (tmp_path / "bad.lpcc").write_bytes(b"XXXX" + bytes(20))
+    with pytest.raises(pc.DataError):
+        pc.load_dataset(tmp_path / "bad.lpcc")
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU failure mode")
+def test_no_cpu_fallback_without_gpu():
+    d = pc.Dataset(values=np.array([[1.0, 2.0, 3.0], [3.0, 1.0, 2.0]]))
+    with pytest.raises(pc.DeviceError):
+        pc.allpairs(d)
+    with pytest.raises(pc.DeviceError):
+        pc.normalize(d)
+
+
+def test_workloads_shapes_and_determinism():
+    from paper_1605_01584_b200.workloads import gen_uniform_splitmix64, make_config
+
+    a = make_config("c3", n=500, l=40)
+    b = make_config("c3", n=500, l=40)
+    assert np.array_equal(a, b) and a.shape == (500, 40)
+    const = [i for i in range(500) if (a[i] == a[i, 0]).all()]
+    assert len(const) == 5
+    c5 = make_config("c5", n=1024, l=64)
+    assert c5.shape == (1024, 64)
+    # splitmix64 known answers: element k = mix(seed + (k+1) * golden) >> 11 * 2^-53
+    def mix(v):
+        v &= 2**64 - 1
+        v = (v ^ (v >> 30)) * 0xBF58476D1CE4E5B9 % 2**64
+        v = (v ^ (v >> 27)) * 0x94D049BB133111EB % 2**64
+        v = v ^ (v >> 31)
+        return (v >> 11) * 2.0**-53
+    assert gen_uniform_splitmix64(1, 2, seed=0)[0].tolist() == [mix(0x9E3779B97F4A7C15), mix(2 * 0x9E3779B97F4A7C15)]
+    assert np.array_equal(gen_uniform_splitmix64(2, 6, seed=9).ravel(), gen_uniform_splitmix64(1, 12, seed=9).ravel())
+    u = gen_uniform_splitmix64(3, 4, seed=0)
+    assert u.shape == (3, 4) and (0 <= u).all() and (u < 1).all()
+    assert math.isclose(float(gen_uniform_splitmix64(1, 1, seed=0)[0, 0]),
+                        float(gen_uniform_splitmix64(2, 2, seed=0)[0, 0]))
