@@ -27,6 +27,7 @@ from ._device import as_device_f64, ptr, resolve_devices, stream_handle
 from .errors import IntegrityError, WorkerError
 from .indexing import sym_job_coord, sym_job_count
 from .tiles import CorrelationResult, TileGeometry
+from .stream import run_stream
 from .transform import Dataset, normalize_device
 
 __all__ = [
@@ -215,6 +216,21 @@ def compute_shard(x_host, n: int, l: int, a: WorkerAssignment, device: torch.dev
         return Shard(a.worker_index, device, a.start, a.stop, lo, vals), flags
 
 
+def stream_shard(x_host, n: int, l: int, a: WorkerAssignment, device: torch.device, host_out=None):
+    """Worker body with overlapped upload / contraction / download (stream.run_stream).
+
+    Uploads and normalises only the rows the range touches (>= its first
+    tile row); ``host_out`` (span-sized, pinned for async copies) receives
+    the shard's packed span.  Returns the shard and the device flags, valid
+    for rows ``[row_lo, n)`` (worker 0 covers every row).
+    """
+    lo, hi = shard_span(n, a.start, a.stop)
+    with torch.cuda.device(device):
+        vals = torch.empty(max(hi - lo, 1), dtype=torch.float64, device=device)
+        _, flags, _ = run_stream(x_host, n, l, device, a.start, a.stop, vals, lo, host_out, lo)
+    return Shard(a.worker_index, device, a.start, a.stop, lo, vals), flags
+
+
 def compute_worker(dataset: Dataset, p: int, worker_index: int, device=None, out=None):
     """Run worker ``worker_index`` of a ``p``-way split as a standalone call.
 
@@ -229,18 +245,14 @@ def compute_worker(dataset: Dataset, p: int, worker_index: int, device=None, out
     n, l = dataset.n, dataset.l
     a = make_assignments(gpu_geometry(n), p)[worker_index]
     dev = resolve_devices(None if device is None else [device])[0]
-    shard, flags = compute_shard(dataset.values, n, l, a, dev)
-    with torch.cuda.device(dev):
-        if out is not None:
-            host = out if isinstance(out, torch.Tensor) else torch.from_numpy(out)
-            lo_span, hi_span = shard_span(n, a.start, a.stop)
-            if host.numel() < hi_span - lo_span:
-                raise ValueError(f"out holds {host.numel()} values, shard needs {hi_span - lo_span}")
-            for lo, hi in owned_runs(n, a.start, a.stop):
-                host[lo - shard.base : hi - shard.base].copy_(shard.values[lo - shard.base : hi - shard.base],
-                                                              non_blocking=host.is_pinned())
-        shard.zero_variance = frozenset(np.flatnonzero(flags.cpu().numpy()).tolist())
-        torch.cuda.current_stream().synchronize()
+    host = None
+    if out is not None:
+        host = out if isinstance(out, torch.Tensor) else torch.from_numpy(out)
+        lo_span, hi_span = shard_span(n, a.start, a.stop)
+        if host.numel() < hi_span - lo_span:
+            raise ValueError(f"out holds {host.numel()} values, shard needs {hi_span - lo_span}")
+    shard, flags = stream_shard(dataset.values, n, l, a, dev, host)
+    shard.zero_variance = frozenset(np.flatnonzero(flags.cpu().numpy()).tolist())
     return shard
 
 

@@ -6,18 +6,16 @@ knobs (``tile_size``, ``capacity``, ``threads``, ``backend``,
 ``buffer_budget``) are validated as the reference validates them and, as the
 reference promises (engine.py:32-37), never change a bit of the result.
 
-Single-device data flow (all asynchronous on one CUDA stream, one host
-synchronisation at the end):
+Single-device data flow (stream.py; one host synchronisation at the end):
 
-    X (host, pinned if given as a pinned tensor) --H2D--> X_dev
-    K1 normalize (csrc/normalize.cuh)              X_dev -> U (padded), flags
-    K2 syrk, packed epilogue (csrc/syrk.cuh)       U -> packed[n(n+1)/2] (device)
-    D2H of each finished pass's packed rows on a copy stream, overlapped with
-    the next pass's contraction (the paper's Alg. 2 double buffering,
-    PAPER.md:235-287, with the device array as the staging buffer)
+    X (host; pinned -> asynchronous) --copy-in stream, bottom rows first--> X_dev
+    K1 normalize per arrived chunk (csrc/normalize.cuh)     X_dev -> U (padded), flags
+    K2 contraction passes from the last tile backwards      U -> packed[n(n+1)/2] (device)
+       (csrc/syrk.cuh, packed epilogue)
+    completed packed rows --copy-out stream--> host, overlapped with later passes
 
-Passes are groups of whole GPU tile rows, so each pass owns one contiguous
-packed range and its copy is a single cudaMemcpyAsync.
+This is the paper's Alg. 2 (asynchronous double-buffered passes,
+PAPER.md:235-287) with the device array as the staging buffer.
 """
 
 from __future__ import annotations
@@ -31,6 +29,7 @@ from . import _lib
 from ._device import as_device_f64, ptr, resolve_devices, stream_handle
 from .distributed import BACKENDS, run_workers
 from .indexing import sym_job_count
+from .stream import run_stream
 from .tiles import DEFAULT_TILE_SIZE, CorrelationResult, TileGeometry
 from .transform import Dataset, normalize_device
 
@@ -91,44 +90,26 @@ def _allpairs_one_device(dataset: Dataset, device: torch.device, keep_on_device:
     n, l = dataset.n, dataset.l
     L = _lib.lib()
     with torch.cuda.device(device):
-        compute = torch.cuda.current_stream()
-        x = as_device_f64(dataset.values, device)
-        u, flags = normalize_device(x)
-        ldu = int(u.shape[1])
-        T = int(L.pcc_gpu_tile_count(n))
-        s = stream_handle(compute)
         if output == "dense":
+            compute = torch.cuda.current_stream()
+            x = as_device_f64(dataset.values, device)
+            u, flags = normalize_device(x)
+            T = int(L.pcc_gpu_tile_count(n))
             dense = torch.empty((n, n), dtype=torch.float64, device=device)
-            _lib.check(L.pcc_syrk_f64(ptr(u), n, l, ldu, 0, T, _lib.LAYOUT_DENSE, ptr(dense), n, 0, 0, 0, 0, s),
-                       "allpairs(dense)")
+            _lib.check(L.pcc_syrk_f64(ptr(u), n, l, u.shape[1], 0, T, _lib.LAYOUT_DENSE, ptr(dense), n, 0, 0, 0, 0,
+                                      stream_handle(compute)), "allpairs(dense)")
             zv = frozenset(np.flatnonzero(flags.cpu().numpy()).tolist())
             return (dense if keep_on_device else dense.cpu().numpy()), zv
 
         total = sym_job_count(n)
+        T = int(L.pcc_gpu_tile_count(n))
         packed = torch.empty(total, dtype=torch.float64, device=device)
+        host = None if keep_on_device else _host_out(out, total)
+        _, flags, _ = run_stream(dataset.values, n, l, device, 0, T, packed, 0, host, 0, chunks=passes * 2)
+        zv = frozenset(np.flatnonzero(flags.cpu().numpy()).tolist())
         if keep_on_device:
-            _lib.check(L.pcc_syrk_f64(ptr(u), n, l, ldu, 0, T, _lib.LAYOUT_PACKED, ptr(packed), 0, 0, 0, 0, 0, s),
-                       "allpairs")
-            zv = frozenset(np.flatnonzero(flags.cpu().numpy()).tolist())
             return packed, zv
-
-        host = _host_out(out, total)
-        pinned = host.is_pinned()
-        copy = torch.cuda.Stream(device)
-        for tb, te, lo, hi in plan_row_passes(n, passes):
-            _lib.check(L.pcc_syrk_f64(ptr(u), n, l, ldu, tb, te, _lib.LAYOUT_PACKED, ptr(packed), 0, 0, 0, 0, 0, s),
-                       "allpairs")
-            ev = torch.cuda.Event()
-            ev.record(compute)
-            copy.wait_event(ev)
-            with torch.cuda.stream(copy):
-                host[lo:hi].copy_(packed[lo:hi], non_blocking=pinned)
-        flags_host = flags.cpu()
-        copy.synchronize()
-        packed.record_stream(copy)
-        zv = frozenset(np.flatnonzero(flags_host.numpy()).tolist())
-        result = out if out is not None else host.numpy()
-        return result, zv
+        return (out if out is not None else host.numpy()), zv
 
 
 def allpairs(
@@ -160,8 +141,8 @@ def allpairs(
       in ``CorrelationResult.packed``);
     * ``out``: caller-owned host float64 buffer for the packed result (pinned
       memory makes the device-to-host copies asynchronous);
-    * ``passes``: number of row-group passes whose D2H copies overlap the
-      contraction.
+    * ``passes``: upload granularity (``2 * passes`` bottom-up row chunks);
+      contraction passes are whole waves, see ``stream.plan_stream``.
     """
     if not isinstance(dataset, Dataset):
         from .fileio import load_dataset

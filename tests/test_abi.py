@@ -57,7 +57,7 @@ def test_invalid_arguments_rejected_before_any_device_work():
     with pytest.raises(ValueError, match="n must be"):
         _lib.check(L.pcc_syrk_f64(None, 0, 17, 32, 0, 1, 0, None, 0, 0, 0, 0, 0, None))
     with pytest.raises(ValueError, match="tile size"):
-        _lib.check(L.pcc_compute_pass_f64(ctypes.c_void_p(16), 10, 5, 16, 0, 0, 1, None, None))
+        _lib.check(L.pcc_compute_pass_f64(ctypes.c_void_p(16), 10, 5, 32, 0, 0, 1, None, None))
     assert L.pcc_last_error()
 
 

@@ -262,14 +262,46 @@ def test_errors_are_loud():
         _lib.check(L.pcc_syrk_f64(None, 10, 5, 16, 0, 1, 0, None, 0, 0, 0, 0, 0, None))
     with pytest.raises(ValueError):
         _lib.check(L.pcc_normalize_rows_f64(None, 1, None, 1, None, 1, 0, 1, None))
-    u = torch.zeros((128, 16), dtype=torch.float64, device="cuda")
+    u = torch.zeros((128, 32), dtype=torch.float64, device="cuda")
     out = torch.zeros(55, dtype=torch.float64, device="cuda")
-    with pytest.raises(ValueError):  # tile range past the end
-        _lib.check(L.pcc_syrk_f64(u.data_ptr(), 10, 5, 16, 0, 2, 0, out.data_ptr(), 0, 0, 0, 0, 0, None))
-    with pytest.raises(ValueError):  # reference tile range past the end
-        _lib.check(L.pcc_compute_pass_f64(u.data_ptr(), 10, 5, 16, 4, 0, 7, out.data_ptr(), None))
+    with pytest.raises(ValueError, match="tile range"):  # tile range past the end
+        _lib.check(L.pcc_syrk_f64(u.data_ptr(), 10, 5, 32, 0, 2, 0, out.data_ptr(), 0, 0, 0, 0, 0, None))
+    with pytest.raises(ValueError, match="tile range"):  # reference tile range past the end
+        _lib.check(L.pcc_compute_pass_f64(u.data_ptr(), 10, 5, 32, 4, 0, 7, out.data_ptr(), None))
+    with pytest.raises(ValueError, match="variant"):
+        _lib.check(L.pcc_syrk_f64_variant(99, u.data_ptr(), 10, 5, 32, 0, 1, 0, out.data_ptr(), 0, 0, 0, 0, 0, None))
 
 
 def test_fp64_probe_reports_plausible_peak():
     tf = _lib.probe_fp64_peak()
     assert 10.0 < tf < 80.0
+
+
+def test_compute_worker_streamed_shards_match_single(rng):
+    from paper_1605_01584_b200.distributed import compute_worker, owned_runs, shard_span
+
+    x = random_values(rng, 1100, 23, special_rows=True)
+    d = pc.Dataset(values=x)
+    ref = pc.allpairs(d).packed
+    n = x.shape[0]
+    mg = -(-n // 128)
+    T = mg * (mg + 1) // 2
+    for p in (1, 2, 3, 5):
+        for w in range(p):
+            lo_t, hi_t = pc.partition(T, p)[w]
+            lo, hi = shard_span(n, lo_t, hi_t)
+            host = torch.full((max(1, hi - lo),), float("nan"), dtype=torch.float64).pin_memory()
+            sh = compute_worker(pc.Dataset(values=torch.from_numpy(x).pin_memory()), p, w, 0, out=host)
+            for a, b in owned_runs(n, lo_t, hi_t):
+                assert np.array_equal(host[a - lo:b - lo].numpy(), ref[a:b])
+                assert np.array_equal(sh.values[a - lo:b - lo].cpu().numpy(), ref[a:b])
+            if w == 0:
+                assert sh.zero_variance == frozenset({1})
+
+
+def test_streamed_upload_from_pageable_and_device_inputs(rng):
+    x = random_values(rng, 900, 64, special_rows=True)
+    ref, zv = oracle.allpairs(x, t=4)
+    for values in (x, torch.from_numpy(x), torch.from_numpy(x).cuda()):
+        res = pc.allpairs(pc.Dataset(values=values), passes=3)
+        _assert_parity(res.packed, ref, frozenset(np.flatnonzero(zv).tolist()), 900)
