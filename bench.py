@@ -135,8 +135,8 @@ def run_reference(args, rank: int, world: int) -> None:
 
 
 def _default_ref_fraction(cfg: str) -> float:
-    # ~1-2 s of 16-thread CPU work per step
-    return {"c1": 1.0, "c2": 1 / 64, "c3": 1 / 8, "c4": 1 / 512, "c5": 1 / 512}[cfg]
+    # ~3 s of 16-thread CPU work per step (the whole --steps/--warmup run ends within ~1 minute)
+    return {"c1": 1.0, "c2": 1 / 4, "c3": 1.0, "c4": 1 / 64, "c5": 1 / 64}[cfg]
 
 
 # --------------------------------------------------------------------------- helpers
@@ -244,20 +244,24 @@ def run_b200(args, rank: int, world: int, local_rank: int) -> None:
     from paper_1605_01584_b200.workloads import CONFIGS, make_config
     from paper_1605_01584_b200.transform import normalize_device
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    ndev = torch.cuda.device_count()
+    dev_index = local_rank % ndev  # N ranks on fewer GPUs only in functional tests
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
     spec = CONFIGS[args.config]
     n, l = spec.n, spec.l
     L = _lib.lib()
 
+    # The process group (gloo, host side) carries only the barrier and the
+    # max-over-ranks timing reduction -- nothing in the data path.
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local_rank])
+            dist.barrier()
 
     def max_over_ranks(v: float) -> float:
         if world == 1:
             return v
-        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        t = torch.tensor([v], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -294,7 +298,7 @@ def run_b200(args, rank: int, world: int, local_rank: int) -> None:
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local_rank) as clocks:
+    with ClockSampler(dev_index) as clocks:
         t0.record(stream)
         for i in range(args.steps):
             step(syrk_events[i])
@@ -311,7 +315,7 @@ def run_b200(args, rank: int, world: int, local_rank: int) -> None:
     peak = _lib.probe_fp64_peak()
     flops_launch = 2.0 * l * my_cells                          # algorithmic: 2 l per owned pair
     achieved = flops_launch / (sum(syrk_ms) / len(syrk_ms) * 1e-3) / 1e12 if te > tb else 0.0
-    achieved = max_over_ranks(achieved) if world == 1 else achieved
+
     roof = {
         "bound": "tensor",
         "achieved": achieved,
@@ -358,7 +362,8 @@ def run_b200(args, rank: int, world: int, local_rank: int) -> None:
         import oracle
 
         threads = oracle.default_threads()
-        frac = args.cpu_fraction or {"c1": 1.0, "c2": 1 / 16, "c3": 1 / 2, "c4": 1 / 256, "c5": 1 / 128}[args.config]
+        # ~10-30 s of host work: the whole c1/c2/c3 job, a prefix of c4/c5
+        frac = args.cpu_fraction or {"c1": 1.0, "c2": 1.0, "c3": 1.0, "c4": 1 / 16, "c5": 1 / 16}[args.config]
         res = cpu_sample(x_host, frac, threads)
         cpu = {
             "value": res["pairs_per_s"],
@@ -407,12 +412,7 @@ def main(argv=None):
     if world > 1:
         import torch.distributed as dist
 
-        backend = "gloo" if args.impl == "reference" else "nccl"
-        if backend == "nccl":
-            import torch
-
-            torch.cuda.set_device(local_rank)
-        dist.init_process_group(backend=backend)
+        dist.init_process_group(backend="gloo")
     try:
         if args.impl == "reference":
             run_reference(args, rank, world)

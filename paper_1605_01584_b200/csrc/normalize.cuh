@@ -86,4 +86,100 @@ normalize_rows_kernel(const double *__restrict__ x, int64_t ldx, double *__restr
   for (k = l + lane8; k < ldu; k += 8) ur[k] = 0.0;
 }
 
+// ---------------------------------------------------------------------------
+// Shared-memory-staged variant (the default when R >= 1 rows of l doubles
+// fit the per-CTA budget): X is read from HBM exactly once.
+//   1. all 256 threads stream R rows into shared memory with 8-byte
+//      cp.async (any l / ldx alignment), many copies in flight per thread;
+//   2. 8 threads per row run the reference's lane chains (sum + constancy,
+//      then ssd) out of shared memory and finish with the shuffle tree;
+//   3. all threads write u = (x - mean) / scale (or the zero row) back with
+//      coalesced stores, plus the zero K padding up to ldu.
+// Two CTAs per SM (<= ~100 KB each) overlap one CTA's chains with the
+// other's copies.  Same arithmetic as normalize_rows_kernel, bit for bit.
+constexpr int kNormSmemBudget = 100 * 1024;
+
+__device__ __forceinline__ void cp_async_8(uint32_t dst, const void *src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src));
+}
+
+__global__ void __launch_bounds__(kNormThreads)
+normalize_rows_smem_kernel(const double *__restrict__ x, int64_t ldx, double *__restrict__ u, int64_t ldu,
+                           uint8_t *__restrict__ zero_variance, int64_t l, int64_t row_lo, int64_t row_hi,
+                           int rows_per_cta) {
+  extern __shared__ __align__(16) double srow[];  // [rows_per_cta][l]
+  __shared__ double s_mean[kNormRowsPerCta], s_scale[kNormRowsPerCta];
+  __shared__ int s_zero[kNormRowsPerCta];
+  const int tid = threadIdx.x;
+  const int64_t r0 = row_lo + (int64_t)blockIdx.x * rows_per_cta;
+  const int rows = (int)((row_hi - r0) < (int64_t)rows_per_cta ? (row_hi - r0) : (int64_t)rows_per_cta);
+  const uint32_t sbase = smem_u32(srow);
+
+  // 1. stage the rows
+  for (int r = 0; r < rows; ++r) {
+    const double *xr = x + (r0 + r) * ldx;
+    const uint32_t sr = sbase + (uint32_t)(r * l * sizeof(double));
+    for (int64_t k = tid; k < l; k += kNormThreads) cp_async_8(sr + (uint32_t)(k * sizeof(double)), xr + k);
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+
+  // 2. lane chains: thread (row = tid / 8, lane8 = tid % 8)
+  const int lane8 = tid & 7;
+  const int row = tid >> 3;
+  const bool active = row < rows;
+  const double *sr = srow + (int64_t)(active ? row : 0) * l;
+  const double first = sr[0];
+  double s = 0.0;
+  bool varies = false;
+  int64_t k = lane8;
+#pragma unroll 8
+  for (; k < l; k += 8) {
+    const double v = sr[k];
+    s = __dadd_rn(s, v);
+    varies |= (v != first);
+  }
+  s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 1));
+  s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 2));
+  s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 4));
+  const unsigned vb = __ballot_sync(0xffffffffu, varies);
+  const bool constant = (vb & (0xffu << (tid & 24))) == 0u;
+  double mean = 0.0, ssd = 0.0;
+  if (!constant) {
+    mean = __ddiv_rn(s, (double)l);
+    double q = 0.0;
+#pragma unroll 8
+    for (k = lane8; k < l; k += 8) {
+      const double d = __dsub_rn(sr[k], mean);
+      q = __dadd_rn(q, __dmul_rn(d, d));
+    }
+    ssd = q;
+  }
+  ssd = __dadd_rn(ssd, __shfl_xor_sync(0xffffffffu, ssd, 1));
+  ssd = __dadd_rn(ssd, __shfl_xor_sync(0xffffffffu, ssd, 2));
+  ssd = __dadd_rn(ssd, __shfl_xor_sync(0xffffffffu, ssd, 4));
+  if (active && lane8 == 0) {
+    const bool zero = constant || ssd == 0.0;
+    s_zero[row] = zero;
+    s_mean[row] = mean;
+    s_scale[row] = zero ? 0.0 : __dsqrt_rn(ssd);
+    zero_variance[r0 + row] = zero ? 1 : 0;
+  }
+  __syncthreads();
+
+  // 3. write U rows (coalesced), zero rows for zero variance, zero K padding
+  for (int r = 0; r < rows; ++r) {
+    double *ur = u + (r0 + r) * ldu;
+    const double *xs = srow + (int64_t)r * l;
+    if (s_zero[r]) {
+      for (k = tid; k < ldu; k += kNormThreads) ur[k] = 0.0;
+    } else {
+      const double m = s_mean[r], sc = s_scale[r];
+      for (k = tid; k < l; k += kNormThreads) ur[k] = __ddiv_rn(__dsub_rn(xs[k], m), sc);
+      for (k = l + tid; k < ldu; k += kNormThreads) ur[k] = 0.0;
+    }
+  }
+}
+
 }  // namespace pcc

@@ -62,7 +62,10 @@ using V5 = pcc::SyrkCfg<2, 4, 8, 4, 8, 12>;  // TMA, BK 8 x 12 stages
 using V6 = pcc::SyrkCfg<2, 4, 8, 4, 16, 7>;  // TMA, BK 16 x 7 stages
 using V7 = pcc::SyrkCfg<2, 4, 8, 4, 32, 3>;  // TMA, BK 32 x 3 stages
 using V8 = pcc::SyrkCfg<4, 2, 4, 8, 16, 6>;  // TMA, 8 warps 32x64
-constexpr int kNumVariants = 9;
+using V9 = pcc::SyrkCfg<4, 4, 4, 4, 16, 6>;  // TMA, 16 warps 32x32
+using V10 = pcc::SyrkCfg<2, 4, 8, 4, 16, 6, 4>;  // TMA, producer 4 steps ahead
+using V11 = pcc::SyrkCfg<2, 4, 8, 4, 16, 6, 2>;  // TMA, producer 2 steps ahead
+constexpr int kNumVariants = 12;
 
 template <class C, int LAYOUT>
 int configure_tma_one(int *ctas) {
@@ -166,6 +169,9 @@ int device_config(const DeviceConfig **out, int device = -1) {
     if (rc == PCC_OK) rc = configure_tma_one<V6, pcc::kLayoutPacked>(&c.variant_ctas[6]);
     if (rc == PCC_OK) rc = configure_tma_one<V7, pcc::kLayoutPacked>(&c.variant_ctas[7]);
     if (rc == PCC_OK) rc = configure_tma_one<V8, pcc::kLayoutPacked>(&c.variant_ctas[8]);
+    if (rc == PCC_OK) rc = configure_tma_one<V9, pcc::kLayoutPacked>(&c.variant_ctas[9]);
+    if (rc == PCC_OK) rc = configure_tma_one<V10, pcc::kLayoutPacked>(&c.variant_ctas[10]);
+    if (rc == PCC_OK) rc = configure_tma_one<V11, pcc::kLayoutPacked>(&c.variant_ctas[11]);
     if (prev != device) cudaSetDevice(prev);
     if (rc != PCC_OK) return rc;
     c.syrk_ctas_per_sm = c.variant_ctas[0];
@@ -240,6 +246,9 @@ int launch_syrk(const double *u, int64_t n, int64_t l, int64_t ldu, uint64_t tb,
     case 6: return launch_tma_cfg<V6, pcc::kLayoutPacked>(u, n, l, ldu, tb, te, ep, stream, vc[6], sms);
     case 7: return launch_tma_cfg<V7, pcc::kLayoutPacked>(u, n, l, ldu, tb, te, ep, stream, vc[7], sms);
     case 8: return launch_tma_cfg<V8, pcc::kLayoutPacked>(u, n, l, ldu, tb, te, ep, stream, vc[8], sms);
+    case 9: return launch_tma_cfg<V9, pcc::kLayoutPacked>(u, n, l, ldu, tb, te, ep, stream, vc[9], sms);
+    case 10: return launch_tma_cfg<V10, pcc::kLayoutPacked>(u, n, l, ldu, tb, te, ep, stream, vc[10], sms);
+    case 11: return launch_tma_cfg<V11, pcc::kLayoutPacked>(u, n, l, ldu, tb, te, ep, stream, vc[11], sms);
     default: return fail(PCC_EINVAL, "unknown contraction variant %d (0..%d)", variant, kNumVariants - 1);
   }
 }
@@ -293,6 +302,28 @@ int pcc_normalize_rows_f64(const double *x, int64_t ldx, double *u, int64_t ldu,
   if (row_hi == row_lo) return PCC_OK;
   if (!x || !u || !zero_variance) return fail(PCC_EINVAL, "null pointer");
   const uint64_t rows = (uint64_t)(row_hi - row_lo);
+  const int64_t row_bytes = l * (int64_t)sizeof(double);
+  const int per_cta = (int)(row_bytes <= pcc::kNormSmemBudget
+                                ? (pcc::kNormSmemBudget / row_bytes < pcc::kNormRowsPerCta ? pcc::kNormSmemBudget / row_bytes
+                                                                                           : pcc::kNormRowsPerCta)
+                                : 0);
+  if (per_cta >= 1) {
+    static std::once_flag attr_once;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(attr_once, [] {
+      attr_err = cudaFuncSetAttribute(pcc::normalize_rows_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      pcc::kNormSmemBudget);
+    });
+    if (attr_err != cudaSuccess) return cuda_fail(attr_err, "cudaFuncSetAttribute(normalize smem)");
+    const uint64_t grid = ceil_div(rows, (uint64_t)per_cta);
+    if (grid > 0x7FFFFFFFull) return fail(PCC_EINVAL, "too many rows");
+    const size_t smem = (size_t)per_cta * (size_t)row_bytes;
+    pcc::normalize_rows_smem_kernel<<<(unsigned)grid, pcc::kNormThreads, smem, (cudaStream_t)stream>>>(
+        x, ldx, u, ldu, zero_variance, l, row_lo, row_hi, per_cta);
+    PCC_CUDA(cudaGetLastError(), "normalize_rows_smem_kernel launch");
+    return PCC_OK;
+  }
+  // rows longer than the shared-memory budget: three streaming passes from global memory
   const uint64_t grid = ceil_div(rows, pcc::kNormRowsPerCta);
   if (grid > 0x7FFFFFFFull) return fail(PCC_EINVAL, "too many rows");
   pcc::normalize_rows_kernel<<<(unsigned)grid, pcc::kNormThreads, 0, (cudaStream_t)stream>>>(

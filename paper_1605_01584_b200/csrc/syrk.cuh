@@ -41,9 +41,10 @@ enum : int { kLayoutPacked = 0, kLayoutDense = 1, kLayoutTiles = 2 };
 // Kernel shape: WARPS_M x WARPS_N warps, each owning MI x NI DMMA 8x8
 // accumulators (CTA tile 128 x 128), K staged BK doubles per stage through
 // a STAGES-deep cp.async ring.
-template <int WARPS_M_, int WARPS_N_, int MI_, int NI_, int BK_, int STAGES_>
+template <int WARPS_M_, int WARPS_N_, int MI_, int NI_, int BK_, int STAGES_, int AHEAD_ = STAGES_ / 2>
 struct SyrkCfg {
   static constexpr int WARPS_M = WARPS_M_, WARPS_N = WARPS_N_, MI = MI_, NI = NI_, BK = BK_, STAGES = STAGES_;
+  static constexpr int AHEAD = AHEAD_;  // TMA producer lead (K steps) over warp 0
   static constexpr int kThreads = 32 * WARPS_M * WARPS_N;
   static constexpr int kSlabs = BK / kSlab;
   static constexpr int kOpDoubles = kSlabs * kTile * kSlab;
@@ -200,7 +201,7 @@ struct TmaLayout {
   static constexpr int kBarOffset = C::kSmemBytes;  // 2 * STAGES mbarriers after the ring
   static constexpr int kSmemBytes = C::kSmemBytes + 2 * C::STAGES * 8;
   static constexpr int kThreads = C::kThreads;
-  static constexpr int kAhead = C::STAGES / 2;  // producer lead over warp 0, in K steps
+  static constexpr int kAhead = C::AHEAD;
   static constexpr uint32_t kStageBytes = (uint32_t)(C::kStageDoubles * sizeof(double));
   static constexpr uint32_t kSlabBytes = (uint32_t)(kTile * kSlab * sizeof(double));
 };

@@ -305,3 +305,18 @@ def test_streamed_upload_from_pageable_and_device_inputs(rng):
     for values in (x, torch.from_numpy(x), torch.from_numpy(x).cuda()):
         res = pc.allpairs(pc.Dataset(values=values), passes=3)
         _assert_parity(res.packed, ref, frozenset(np.flatnonzero(zv).tolist()), 900)
+
+
+@pytest.mark.parametrize("n,l", [(3, 12_801), (2, 20_000), (1, 1_000_000), (40, 12_800), (33, 4_096)])
+def test_normalize_long_rows_bit_exact(n, l):
+    """Rows beyond the shared-memory budget take the three-pass global kernel;
+    both paths must equal the reference's normalize_rows bit for bit
+    (the reference tests a 10^6-sample row, test_transform.py:91-97)."""
+    rng = np.random.default_rng(l)
+    x = rng.random((n, l))
+    if n > 1:
+        x[1] = 0.5
+    u, zv = _abi_normalize(x)
+    u_ref, zv_ref = oracle.normalize(x)
+    assert np.array_equal(u.cpu().numpy()[:n, :l], u_ref)
+    assert np.array_equal(zv.cpu().numpy().astype(bool), zv_ref)
