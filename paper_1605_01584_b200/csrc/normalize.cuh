@@ -25,6 +25,56 @@
 
 namespace pcc {
 
+// ---------------------------------------------------------------------------
+// One reference reduction lane, software-pipelined: the next PF elements of
+// the lane (stride 8) are loaded while the current PF are added, so the
+// dependent add chain -- which the reference's order makes inherently
+// sequential -- runs at FP64-add latency instead of load latency.
+// SSD = false: sum8 lane + constancy test against `ref` (= x[0]);
+// SSD = true:  ssd8 lane with `ref` = mean.
+template <bool SSD, int PF>
+__device__ __forceinline__ double lane_chain(const double *p, int64_t nsteps64, double ref, bool &varies) {
+  const int nsteps = (int)nsteps64;
+  const int full = (nsteps / PF) * PF;
+  double s = 0.0;
+  double nxt[PF];
+  if (full > 0) {
+#pragma unroll
+    for (int i = 0; i < PF; ++i) nxt[i] = p[8 * i];
+  }
+  int t = 0;
+  for (; t < full; t += PF) {
+    double cur[PF];
+#pragma unroll
+    for (int i = 0; i < PF; ++i) cur[i] = nxt[i];
+    if (t + PF < full) {
+#pragma unroll
+      for (int i = 0; i < PF; ++i) nxt[i] = p[8 * (t + PF + i)];
+    }
+#pragma unroll
+    for (int i = 0; i < PF; ++i) {
+      if (SSD) {
+        const double d = __dsub_rn(cur[i], ref);
+        s = __dadd_rn(s, __dmul_rn(d, d));
+      } else {
+        s = __dadd_rn(s, cur[i]);
+        varies |= (cur[i] != ref);
+      }
+    }
+  }
+  for (; t < nsteps; ++t) {
+    const double v = p[8 * t];
+    if (SSD) {
+      const double d = __dsub_rn(v, ref);
+      s = __dadd_rn(s, __dmul_rn(d, d));
+    } else {
+      s = __dadd_rn(s, v);
+      varies |= (v != ref);
+    }
+  }
+  return s;
+}
+
 constexpr int kNormThreads = 256;
 constexpr int kNormRowsPerCta = kNormThreads / 8;
 
@@ -41,16 +91,10 @@ normalize_rows_kernel(const double *__restrict__ x, int64_t ldx, double *__restr
   double *ur = u + r * ldu;
 
   // Pass 1: lane sum (sum8 order) + exact constancy test.
-  const double first = xr[0];
-  double s = 0.0;
+  const int64_t nsteps = (l - lane8 + 7) >> 3;
   bool varies = false;
-  int64_t k = lane8;
-#pragma unroll 4
-  for (; k < l; k += 8) {
-    double v = __ldg(xr + k);
-    s = __dadd_rn(s, v);
-    varies |= (v != first);
-  }
+  double s = lane_chain<false, 16>(xr + lane8, nsteps, xr[0], varies);
+  int64_t k;
   // Tree ((s0+s1)+(s2+s3))+((s4+s5)+(s6+s7)) inside each 8-lane group.
   s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 1));
   s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 2));
@@ -62,12 +106,8 @@ normalize_rows_kernel(const double *__restrict__ x, int64_t ldx, double *__restr
   double ssd = 0.0, mean = 0.0;
   if (!constant) {  // uniform within the 8-lane group
     mean = __ddiv_rn(s, (double)l);
-    double q = 0.0;
-    for (k = lane8; k < l; k += 8) {
-      double d = __dsub_rn(__ldg(xr + k), mean);
-      q = __dadd_rn(q, __dmul_rn(d, d));
-    }
-    ssd = q;
+    bool unused = false;
+    ssd = lane_chain<true, 16>(xr + lane8, nsteps, mean, unused);
   }
   // Every lane of the warp reaches this point (constant groups carry 0.0).
   ssd = __dadd_rn(ssd, __shfl_xor_sync(0xffffffffu, ssd, 1));
@@ -86,30 +126,31 @@ normalize_rows_kernel(const double *__restrict__ x, int64_t ldx, double *__restr
   for (k = l + lane8; k < ldu; k += 8) ur[k] = 0.0;
 }
 
-// ---------------------------------------------------------------------------
-// Shared-memory-staged variant (the default when R >= 1 rows of l doubles
-// fit the per-CTA budget): X is read from HBM exactly once.
-//   1. all 256 threads stream R rows into shared memory with 8-byte
-//      cp.async (any l / ldx alignment), many copies in flight per thread;
+// Shared-memory-staged variant (default whenever a row fits): X is read from
+// HBM exactly once.
+//   1. the CTA streams its R rows into shared memory with 8-byte cp.async
+//      (any l / ldx alignment, many copies in flight per thread);
 //   2. 8 threads per row run the reference's lane chains (sum + constancy,
 //      then ssd) out of shared memory and finish with the shuffle tree;
 //   3. all threads write u = (x - mean) / scale (or the zero row) back with
 //      coalesced stores, plus the zero K padding up to ldu.
-// Two CTAs per SM (<= ~100 KB each) overlap one CTA's chains with the
-// other's copies.  Same arithmetic as normalize_rows_kernel, bit for bit.
-constexpr int kNormSmemBudget = 100 * 1024;
+// Small CTAs (64 threads, R <= 8 rows) so several CTAs share an SM and one
+// CTA's chains overlap the others' copies.  Same arithmetic as
+// normalize_rows_kernel, bit for bit.
+constexpr int kNormSmemThreads = 64;
+constexpr int kNormSmemMaxRows = kNormSmemThreads / 8;
 
 __device__ __forceinline__ void cp_async_8(uint32_t dst, const void *src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src));
 }
 
-__global__ void __launch_bounds__(kNormThreads)
+__global__ void __launch_bounds__(kNormSmemThreads)
 normalize_rows_smem_kernel(const double *__restrict__ x, int64_t ldx, double *__restrict__ u, int64_t ldu,
                            uint8_t *__restrict__ zero_variance, int64_t l, int64_t row_lo, int64_t row_hi,
                            int rows_per_cta) {
   extern __shared__ __align__(16) double srow[];  // [rows_per_cta][l]
-  __shared__ double s_mean[kNormRowsPerCta], s_scale[kNormRowsPerCta];
-  __shared__ int s_zero[kNormRowsPerCta];
+  __shared__ double s_mean[kNormSmemMaxRows], s_scale[kNormSmemMaxRows];
+  __shared__ int s_zero[kNormSmemMaxRows];
   const int tid = threadIdx.x;
   const int64_t r0 = row_lo + (int64_t)blockIdx.x * rows_per_cta;
   const int rows = (int)((row_hi - r0) < (int64_t)rows_per_cta ? (row_hi - r0) : (int64_t)rows_per_cta);
@@ -119,7 +160,7 @@ normalize_rows_smem_kernel(const double *__restrict__ x, int64_t ldx, double *__
   for (int r = 0; r < rows; ++r) {
     const double *xr = x + (r0 + r) * ldx;
     const uint32_t sr = sbase + (uint32_t)(r * l * sizeof(double));
-    for (int64_t k = tid; k < l; k += kNormThreads) cp_async_8(sr + (uint32_t)(k * sizeof(double)), xr + k);
+    for (int64_t k = tid; k < l; k += kNormSmemThreads) cp_async_8(sr + (uint32_t)(k * sizeof(double)), xr + k);
   }
   cp_async_commit();
   cp_async_wait<0>();
@@ -130,16 +171,9 @@ normalize_rows_smem_kernel(const double *__restrict__ x, int64_t ldx, double *__
   const int row = tid >> 3;
   const bool active = row < rows;
   const double *sr = srow + (int64_t)(active ? row : 0) * l;
-  const double first = sr[0];
-  double s = 0.0;
+  const int64_t nsteps = (l - lane8 + 7) >> 3;
   bool varies = false;
-  int64_t k = lane8;
-#pragma unroll 8
-  for (; k < l; k += 8) {
-    const double v = sr[k];
-    s = __dadd_rn(s, v);
-    varies |= (v != first);
-  }
+  double s = lane_chain<false, 8>(sr + lane8, nsteps, sr[0], varies);
   s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 1));
   s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 2));
   s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 4));
@@ -148,13 +182,8 @@ normalize_rows_smem_kernel(const double *__restrict__ x, int64_t ldx, double *__
   double mean = 0.0, ssd = 0.0;
   if (!constant) {
     mean = __ddiv_rn(s, (double)l);
-    double q = 0.0;
-#pragma unroll 8
-    for (k = lane8; k < l; k += 8) {
-      const double d = __dsub_rn(sr[k], mean);
-      q = __dadd_rn(q, __dmul_rn(d, d));
-    }
-    ssd = q;
+    bool unused = false;
+    ssd = lane_chain<true, 8>(sr + lane8, nsteps, mean, unused);
   }
   ssd = __dadd_rn(ssd, __shfl_xor_sync(0xffffffffu, ssd, 1));
   ssd = __dadd_rn(ssd, __shfl_xor_sync(0xffffffffu, ssd, 2));
@@ -173,11 +202,11 @@ normalize_rows_smem_kernel(const double *__restrict__ x, int64_t ldx, double *__
     double *ur = u + (r0 + r) * ldu;
     const double *xs = srow + (int64_t)r * l;
     if (s_zero[r]) {
-      for (k = tid; k < ldu; k += kNormThreads) ur[k] = 0.0;
+      for (int64_t k = tid; k < ldu; k += kNormSmemThreads) ur[k] = 0.0;
     } else {
       const double m = s_mean[r], sc = s_scale[r];
-      for (k = tid; k < l; k += kNormThreads) ur[k] = __ddiv_rn(__dsub_rn(xs[k], m), sc);
-      for (k = l + tid; k < ldu; k += kNormThreads) ur[k] = 0.0;
+      for (int64_t k = tid; k < l; k += kNormSmemThreads) ur[k] = __ddiv_rn(__dsub_rn(xs[k], m), sc);
+      for (int64_t k = l + tid; k < ldu; k += kNormSmemThreads) ur[k] = 0.0;
     }
   }
 }

@@ -6,6 +6,7 @@
 // to a CPU path.
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -303,22 +304,36 @@ int pcc_normalize_rows_f64(const double *x, int64_t ldx, double *u, int64_t ldu,
   if (!x || !u || !zero_variance) return fail(PCC_EINVAL, "null pointer");
   const uint64_t rows = (uint64_t)(row_hi - row_lo);
   const int64_t row_bytes = l * (int64_t)sizeof(double);
-  const int per_cta = (int)(row_bytes <= pcc::kNormSmemBudget
-                                ? (pcc::kNormSmemBudget / row_bytes < pcc::kNormRowsPerCta ? pcc::kNormSmemBudget / row_bytes
-                                                                                           : pcc::kNormRowsPerCta)
-                                : 0);
-  if (per_cta >= 1) {
+  // Shared-memory staging: as many 64-thread CTAs per SM as rows allow
+  // (4, 3, 2, then 1 CTA/SM), up to 8 rows per CTA.
+  constexpr int64_t kSmPerSmem = 224 * 1024;
+  int per_cta = 0;
+  size_t smem = 0;
+  // Measured (round 1, profiles/r01_normalize.log): staging wins up to
+  // 32 KB rows (c2: 390 vs 470 us), the 3-pass kernel wins at 64 KB (c4).
+  constexpr int64_t kMaxStagedRow = 48 * 1024;
+  for (int ctas = 4; ctas >= 1 && per_cta == 0 && row_bytes <= kMaxStagedRow; --ctas) {
+    const int64_t budget = kSmPerSmem / ctas - 1024;
+    if (row_bytes <= budget) {
+      per_cta = (int)(budget / row_bytes < pcc::kNormSmemMaxRows ? budget / row_bytes : pcc::kNormSmemMaxRows);
+      smem = (size_t)per_cta * (size_t)row_bytes;
+    }
+  }
+  static const bool force_global = [] {
+    const char *e = getenv("PCC_NORMALIZE_KERNEL");  // tuning knob: "global" forces the 3-pass kernel
+    return e != nullptr && strcmp(e, "global") == 0;
+  }();
+  if (per_cta >= 1 && !force_global) {
     static std::once_flag attr_once;
     static cudaError_t attr_err = cudaSuccess;
     std::call_once(attr_once, [] {
       attr_err = cudaFuncSetAttribute(pcc::normalize_rows_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      pcc::kNormSmemBudget);
+                                      (int)kSmPerSmem);
     });
     if (attr_err != cudaSuccess) return cuda_fail(attr_err, "cudaFuncSetAttribute(normalize smem)");
     const uint64_t grid = ceil_div(rows, (uint64_t)per_cta);
     if (grid > 0x7FFFFFFFull) return fail(PCC_EINVAL, "too many rows");
-    const size_t smem = (size_t)per_cta * (size_t)row_bytes;
-    pcc::normalize_rows_smem_kernel<<<(unsigned)grid, pcc::kNormThreads, smem, (cudaStream_t)stream>>>(
+    pcc::normalize_rows_smem_kernel<<<(unsigned)grid, pcc::kNormSmemThreads, smem, (cudaStream_t)stream>>>(
         x, ldx, u, ldu, zero_variance, l, row_lo, row_hi, per_cta);
     PCC_CUDA(cudaGetLastError(), "normalize_rows_smem_kernel launch");
     return PCC_OK;

@@ -320,3 +320,35 @@ def test_normalize_long_rows_bit_exact(n, l):
     u_ref, zv_ref = oracle.normalize(x)
     assert np.array_equal(u.cpu().numpy()[:n, :l], u_ref)
     assert np.array_equal(zv.cpu().numpy().astype(bool), zv_ref)
+
+
+@pytest.mark.parametrize("name", ["c2", "c4", "c5"])
+def test_full_size_configs_sampled_rows_and_properties(name):
+    """BASELINE configs at full size: U bit-exact; sampled packed rows (tile
+    edges, first/last, random) within 1e-12 of the reference's dot8; every
+    coefficient in [-1-1e-12, 1+1e-12]; every diagonal within 1e-12 of 1."""
+    x = make_config(name)
+    n, l = x.shape
+    d = pc.Dataset(values=torch.from_numpy(x).pin_memory())
+    res = pc.allpairs(d, keep_on_device=True)
+    packed = res.packed
+    nd = pc.normalize(d)
+    u_ref, zv_ref = oracle.normalize(x)
+    assert torch.equal(nd.u_device[:n, :l].cpu(), torch.from_numpy(u_ref))
+    assert res.zero_variance == frozenset(np.flatnonzero(zv_ref).tolist())
+    rng = np.random.default_rng(11)
+    rows = sorted({0, 1, 127, 128, 129, 255, 256, n // 2, n - 129, n - 128, n - 1,
+                   *rng.integers(0, n, 6).tolist()})
+    ref_rows = oracle.packed_rows(u_ref, rows)
+    worst = 0.0
+    for y in rows:
+        lo = (y * (2 * n + 1 - y)) // 2
+        got = packed[lo:lo + n - y].cpu().numpy()
+        worst = max(worst, float(np.abs(got - ref_rows[y]).max()))
+    assert worst <= TOL, f"{name}: max dev {worst:.3e}"
+    assert float(packed.min()) >= -1.0 - 1e-12 and float(packed.max()) <= 1.0 + 1e-12
+    ys = torch.arange(n, device=packed.device, dtype=torch.int64)
+    diag = packed[(ys * (2 * n + 1 - ys)) // 2]
+    assert float((diag - 1.0).abs().max()) <= 1e-12
+    del packed, res, nd
+    torch.cuda.empty_cache()
