@@ -148,6 +148,14 @@ int pcc_allpairs_f64(const double *x, int64_t n, int64_t l, int64_t ldx, double 
                      uint8_t *zero_variance, uint64_t tile_begin, uint64_t tile_end,
                      int32_t layout, double *out, int64_t ld_out, uint64_t out_base, void *stream);
 
+/* Diagnostics (host only, no GPU): the order in which the production
+ * contraction visits the GPU tiles [tile_begin, tile_end) -- partial first
+ * row, full rows in groups of `group` rows walked column by column, partial
+ * last row.  Writes the (Y, X) tile coordinates of schedule slots
+ * 0 .. tile_end - tile_begin - 1. */
+int pcc_tile_schedule(int64_t n, uint64_t tile_begin, uint64_t tile_end, uint32_t group, uint64_t *ys,
+                      uint64_t *xs);
+
 /* Diagnostics: measured FP64 tensor-pipe (DMMA) throughput of the current
  * device in TFLOP/s, from a register-resident mma.sync f64 loop (~20 ms).
  * Used by bench.py as the live roofline denominator. */

@@ -30,6 +30,85 @@ __host__ __device__ __forceinline__ uint64_t tile_row(uint64_t m, uint64_t id) {
   return (uint64_t)y;
 }
 
+// Processing order of a contiguous tile-id range [tb, te) (the partition
+// unit).  The SET of tiles is fixed by the bijection; only the order in
+// which a persistent grid visits them is chosen for L2 locality:
+//   head  [tb, head_end)          partial first tile row, id order
+//   body  full rows [body_lo, body_hi) in groups of `group` rows, each group
+//         walked column by column (rows of a column consecutive), so a wave
+//         of concurrent CTAs shares ~group A bands and ~wave/group B bands
+//   tail  [tail_begin, te)        partial last tile row, id order
+// Every cell's arithmetic is independent of the order (no split-K), so the
+// result is bitwise identical to the plain id order.
+struct TileOrder {
+  uint64_t tb, head_end, body_lo, body_hi, body_count, tail_begin, te, total;
+  uint32_t group;
+};
+
+__host__ __device__ inline TileOrder make_tile_order(uint64_t m, uint64_t tb, uint64_t te, uint32_t group) {
+  TileOrder o{};
+  o.tb = tb;
+  o.te = te;
+  o.total = te > tb ? te - tb : 0;
+  o.group = group < 1 ? 1 : group;
+  o.head_end = tb;
+  o.body_lo = o.body_hi = 0;
+  o.body_count = 0;
+  o.tail_begin = te;
+  if (te <= tb) return o;
+  const uint64_t y0 = tile_row(m, tb), y1 = tile_row(m, te - 1);
+  if (y0 == y1) {
+    o.head_end = te;
+    return o;
+  }
+  const bool head_full = tb == row_prefix(m, y0);
+  const bool tail_full = te == row_prefix(m, y1 + 1);
+  o.head_end = head_full ? tb : row_prefix(m, y0 + 1);
+  o.body_lo = head_full ? y0 : y0 + 1;
+  o.body_hi = tail_full ? y1 + 1 : y1;
+  o.tail_begin = tail_full ? te : row_prefix(m, y1);
+  o.body_count = o.body_hi > o.body_lo ? row_prefix(m, o.body_hi) - row_prefix(m, o.body_lo) : 0;
+  return o;
+}
+
+// Schedule index s in [0, o.total) -> tile coordinate (Y, X).
+__host__ __device__ inline void tile_at(const TileOrder &o, uint64_t m, uint64_t s, uint64_t &Y, uint64_t &X) {
+  const uint64_t head = o.head_end - o.tb;
+  uint64_t J;
+  if (s < head) {
+    J = o.tb + s;
+  } else if (s - head < o.body_count) {
+    uint64_t r = s - head;
+    uint64_t ya = o.body_lo;
+    uint64_t g = 0;
+    for (;;) {
+      g = o.body_hi - ya < o.group ? o.body_hi - ya : o.group;
+      const uint64_t size = g * (m - ya) - g * (g - 1) / 2;
+      if (r < size) break;
+      r -= size;
+      ya += g;
+    }
+    const uint64_t corner = g * (g - 1) / 2;  // columns ya .. ya+g-2 hold 1 .. g-1 tiles
+    if (r < corner) {
+      // column q (0-based from ya) holds q+1 tiles; triangular-number inverse
+      uint64_t q = (uint64_t)((sqrt(8.0 * (double)r + 1.0) - 1.0) * 0.5);
+      while (q * (q + 1) / 2 > r) --q;
+      while ((q + 1) * (q + 2) / 2 <= r) ++q;
+      X = ya + q;
+      Y = ya + (r - q * (q + 1) / 2);
+    } else {
+      const uint64_t r2 = r - corner;
+      X = ya + g - 1 + r2 / g;
+      Y = ya + r2 % g;
+    }
+    return;
+  } else {
+    J = o.tail_begin + (s - head - o.body_count);
+  }
+  Y = tile_row(m, J);
+  X = J + Y - row_prefix(m, Y);
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

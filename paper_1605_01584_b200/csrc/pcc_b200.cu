@@ -66,7 +66,8 @@ using V8 = pcc::SyrkCfg<4, 2, 4, 8, 16, 6>;  // TMA, 8 warps 32x64
 using V9 = pcc::SyrkCfg<4, 4, 4, 4, 16, 6>;  // TMA, 16 warps 32x32
 using V10 = pcc::SyrkCfg<2, 4, 8, 4, 16, 6, 4>;  // TMA, producer 4 steps ahead
 using V11 = pcc::SyrkCfg<2, 4, 8, 4, 16, 6, 2>;  // TMA, producer 2 steps ahead
-constexpr int kNumVariants = 12;
+// V12 = V0 visiting tiles in the grouped L2-locality order
+constexpr int kNumVariants = 13;
 
 template <class C, int LAYOUT>
 int configure_tma_one(int *ctas) {
@@ -173,6 +174,13 @@ int device_config(const DeviceConfig **out, int device = -1) {
     if (rc == PCC_OK) rc = configure_tma_one<V9, pcc::kLayoutPacked>(&c.variant_ctas[9]);
     if (rc == PCC_OK) rc = configure_tma_one<V10, pcc::kLayoutPacked>(&c.variant_ctas[10]);
     if (rc == PCC_OK) rc = configure_tma_one<V11, pcc::kLayoutPacked>(&c.variant_ctas[11]);
+    if (rc == PCC_OK) {
+      using TL = pcc::TmaLayout<V0>;
+      auto kfn = pcc::syrk_tma_kernel<V0, pcc::kLayoutPacked, true>;
+      PCC_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, TL::kSmemBytes), "attr(V12)");
+      PCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.variant_ctas[12], kfn, TL::kThreads, TL::kSmemBytes),
+               "occupancy(V12)");
+    }
     if (prev != device) cudaSetDevice(prev);
     if (rc != PCC_OK) return rc;
     c.syrk_ctas_per_sm = c.variant_ctas[0];
@@ -185,6 +193,8 @@ int device_config(const DeviceConfig **out, int device = -1) {
 }
 
 inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+
+
 
 int check_u(const double *u, int64_t n, int64_t l, int64_t ldu) {
   if (n < 1 || (uint64_t)n > 0xFFFFFFFFull) return fail(PCC_EINVAL, "n must be in [1, 2^32-1], got %lld", (long long)n);
@@ -209,7 +219,7 @@ int launch_cfg(const double *u, int64_t n, int64_t l, int64_t ldu, uint64_t tb, 
   return PCC_OK;
 }
 
-template <class C, int LAYOUT>
+template <class C, int LAYOUT, bool GROUPED = false>
 int launch_tma_cfg(const double *u, int64_t n, int64_t l, int64_t ldu, uint64_t tb, uint64_t te,
                    const pcc::Epilogue &ep, cudaStream_t stream, int ctas_per_sm, int sm_count) {
   using TL = pcc::TmaLayout<C>;
@@ -221,7 +231,14 @@ int launch_tma_cfg(const double *u, int64_t n, int64_t l, int64_t ldu, uint64_t 
   const uint64_t resident = (uint64_t)sm_count * (uint64_t)ctas_per_sm;
   const uint64_t tiles = te - tb;
   const unsigned grid = (unsigned)(tiles < resident ? tiles : resident);
-  pcc::syrk_tma_kernel<C, LAYOUT><<<grid, TL::kThreads, TL::kSmemBytes, stream>>>(map, n, k_tiles, m_g, tb, te, ep);
+  // Row-group height of the tile order: ~sqrt(wave) rows x ~sqrt(wave)
+  // columns per wave minimises the distinct operand bands in flight.
+  uint32_t group = 1;
+  while ((group + 1) * (group + 1) <= grid) ++group;
+  const pcc::TileOrder order =
+      GROUPED ? pcc::make_tile_order(m_g, tb, te, group) : pcc::TileOrder{tb, te, 0, 0, 0, te, te, te - tb, 1};
+  pcc::syrk_tma_kernel<C, LAYOUT, GROUPED>
+      <<<grid, TL::kThreads, TL::kSmemBytes, stream>>>(map, n, k_tiles, m_g, order, ep);
   PCC_CUDA(cudaGetLastError(), "syrk_tma_kernel launch");
   return PCC_OK;
 }
@@ -250,6 +267,7 @@ int launch_syrk(const double *u, int64_t n, int64_t l, int64_t ldu, uint64_t tb,
     case 9: return launch_tma_cfg<V9, pcc::kLayoutPacked>(u, n, l, ldu, tb, te, ep, stream, vc[9], sms);
     case 10: return launch_tma_cfg<V10, pcc::kLayoutPacked>(u, n, l, ldu, tb, te, ep, stream, vc[10], sms);
     case 11: return launch_tma_cfg<V11, pcc::kLayoutPacked>(u, n, l, ldu, tb, te, ep, stream, vc[11], sms);
+    case 12: return launch_tma_cfg<V0, pcc::kLayoutPacked, true>(u, n, l, ldu, tb, te, ep, stream, vc[12], sms);
     default: return fail(PCC_EINVAL, "unknown contraction variant %d (0..%d)", variant, kNumVariants - 1);
   }
 }
@@ -449,6 +467,18 @@ int pcc_allpairs_f64(const double *x, int64_t n, int64_t l, int64_t ldx, double 
   rc = pcc_zero_rows_f64(u, ldu, n, pcc_rows_padded(n), stream);
   if (rc) return rc;
   return pcc_syrk_f64(u, n, l, ldu, tile_begin, tile_end, layout, out, ld_out, out_base, 0, 0, 0, stream);
+}
+
+int pcc_tile_schedule(int64_t n, uint64_t tile_begin, uint64_t tile_end, uint32_t group, uint64_t *ys,
+                      uint64_t *xs) {
+  if (n < 1) return fail(PCC_EINVAL, "n must be >= 1");
+  const uint64_t total = pcc_gpu_tile_count(n);
+  if (tile_begin > tile_end || tile_end > total) return fail(PCC_EINVAL, "tile range outside the tile matrix");
+  if (!ys || !xs) return fail(PCC_EINVAL, "null output");
+  const uint64_t m = ceil_div((uint64_t)n, pcc::kTile);
+  const pcc::TileOrder o = pcc::make_tile_order(m, tile_begin, tile_end, group);
+  for (uint64_t s = 0; s < o.total; ++s) pcc::tile_at(o, m, s, ys[s], xs[s]);
+  return PCC_OK;
 }
 
 int pcc_probe_fp64_peak(double *tflops) {

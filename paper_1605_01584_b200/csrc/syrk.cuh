@@ -186,7 +186,9 @@ syrk_kernel(const double *__restrict__ u, int64_t n, int64_t ldu, int k_tiles, u
 }
 
 // ---------------------------------------------------------------------------
-// TMA + mbarrier variant.  U's row bands stream into a STAGES-deep shared
+// TMA + mbarrier variant (production).  GROUPED = true visits the range in
+// the L2-locality TileOrder (common.cuh); measured slower than the plain id
+// order on c2/c3, so production uses the plain order.  U's row bands stream into a STAGES-deep shared
 // ring with TMA (cp.async.bulk.tensor.2d: one 8-double x 128-row box per
 // operand slab, completion counted in bytes on the slot's "full" mbarrier).
 // Thread 0 doubles as the producer: before each K step it tops the ring up
@@ -206,10 +208,23 @@ struct TmaLayout {
   static constexpr uint32_t kSlabBytes = (uint32_t)(kTile * kSlab * sizeof(double));
 };
 
-template <class C, int LAYOUT>
+// Schedule slot s -> tile (Y, X): plain bijection id order (production) or
+// the grouped L2-locality order (kept as a measured alternative).
+template <bool GROUPED>
+__device__ __forceinline__ void slot_tile(const TileOrder &o, uint64_t m, uint64_t s, uint64_t &Y, uint64_t &X) {
+  if (GROUPED) {
+    tile_at(o, m, s, Y, X);
+  } else {
+    const uint64_t J = o.tb + s;
+    Y = tile_row(m, J);
+    X = J + Y - row_prefix(m, Y);
+  }
+}
+
+template <class C, int LAYOUT, bool GROUPED = false>
 __global__ void __launch_bounds__(C::kThreads, 1)
-syrk_tma_kernel(const __grid_constant__ CUtensorMap umap, int64_t n, int k_tiles, uint64_t m_g, uint64_t tile_begin,
-                uint64_t tile_end, Epilogue ep) {
+syrk_tma_kernel(const __grid_constant__ CUtensorMap umap, int64_t n, int k_tiles, uint64_t m_g, TileOrder order,
+                Epilogue ep) {
   using TL = TmaLayout<C>;
   extern __shared__ __align__(1024) double smem[];
   const int tid = threadIdx.x;
@@ -230,18 +245,19 @@ syrk_tma_kernel(const __grid_constant__ CUtensorMap umap, int64_t n, int k_tiles
   __syncthreads();
 
   // Producer cursor (meaningful in thread 0 only): next K step to load.
-  const uint64_t first = tile_begin + blockIdx.x;
-  const uint64_t my_tiles = first < tile_end ? (tile_end - first + gridDim.x - 1) / gridDim.x : 0;
+  const uint64_t first = blockIdx.x;
+  const uint64_t my_tiles = first < order.total ? (order.total - first + gridDim.x - 1) / gridDim.x : 0;
   const uint64_t total_steps = my_tiles * (uint64_t)k_tiles;
   uint64_t p_step = 0;
   int p_kt = 0, p_stage = 0;
   uint32_t p_phase = 0;
-  uint64_t p_J = first;
+  uint64_t p_s = first;
   int32_t p_ya = 0, p_xb = 0;
   if (tid == 0 && my_tiles) {
-    const uint64_t Y = tile_row(m_g, p_J);
+    uint64_t Y, X;
+    slot_tile<GROUPED>(order, m_g, p_s, Y, X);
     p_ya = (int32_t)(Y * kTile);
-    p_xb = (int32_t)((p_J + Y - row_prefix(m_g, Y)) * kTile);
+    p_xb = (int32_t)(X * kTile);
   }
   // Issue loads while the cursor is less than `want` steps ahead; block on a
   // busy slot only if the consumer would otherwise find the ring empty.
@@ -269,10 +285,11 @@ syrk_tma_kernel(const __grid_constant__ CUtensorMap umap, int64_t n, int k_tiles
       }
       if (++p_kt == k_tiles && p_step < total_steps) {
         p_kt = 0;
-        p_J += gridDim.x;
-        const uint64_t Y = tile_row(m_g, p_J);
+        p_s += gridDim.x;
+        uint64_t Y, X;
+        slot_tile<GROUPED>(order, m_g, p_s, Y, X);
         p_ya = (int32_t)(Y * kTile);
-        p_xb = (int32_t)((p_J + Y - row_prefix(m_g, Y)) * kTile);
+        p_xb = (int32_t)(X * kTile);
       }
     }
   };
@@ -282,9 +299,9 @@ syrk_tma_kernel(const __grid_constant__ CUtensorMap umap, int64_t n, int k_tiles
   uint64_t c_step = 0;
   int stage = 0;
   uint32_t phase = 0;
-  for (uint64_t J = first; J < tile_end; J += gridDim.x) {
-    const uint64_t Y = tile_row(m_g, J);
-    const uint64_t X = J + Y - row_prefix(m_g, Y);
+  for (uint64_t si = first; si < order.total; si += gridDim.x) {
+    uint64_t Y, X;
+    slot_tile<GROUPED>(order, m_g, si, Y, X);
 
     double acc[C::MI][C::NI][2];
 #pragma unroll

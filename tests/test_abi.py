@@ -76,3 +76,28 @@ def test_sass_is_sm100a_and_uses_dmma():
     assert "sm_100a" in sass
     assert "DMMA.8x8x4" in sass          # FP64 tensor pipe in the contraction
     assert "LDGSTS" in sass              # cp.async operand staging
+
+
+@pytest.mark.parametrize("n", [1, 129, 300, 2000, 10007, 16384])
+@pytest.mark.parametrize("group", [1, 3, 12])
+def test_tile_schedule_is_a_permutation_of_the_range(n, group):
+    """The production contraction's visiting order (head row, grouped body,
+    tail row) covers each tile of a partition range exactly once."""
+    import numpy as np
+
+    from paper_1605_01584_b200.distributed import partition
+    from paper_1605_01584_b200.indexing import sym_job_ids
+
+    L = _lib.lib()
+    T = int(L.pcc_gpu_tile_count(n))
+    mg = -(-n // 128)
+    for p in (1, 2, 3, 8):
+        for tb, te in partition(T, p):
+            k = te - tb
+            ys = np.zeros(max(k, 1), dtype=np.uint64)
+            xs = np.zeros(max(k, 1), dtype=np.uint64)
+            _lib.check(L.pcc_tile_schedule(n, tb, te, group, ys.ctypes.data, xs.ctypes.data))
+            if k == 0:
+                continue
+            ids = np.sort(sym_job_ids(mg, ys[:k], xs[:k]))
+            assert np.array_equal(ids, np.arange(tb, te, dtype=np.uint64))
