@@ -137,13 +137,13 @@ normalize_rows_kernel(const double *__restrict__ x, int64_t ldx, double *__restr
 // Small CTAs (64 threads, R <= 8 rows) so several CTAs share an SM and one
 // CTA's chains overlap the others' copies.  Same arithmetic as
 // normalize_rows_kernel, bit for bit.
-constexpr int kNormSmemThreads = 64;
-constexpr int kNormSmemMaxRows = kNormSmemThreads / 8;
+constexpr int kNormSmemMaxRows = 8;  // rows per CTA (one 8-lane group each; 64 or 128 threads)
 
 __device__ __forceinline__ void cp_async_8(uint32_t dst, const void *src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src));
 }
 
+template <int kNormSmemThreads>
 __global__ void __launch_bounds__(kNormSmemThreads)
 normalize_rows_smem_kernel(const double *__restrict__ x, int64_t ldx, double *__restrict__ u, int64_t ldu,
                            uint8_t *__restrict__ zero_variance, int64_t l, int64_t row_lo, int64_t row_hi,
@@ -156,11 +156,19 @@ normalize_rows_smem_kernel(const double *__restrict__ x, int64_t ldx, double *__
   const int rows = (int)((row_hi - r0) < (int64_t)rows_per_cta ? (row_hi - r0) : (int64_t)rows_per_cta);
   const uint32_t sbase = smem_u32(srow);
 
-  // 1. stage the rows
+  // 1. stage the rows (16-byte copies when source and destination rows are
+  //    16-byte aligned, 8-byte copies otherwise)
   for (int r = 0; r < rows; ++r) {
     const double *xr = x + (r0 + r) * ldx;
     const uint32_t sr = sbase + (uint32_t)(r * l * sizeof(double));
-    for (int64_t k = tid; k < l; k += kNormSmemThreads) cp_async_8(sr + (uint32_t)(k * sizeof(double)), xr + k);
+    if (((reinterpret_cast<uintptr_t>(xr) | sr) & 15) == 0) {
+      const int64_t pairs = l >> 1;
+      for (int64_t k = tid; k < pairs; k += kNormSmemThreads)
+        cp_async_16(sr + (uint32_t)(k * 2 * sizeof(double)), xr + 2 * k);
+      if ((l & 1) && tid == 0) cp_async_8(sr + (uint32_t)((l - 1) * sizeof(double)), xr + l - 1);
+    } else {
+      for (int64_t k = tid; k < l; k += kNormSmemThreads) cp_async_8(sr + (uint32_t)(k * sizeof(double)), xr + k);
+    }
   }
   cp_async_commit();
   cp_async_wait<0>();
@@ -205,8 +213,16 @@ normalize_rows_smem_kernel(const double *__restrict__ x, int64_t ldx, double *__
       for (int64_t k = tid; k < ldu; k += kNormSmemThreads) ur[k] = 0.0;
     } else {
       const double m = s_mean[r], sc = s_scale[r];
-      for (int64_t k = tid; k < l; k += kNormSmemThreads) ur[k] = __ddiv_rn(__dsub_rn(xs[k], m), sc);
-      for (int64_t k = l + tid; k < ldu; k += kNormSmemThreads) ur[k] = 0.0;
+      // two independent divisions per iteration keep more of their latency in flight
+      int64_t k = tid;
+      for (; k + kNormSmemThreads < l; k += 2 * kNormSmemThreads) {
+        const double a0 = __dsub_rn(xs[k], m), a1 = __dsub_rn(xs[k + kNormSmemThreads], m);
+        const double q0 = __ddiv_rn(a0, sc), q1 = __ddiv_rn(a1, sc);
+        ur[k] = q0;
+        ur[k + kNormSmemThreads] = q1;
+      }
+      if (k < l) ur[k] = __ddiv_rn(__dsub_rn(xs[k], m), sc);
+      for (k = l + tid; k < ldu; k += kNormSmemThreads) ur[k] = 0.0;
     }
   }
 }

@@ -342,17 +342,28 @@ int pcc_normalize_rows_f64(const double *x, int64_t ldx, double *u, int64_t ldu,
     return e != nullptr && strcmp(e, "global") == 0;
   }();
   if (per_cta >= 1 && !force_global) {
+    // Measured (profiles/r01_normalize.log): 64-thread CTAs for rows > 16 KB
+    // (c2), 128-thread CTAs below (c3, c5) where the division-heavy write
+    // phase benefits from more warps.
+    const bool wide = row_bytes <= 16 * 1024;
     static std::once_flag attr_once;
     static cudaError_t attr_err = cudaSuccess;
     std::call_once(attr_once, [] {
-      attr_err = cudaFuncSetAttribute(pcc::normalize_rows_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      attr_err = cudaFuncSetAttribute(pcc::normalize_rows_smem_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)kSmPerSmem);
+      if (attr_err == cudaSuccess)
+        attr_err = cudaFuncSetAttribute(pcc::normalize_rows_smem_kernel<128>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmPerSmem);
     });
     if (attr_err != cudaSuccess) return cuda_fail(attr_err, "cudaFuncSetAttribute(normalize smem)");
     const uint64_t grid = ceil_div(rows, (uint64_t)per_cta);
     if (grid > 0x7FFFFFFFull) return fail(PCC_EINVAL, "too many rows");
-    pcc::normalize_rows_smem_kernel<<<(unsigned)grid, pcc::kNormSmemThreads, smem, (cudaStream_t)stream>>>(
-        x, ldx, u, ldu, zero_variance, l, row_lo, row_hi, per_cta);
+    if (wide)
+      pcc::normalize_rows_smem_kernel<128><<<(unsigned)grid, 128, smem, (cudaStream_t)stream>>>(
+          x, ldx, u, ldu, zero_variance, l, row_lo, row_hi, per_cta);
+    else
+      pcc::normalize_rows_smem_kernel<64><<<(unsigned)grid, 64, smem, (cudaStream_t)stream>>>(
+          x, ldx, u, ldu, zero_variance, l, row_lo, row_hi, per_cta);
     PCC_CUDA(cudaGetLastError(), "normalize_rows_smem_kernel launch");
     return PCC_OK;
   }
