@@ -33,7 +33,7 @@ from .stream import run_stream
 from .tiles import DEFAULT_TILE_SIZE, CorrelationResult, TileGeometry
 from .transform import Dataset, normalize_device
 
-__all__ = ["allpairs", "default_capacity", "DEFAULT_BUFFER_BUDGET", "plan_row_passes"]
+__all__ = ["allpairs", "default_capacity", "DEFAULT_BUFFER_BUDGET"]
 
 DEFAULT_BUFFER_BUDGET = 256 * 2**20  # engine.py:14
 
@@ -48,32 +48,6 @@ def _F(n: int, y: int) -> int:
     return (y * (2 * n + 1 - y)) >> 1
 
 
-def plan_row_passes(n: int, passes: int) -> list[tuple[int, int, int, int]]:
-    """Split the GPU tile matrix into <= ``passes`` groups of whole tile rows.
-
-    Returns ``(tile_begin, tile_end, packed_lo, packed_hi)`` per pass with
-    roughly equal tile counts; the packed ranges are contiguous and
-    disjoint and cover ``[0, n(n+1)/2)``.
-    """
-    T = _lib.GPU_TILE
-    mg = -(-n // T)
-    total = mg * (mg + 1) // 2
-    passes = max(1, min(passes, mg))
-    cuts = [0]
-    acc, y = 0, 0
-    for k in range(1, passes):
-        goal = total * k / passes
-        # take row y while its midpoint lies before the goal
-        while y < mg and acc + (mg - y) / 2 < goal:
-            acc += mg - y
-            y += 1
-        if y > cuts[-1]:
-            cuts.append(y)
-    if cuts[-1] != mg:
-        cuts.append(mg)
-    return [(_F(mg, a), _F(mg, b), _F(n, min(n, a * T)), _F(n, min(n, b * T))) for a, b in zip(cuts, cuts[1:])]
-
-
 def _host_out(out, total: int) -> torch.Tensor:
     if out is None:
         return torch.from_numpy(np.empty(total, dtype=np.float64))
@@ -85,7 +59,7 @@ def _host_out(out, total: int) -> torch.Tensor:
     return t
 
 
-def _allpairs_one_device(dataset: Dataset, device: torch.device, keep_on_device: bool, out, passes: int,
+def _allpairs_one_device(dataset: Dataset, device: torch.device, keep_on_device: bool, out, chunk_rows: int,
                          output: str):
     n, l = dataset.n, dataset.l
     L = _lib.lib()
@@ -105,7 +79,7 @@ def _allpairs_one_device(dataset: Dataset, device: torch.device, keep_on_device:
         T = int(L.pcc_gpu_tile_count(n))
         packed = torch.empty(total, dtype=torch.float64, device=device)
         host = None if keep_on_device else _host_out(out, total)
-        _, flags, _ = run_stream(dataset.values, n, l, device, 0, T, packed, 0, host, 0, chunks=passes * 2)
+        _, flags, _ = run_stream(dataset.values, n, l, device, 0, T, packed, 0, host, 0, chunk_rows=chunk_rows)
         zv = frozenset(np.flatnonzero(flags.cpu().numpy()).tolist())
         if keep_on_device:
             return packed, zv
@@ -125,7 +99,7 @@ def allpairs(
     output: str = "packed",
     keep_on_device: bool = False,
     out=None,
-    passes: int = 8,
+    chunk_rows: int = 4,
 ):
     """All-pairs Pearson correlation of ``dataset`` on B200 GPUs (engine.py:23-56).
 
@@ -141,8 +115,8 @@ def allpairs(
       in ``CorrelationResult.packed``);
     * ``out``: caller-owned host float64 buffer for the packed result (pinned
       memory makes the device-to-host copies asynchronous);
-    * ``passes``: upload granularity (``2 * passes`` bottom-up row chunks);
-      contraction passes are whole waves, see ``stream.plan_stream``.
+    * ``chunk_rows``: upload granularity in 128-row GPU tile rows; each
+      uploaded chunk releases one contraction pass (``stream.plan_stream``).
     """
     if not isinstance(dataset, Dataset):
         from .fileio import load_dataset
@@ -165,7 +139,7 @@ def allpairs(
     if workers > 1 or len(devs) > 1:
         raise ValueError("multi-worker runs support output='packed' gathered to host "
                          "(use run_workers(..., gather=False) for device-resident shards)")
-    res, zv = _allpairs_one_device(dataset, devs[0], keep_on_device, out, passes, output)
+    res, zv = _allpairs_one_device(dataset, devs[0], keep_on_device, out, chunk_rows, output)
     if output == "dense":
         return res, zv
     return CorrelationResult(n=dataset.n, packed=res, zero_variance=zv)

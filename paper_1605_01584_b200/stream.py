@@ -3,8 +3,10 @@
 B200 with three engines working at once.
 
     copy-in stream   X row chunks, host -> HBM, bottom rows first
-    compute stream   K1 normalize per arrived chunk, then K2 contraction
-                     passes over the tile range from the END backwards
+    compute stream   K1 normalize per arrived chunk
+    pass streams     K2 contraction passes over the tile range from the END
+                     backwards, each released by the chunk it needs (4
+                     rotating streams: small early passes run concurrently)
     copy-out stream  each pass's completed packed rows, HBM -> host
 
 Why bottom-up: tile (Y, X) needs the row bands Y and X >= Y, so a tile row Y
@@ -13,7 +15,8 @@ rows first lets the contraction start after a fraction of the upload, and
 the packed rows of finished tile rows leave the device while later passes
 run.  Pass sizes are whole waves (SMs x resident CTAs) so no pass ends on a
 partially idle wave; they ramp up (start early) and down (a short final pass
-leaves little copy-out exposed at the end).
+leaves little copy-out exposed at the end).  Passes of different streams
+overlap, so a pass's partial last wave is filled by the next pass's CTAs.
 
 Results do not depend on the schedule: every cell's K order is fixed by the
 kernel (see csrc/syrk.cuh), so this path is bitwise identical to a single
@@ -62,60 +65,73 @@ def wave_plan(waves: int, mid: int = 8) -> list[int]:
 
 @dataclass(frozen=True)
 class StreamPlan:
-    row_lo: int                         # first job row the range needs (upload/normalise [row_lo, n))
+    row_lo: int                          # first job row the range needs (upload/normalise [row_lo, n))
     chunks: tuple[tuple[int, int], ...]  # upload/normalise order: bottom-up row chunks
-    passes: tuple[tuple[int, int, int, int], ...]  # (tile_lo, tile_hi, need_row, copy_lo_row) in launch order
+    # launch order: (tile_lo, tile_hi, chunks_needed, done_row); the pass may
+    # start once the first `chunks_needed` chunks are normalised; after it
+    # (and every earlier pass) packed rows >= done_row are final
+    passes: tuple[tuple[int, int, int, int], ...]
 
 
-def plan_stream(n: int, tile_begin: int, tile_end: int, wave: int, chunks: int = 16, mid: int = 8) -> StreamPlan:
+def plan_stream(n: int, tile_begin: int, tile_end: int, wave: int, chunk_rows: int = 4, mid: int = 8) -> StreamPlan:
     """Plan the streamed execution of GPU tiles ``[tile_begin, tile_end)``.
 
-    ``need_row``: rows ``[need_row, n)`` must be normalised before the pass;
-    ``copy_lo_row``: after the pass, packed rows ``>= copy_lo_row`` (within
-    the range's span) are final.
+    X arrives bottom-up in chunks of ``chunk_rows`` GPU tile rows.  Each
+    chunk releases the tiles whose row band it completes (tile row Y needs
+    bands >= Y only) as one pass; passes run on rotating streams, so the
+    small early ones share the GPU instead of queueing behind each other.
+    The last chunk's tiles end in a ramp-down of whole waves (..., 2, 1, 1)
+    so little download remains exposed after the final pass.
     """
     mg = -(-n // T_G)
     if tile_end <= tile_begin:
         return StreamPlan(n, (), ())
     y_first = sym_job_coord(mg, tile_begin).y
     row_lo = y_first * T_G
-    # bottom-up row chunks aligned to the GPU tile
-    bands = mg - y_first
-    k = max(1, min(chunks, bands))
-    per = -(-bands // k)
-    cuts = []
+    chunk_rows = max(1, chunk_rows)
+    # bottom-up row chunks aligned to the GPU tile (the lowest one may be short)
+    bands = []
     top = mg
     while top > y_first:
-        b = max(y_first, top - per)
-        cuts.append((b * T_G, min(n, top * T_G)))
+        b = max(y_first, top - chunk_rows)
+        bands.append((b, top))
         top = b
-    total = tile_end - tile_begin
-    waves = -(-total // wave)
-    sizes = [w * wave for w in wave_plan(waves, mid)]
-    # the partial wave goes to the first (bottom-most) pass, hidden under the upload
-    excess = sum(sizes) - total
-    sizes[0] -= excess
-    if sizes[0] <= 0:
-        sizes[1] += sizes[0]
-        sizes.pop(0)
+    chunks = tuple((b * T_G, min(n, t * T_G)) for b, t in bands)
+    groups = []  # (tile_lo, tile_hi, chunks_needed) per chunk, descending tiles
+    for c, (b, t) in enumerate(bands):
+        lo = max(tile_begin, _F(mg, b))
+        hi = min(tile_end, _F(mg, t))
+        if hi > lo:
+            groups.append((lo, hi, c + 1))
     passes = []
-    hi = tile_end
-    for s in sizes:
-        lo = hi - s
-        y_lo, x_lo = sym_job_coord(mg, lo)
-        need = y_lo * T_G
-        # tile rows fully done once every tile from the row's first tile up is computed
-        row_first = _F(mg, y_lo)
-        done_y = y_lo if lo == row_first else y_lo + 1
+
+    def add(lo, hi, need):
+        y_lo = sym_job_coord(mg, lo).y
+        done_y = y_lo if lo == _F(mg, y_lo) else y_lo + 1
         passes.append((lo, hi, need, min(n, done_y * T_G)))
-        hi = lo
-    assert hi == tile_begin
-    return StreamPlan(row_lo, tuple(cuts), tuple(passes))
+
+    for i, (lo, hi, need) in enumerate(groups):
+        if i < len(groups) - 1:
+            add(lo, hi, need)
+            continue
+        # last group: ramp down so the final passes (and their downloads) are short
+        ramp = [w * wave for w in reversed([1, 1, 2, 4, mid])]
+        tail = []
+        h = lo
+        for r in reversed(ramp):  # 1, 1, 2, 4, mid waves from the bottom of the id range
+            if hi - h - r < wave:
+                break
+            tail.append((h, h + r))
+            h += r
+        add(h, hi, need)
+        for a, b in reversed(tail):
+            add(a, b, need)
+    return StreamPlan(row_lo, chunks, tuple(passes))
 
 
 def run_stream(x, n: int, l: int, device: torch.device, tile_begin: int, tile_end: int,
                out_dev: torch.Tensor, out_base: int, host_out: torch.Tensor | None,
-               host_base: int = 0, chunks: int = 16):
+               host_base: int = 0, chunk_rows: int = 4, trace: list | None = None):
     """Execute GPU tiles ``[tile_begin, tile_end)`` with overlapped upload,
     normalisation, contraction and download.
 
@@ -123,19 +139,29 @@ def run_stream(x, n: int, l: int, device: torch.device, tile_begin: int, tile_en
     tensor (already resident: no upload).  ``out_dev``: device packed span,
     ``out_dev[i - out_base]`` holds packed cell ``i``.  ``host_out``: if given,
     ``host_out[i - host_base]`` receives every packed cell of the range's span.
-    Returns ``(u, flags)`` (device) after the host has synchronised.
+    ``trace``: if a list is given, ``(label, cuda.Event)`` pairs are appended
+    for the upload, pass and download milestones (tools/trace_stream.py).
+    Returns ``(u, flags, x_device)`` after the host has synchronised.
     """
+
+    def mark(label, stream):
+        if trace is not None:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record(stream)
+            trace.append((label, ev))
+
     L = _lib.lib()
     with torch.cuda.device(device):
         info = _lib.device_info(device.index)
         wave = info.sm_count * info.syrk_ctas_per_sm
-        plan = plan_stream(n, tile_begin, tile_end, wave, chunks)
+        plan = plan_stream(n, tile_begin, tile_end, wave, chunk_rows)
         compute = torch.cuda.current_stream()
         s = stream_handle(compute)
         rows_pad = int(L.pcc_rows_padded(n))
         ldu = int(L.pcc_ldu(l))
         u = torch.empty((rows_pad, ldu), dtype=torch.float64, device=device)
         flags = torch.zeros(n, dtype=torch.uint8, device=device)
+        mark("start", compute)
         _lib.check(L.pcc_zero_rows_f64(ptr(u), ldu, n, rows_pad, s), "pad rows")
 
         on_device = isinstance(x, torch.Tensor) and x.is_cuda
@@ -156,54 +182,65 @@ def run_stream(x, n: int, l: int, device: torch.device, tile_begin: int, tile_en
                     ev = torch.cuda.Event()
                     ev.record(copy_in)
                     up_events.append(ev)
+                    mark(f"upload rows [{lo},{hi})", copy_in)
         if host_out is not None:
             copy_out = torch.cuda.Stream(device)
             pinned_out = host_out.is_pinned()
 
         span_lo = out_base
         span_hi = out_base + out_dev.numel()
-        normalized = 0  # chunks normalised so far (bottom-up)
-        copied_to_row = n  # packed rows >= this are already downloaded
-        for p_lo, p_hi, need_row, done_row in plan.passes:
-            while normalized < len(plan.chunks) and plan.chunks[normalized][1] > need_row:
-                lo, hi = plan.chunks[normalized]
+        workers = [torch.cuda.Stream(device) for _ in range(min(4, max(1, len(plan.passes))))]
+        for w in workers:
+            w.wait_stream(compute)  # u / out_dev allocations precede every pass
+        norm_done = []  # event after chunk i is normalised (compute stream)
+
+        def normalise_through(count):
+            while len(norm_done) < count:
+                i = len(norm_done)
+                lo, hi = plan.chunks[i]
                 if up_events is not None:
-                    compute.wait_event(up_events[normalized])
+                    compute.wait_event(up_events[i])
                 _lib.check(L.pcc_normalize_rows_f64(ptr(xd), xd.stride(0), ptr(u), ldu, ptr(flags), l, lo, hi, s),
                            "normalize")
-                normalized += 1
+                ev = torch.cuda.Event()
+                ev.record(compute)
+                norm_done.append(ev)
+
+        copied_to_row = n  # packed rows >= this are already downloaded
+        for k, (p_lo, p_hi, need, done_row) in enumerate(plan.passes):
+            normalise_through(need)
+            ws = workers[k % len(workers)]
+            ws.wait_event(norm_done[need - 1])
             _lib.check(L.pcc_syrk_f64(ptr(u), n, l, ldu, p_lo, p_hi, _lib.LAYOUT_PACKED, ptr(out_dev), 0, out_base,
-                                      0, 0, 0, s), "syrk")
-            if host_out is not None and done_row < copied_to_row:
-                a = max(span_lo, _F(n, done_row))
-                b = min(span_hi, _F(n, copied_to_row))
-                if b > a:
-                    ev = torch.cuda.Event()
-                    ev.record(compute)
-                    copy_out.wait_event(ev)
-                    with torch.cuda.stream(copy_out):
-                        host_out[a - host_base:b - host_base].copy_(out_dev[a - out_base:b - out_base],
-                                                                    non_blocking=pinned_out)
-                copied_to_row = done_row
-        # any rows the range did not finish (its first, partial tile row) and
-        # never-normalised chunks (rows the range does not touch)
-        while normalized < len(plan.chunks):
-            lo, hi = plan.chunks[normalized]
-            if up_events is not None:
-                compute.wait_event(up_events[normalized])
-            _lib.check(L.pcc_normalize_rows_f64(ptr(xd), xd.stride(0), ptr(u), ldu, ptr(flags), l, lo, hi, s),
-                       "normalize")
-            normalized += 1
+                                      0, 0, 0, stream_handle(ws)), "syrk")
+            done = torch.cuda.Event()
+            done.record(ws)
+            mark(f"pass tiles [{p_lo},{p_hi})", ws)
+            if host_out is not None:
+                copy_out.wait_event(done)  # in-order: every earlier pass is waited on too
+                if done_row < copied_to_row:
+                    a = max(span_lo, _F(n, done_row))
+                    b = min(span_hi, _F(n, copied_to_row))
+                    if b > a:
+                        with torch.cuda.stream(copy_out):
+                            host_out[a - host_base:b - host_base].copy_(out_dev[a - out_base:b - out_base],
+                                                                        non_blocking=pinned_out)
+                        mark(f"download {8 * (b - a) / 1e6:.0f} MB", copy_out)
+                    copied_to_row = done_row
+        # chunks no pass needed (rows above the range's first tile row are not uploaded;
+        # the range's own first partial row is covered by its chunk)
+        normalise_through(len(plan.chunks))
+        for w in workers:
+            compute.wait_stream(w)
         if host_out is not None:
             a = span_lo
             b = min(span_hi, _F(n, copied_to_row))
             if b > a:
-                ev = torch.cuda.Event()
-                ev.record(compute)
-                copy_out.wait_event(ev)
+                copy_out.wait_stream(compute)
                 with torch.cuda.stream(copy_out):
                     host_out[a - host_base:b - host_base].copy_(out_dev[a - out_base:b - out_base],
                                                                 non_blocking=pinned_out)
+                mark(f"download {8 * (b - a) / 1e6:.0f} MB (final)", copy_out)
             copy_out.synchronize()
         compute.synchronize()
         return u, flags, xd

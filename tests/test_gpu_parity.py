@@ -184,8 +184,8 @@ def test_schedule_invariance_bitwise(rng):
     for workers in (2, 3, 5, 8):
         got = pc.allpairs(pc.Dataset(values=x), workers=workers)
         assert np.array_equal(got.packed, ref)
-    for passes in (1, 2, 7):
-        got = pc.allpairs(pc.Dataset(values=x), passes=passes)
+    for chunk_rows in (1, 2, 7):
+        got = pc.allpairs(pc.Dataset(values=x), chunk_rows=chunk_rows)
         assert np.array_equal(got.packed, ref)
     for t in (1, 4, 16):
         got = pc.allpairs(pc.Dataset(values=x), tile_size=t, threads=3)
@@ -303,7 +303,7 @@ def test_streamed_upload_from_pageable_and_device_inputs(rng):
     x = random_values(rng, 900, 64, special_rows=True)
     ref, zv = oracle.allpairs(x, t=4)
     for values in (x, torch.from_numpy(x), torch.from_numpy(x).cuda()):
-        res = pc.allpairs(pc.Dataset(values=values), passes=3)
+        res = pc.allpairs(pc.Dataset(values=values), chunk_rows=3)
         _assert_parity(res.packed, ref, frozenset(np.flatnonzero(zv).tolist()), 900)
 
 

@@ -14,7 +14,7 @@ from hypothesis import strategies as st
 import oracle
 import paper_1605_01584_b200 as pc
 from paper_1605_01584_b200.distributed import owned_runs, partition, shard_span
-from paper_1605_01584_b200.engine import plan_row_passes
+from paper_1605_01584_b200.stream import plan_stream
 from paper_1605_01584_b200.tiles import _scatter_host
 
 from conftest import GOLDEN, random_values, triangle_walk
@@ -123,15 +123,30 @@ def test_plan_passes():
 
 
 @pytest.mark.parametrize("n", [1, 127, 128, 129, 2000, 10007, 16384, 65536])
-@pytest.mark.parametrize("passes", [1, 3, 8, 64])
-def test_row_passes_cover_packed_and_tiles(n, passes):
-    ps = plan_row_passes(n, passes)
+@pytest.mark.parametrize("chunk_rows", [1, 3, 4, 64])
+@pytest.mark.parametrize("p", [1, 3])
+def test_stream_plan_covers_range_and_respects_dependencies(n, chunk_rows, p):
+    """Streamed passes (stream.plan_stream) tile each partition range exactly
+    once, in descending id order, never before the chunk holding their first
+    tile row is normalised, and the rows they mark final are complete."""
     mg = -(-n // 128)
-    assert ps[0][0] == 0 and ps[-1][1] == mg * (mg + 1) // 2
-    assert ps[0][2] == 0 and ps[-1][3] == n * (n + 1) // 2
-    for a, b in zip(ps, ps[1:]):
-        assert a[1] == b[0] and a[3] == b[2]
-    assert all(p[1] > p[0] and p[3] > p[2] for p in ps)
+    T = mg * (mg + 1) // 2
+    for tb, te in partition(T, p):
+        sp = plan_stream(n, tb, te, 148, chunk_rows)
+        if te == tb:
+            assert sp.passes == ()
+            continue
+        assert sp.passes[0][1] == te and sp.passes[-1][0] == tb
+        for a, b in zip(sp.passes, sp.passes[1:]):
+            assert a[0] == b[1]
+        assert all(c[0] < c[1] for c in sp.chunks)
+        assert sp.chunks[0][1] == n and sp.chunks[-1][0] == sp.row_lo
+        for lo, hi, need, done in sp.passes:
+            y = pc.sym_job_coord(mg, lo).y
+            assert sp.chunks[need - 1][0] <= y * 128  # needed rows are normalised
+            # every tile of a row >= done_row // 128 lies in [lo, te)
+            if done < n:
+                assert pc.row_prefix(mg, done // 128) >= lo
 
 
 @pytest.mark.parametrize("n", [1, 5, 128, 129, 300, 1000])
