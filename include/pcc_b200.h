@@ -148,6 +148,18 @@ int pcc_allpairs_f64(const double *x, int64_t n, int64_t l, int64_t ldx, double 
                      uint8_t *zero_variance, uint64_t tile_begin, uint64_t tile_end,
                      int32_t layout, double *out, int64_t ld_out, uint64_t out_base, void *stream);
 
+/* GPU brute-force oracle (the product's `verify`): replaces
+ * _kernels.constant_row_flags / pcc_naive_pair / naive_allpairs_packed
+ * (_kernels.py:255-298), bit for bit.  pcc_row_stats_f64 computes, per row
+ * of x (n x l, stride ldx), is_constant, mean = sum8/l and ssd = ssd8 in the
+ * reference's order; pcc_naive_pairs_f64 then evaluates the definition for
+ * packed job ids [id_lo, id_hi) into out[id - id_lo]. */
+int pcc_row_stats_f64(const double *x, int64_t ldx, int64_t n, int64_t l, double *mean, double *ssd,
+                      uint8_t *constant, void *stream);
+int pcc_naive_pairs_f64(const double *x, int64_t ldx, int64_t n, int64_t l, const double *mean,
+                        const double *ssd, const uint8_t *constant, uint64_t id_lo, uint64_t id_hi,
+                        double *out, void *stream);
+
 /* Diagnostics (host only, no GPU): the order in which the production
  * contraction visits the GPU tiles [tile_begin, tile_end) -- partial first
  * row, full rows in groups of `group` rows walked column by column, partial

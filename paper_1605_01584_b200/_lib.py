@@ -52,6 +52,8 @@ EXPORTED_SYMBOLS = (
     "pcc_compute_pass_f64",
     "pcc_scatter_range_f64",
     "pcc_allpairs_f64",
+    "pcc_row_stats_f64",
+    "pcc_naive_pairs_f64",
     "pcc_tile_schedule",
     "pcc_probe_fp64_peak",
 )
@@ -93,6 +95,8 @@ def _bind(l: ctypes.CDLL) -> None:
         "pcc_compute_pass_f64": (ctypes.c_int, [_vp, _i64, _i64, _i64, _i64, _u64, _u64, _vp, _vp]),
         "pcc_scatter_range_f64": (ctypes.c_int, [_vp, _vp, _u64, _u64, _i64, _i64, _vp]),
         "pcc_allpairs_f64": (ctypes.c_int, [_vp, _i64, _i64, _i64, _vp, _i64, _vp, _u64, _u64, _i32, _vp, _i64, _u64, _vp]),
+        "pcc_row_stats_f64": (ctypes.c_int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp]),
+        "pcc_naive_pairs_f64": (ctypes.c_int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _u64, _u64, _vp, _vp]),
         "pcc_tile_schedule": (ctypes.c_int, [_i64, _u64, _u64, ctypes.c_uint32, _vp, _vp]),
         "pcc_probe_fp64_peak": (ctypes.c_int, [ctypes.POINTER(ctypes.c_double)]),
     }

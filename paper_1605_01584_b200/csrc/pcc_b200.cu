@@ -13,6 +13,7 @@
 #include "../../include/pcc_b200.h"
 #include "normalize.cuh"
 #include "syrk.cuh"
+#include "verify.cuh"
 
 namespace {
 
@@ -478,6 +479,38 @@ int pcc_allpairs_f64(const double *x, int64_t n, int64_t l, int64_t ldx, double 
   rc = pcc_zero_rows_f64(u, ldu, n, pcc_rows_padded(n), stream);
   if (rc) return rc;
   return pcc_syrk_f64(u, n, l, ldu, tile_begin, tile_end, layout, out, ld_out, out_base, 0, 0, 0, stream);
+}
+
+int pcc_row_stats_f64(const double *x, int64_t ldx, int64_t n, int64_t l, double *mean, double *ssd,
+                      uint8_t *constant, void *stream) {
+  if (n < 1 || l < 1 || ldx < l) return fail(PCC_EINVAL, "bad shape n=%lld l=%lld ldx=%lld", (long long)n,
+                                              (long long)l, (long long)ldx);
+  if (!x || !mean || !ssd || !constant) return fail(PCC_EINVAL, "null pointer");
+  pcc::row_stats_kernel<<<(unsigned)ceil_div((uint64_t)n, 32), 256, 0, (cudaStream_t)stream>>>(x, ldx, l, n, mean, ssd,
+                                                                                               constant);
+  PCC_CUDA(cudaGetLastError(), "row_stats_kernel launch");
+  return PCC_OK;
+}
+
+int pcc_naive_pairs_f64(const double *x, int64_t ldx, int64_t n, int64_t l, const double *mean, const double *ssd,
+                        const uint8_t *constant, uint64_t id_lo, uint64_t id_hi, double *out, void *stream) {
+  if (n < 1 || l < 1 || ldx < l) return fail(PCC_EINVAL, "bad shape");
+  const uint64_t total = (uint64_t)n * ((uint64_t)n + 1) / 2;
+  if (id_lo > id_hi || id_hi > total) return fail(PCC_EINVAL, "job id range [%llu, %llu) outside [0, %llu)",
+                                                  (unsigned long long)id_lo, (unsigned long long)id_hi,
+                                                  (unsigned long long)total);
+  if (id_hi == id_lo) return PCC_OK;
+  if (!x || !mean || !ssd || !constant || !out) return fail(PCC_EINVAL, "null pointer");
+  const DeviceConfig *dc = nullptr;
+  int rc = device_config(&dc);
+  if (rc) return rc;
+  uint64_t grid = ceil_div(id_hi - id_lo, 32);  // 8 warps x 4 pairs per CTA
+  const uint64_t cap = (uint64_t)dc->sm_count * 8;
+  if (grid > cap) grid = cap;
+  pcc::naive_pairs_kernel<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(x, ldx, l, n, mean, ssd, constant, id_lo,
+                                                                           id_hi, out);
+  PCC_CUDA(cudaGetLastError(), "naive_pairs_kernel launch");
+  return PCC_OK;
 }
 
 int pcc_tile_schedule(int64_t n, uint64_t tile_begin, uint64_t tile_end, uint32_t group, uint64_t *ys,

@@ -352,3 +352,40 @@ def test_full_size_configs_sampled_rows_and_properties(name):
     assert float((diag - 1.0).abs().max()) <= 1e-12
     del packed, res, nd
     torch.cuda.empty_cache()
+
+
+def test_gpu_naive_oracle_bit_exact_vs_reference_golden(golden_small):
+    """csrc/verify.cuh restates _kernels.pcc_naive_pair: the reference's own
+    allpairs_naive output (golden 'naive') must be reproduced bit for bit."""
+    for name, case in golden_small.items():
+        d = pc.Dataset(values=case["x"])
+        got = pc.naive_pairs(d).cpu().numpy()
+        assert np.array_equal(got, case["naive"]), name
+        assert pc.naive_zero_variance(d) == frozenset(np.flatnonzero(case["zv"]).tolist()), name
+
+
+def test_verify_accepts_engine_and_catches_corruption(rng):
+    x = random_values(rng, 700, 33, special_rows=True)
+    d = pc.Dataset(values=x)
+    res = pc.allpairs(d)
+    rep = pc.verify(d, res, tolerance=1e-12)
+    assert rep.ok and rep.pairs_checked == 700 * 701 // 2 and rep.max_abs_deviation <= 1e-12
+    rows = pc.verify(d, res, rows=[0, 5, 699], tolerance=1e-12)
+    assert rows.ok and rows.pairs_checked == 700 + 695 + 1
+    bad = pc.CorrelationResult(n=700, packed=res.packed.copy(), zero_variance=res.zero_variance)
+    bad.packed[pc.sym_job_id(700, 3, 400)] += 1e-9
+    with pytest.raises(pc.VerificationError) as ei:
+        pc.verify(d, bad, tolerance=1e-10)
+    assert ei.value.report.first_bad_pair == (3, 400)
+    wrong_zv = pc.CorrelationResult(n=700, packed=res.packed, zero_variance=frozenset())
+    assert not pc.verify(d, wrong_zv, raise_on_failure=False).zero_variance_match
+
+
+def test_verify_full_c3_against_gpu_oracle():
+    """Config c3 (ragged, 1% constant rows), every one of its 50 M pairs."""
+    x = make_config("c3")
+    d = pc.Dataset(values=torch.from_numpy(x).pin_memory())
+    res = pc.allpairs(d, keep_on_device=True)
+    rep = pc.verify(d, res, tolerance=1e-12)
+    assert rep.ok, rep
+    assert rep.pairs_checked == x.shape[0] * (x.shape[0] + 1) // 2
