@@ -99,7 +99,7 @@ def allpairs(
     output: str = "packed",
     keep_on_device: bool = False,
     out=None,
-    chunk_rows: int = 4,
+    chunk_rows: int = 8,
 ):
     """All-pairs Pearson correlation of ``dataset`` on B200 GPUs (engine.py:23-56).
 

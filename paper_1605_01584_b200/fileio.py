@@ -8,9 +8,11 @@ and fileio.py:1-20):
   zv_count sorted u64 | n(n+1)/2 f64`` in job-id order, so a pair lookup is
   one seek at a bijection-computed offset (``query_pair``).
 
-Only the binary dataset container and the packed result file are provided;
-text ingestion, the streaming ``PackedFileWriterSink`` and ``verify`` are
-outside this build's hot-path scope.
+Streaming the result to disk: ``PackedFileWriterSink``
+is the reference's ``ResultSink`` that writes each pass's owned cells into
+the file (fileio.py:233-274), for ``run_pipeline``; ``allpairs_to_file`` is the
+GPU fast path -- the streamed engine downloads finished packed rows straight
+into a memory map of the file's payload.  Text ingestion stays out of scope.
 """
 
 from __future__ import annotations
@@ -22,10 +24,12 @@ import numpy as np
 
 from .errors import DataError
 from .indexing import sym_job_count, sym_job_id
-from .tiles import CorrelationResult
+from .pipeline import ResultSink
+from .tiles import CorrelationResult, TileGeometry, _scatter_host
 from .transform import Dataset
 
-__all__ = ["save_dataset", "load_dataset", "save_result", "load_result", "query_pair"]
+__all__ = ["save_dataset", "load_dataset", "save_result", "load_result", "query_pair", "PackedResultReader",
+           "PackedFileWriterSink", "allpairs_to_file"]
 
 _HDR = struct.Struct("<4sIQQ")
 _VERSION = 1
@@ -102,3 +106,115 @@ def query_pair(result_path, i: int, j: int) -> float:
             raise ValueError(f"pair ({i}, {j}) outside [0, {n})")
         f.seek(_HDR.size + 8 * (zc + sym_job_id(n, min(i, j), max(i, j))))
         return float(np.frombuffer(f.read(8), dtype="<f8")[0])
+
+
+class PackedResultReader:
+    """Seek-based random access to an ``LPCR`` file (fileio.py:175-230)."""
+
+    def __init__(self, path):
+        self.path = Path(path)
+        self._f = open(self.path, "rb")
+        try:
+            self.n, zc = _result_header(self._f, self.path)
+            zv = np.fromfile(self._f, dtype="<u8", count=zc)
+            if zv.size != zc:
+                raise DataError(f"{self.path}: truncated zero-variance index list")
+            self.zero_variance = frozenset(int(i) for i in zv)
+            self._data_offset = _HDR.size + 8 * zc
+            expected = self._data_offset + 8 * sym_job_count(self.n)
+            if self.path.stat().st_size != expected:
+                raise DataError(f"{self.path}: file is {self.path.stat().st_size} bytes but header declares {expected}")
+        except Exception:
+            self._f.close()
+            raise
+
+    def query(self, i: int, j: int) -> float:
+        if not (0 <= i < self.n and 0 <= j < self.n):
+            raise ValueError(f"pair ({i}, {j}) outside [0, {self.n})")
+        self._f.seek(self._data_offset + 8 * sym_job_id(self.n, min(i, j), max(i, j)))
+        return float(np.frombuffer(self._f.read(8), dtype="<f8")[0])
+
+    def read_all(self) -> np.ndarray:
+        self._f.seek(self._data_offset)
+        return np.fromfile(self._f, dtype="<f8", count=sym_job_count(self.n)).astype(np.float64, copy=False)
+
+    def close(self) -> None:
+        self._f.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc_info):
+        self.close()
+
+
+def _create_result_file(path, n: int, zero_variance: frozenset[int]) -> np.memmap:
+    zv = np.array(sorted(zero_variance), dtype="<u8")
+    offset = _HDR.size + 8 * zv.size
+    with open(path, "wb") as f:
+        f.write(_HDR.pack(b"LPCR", _VERSION, n, zv.size))
+        f.write(zv.tobytes())
+        f.truncate(offset + 8 * sym_job_count(n))
+    return np.memmap(path, dtype="<f8", mode="r+", offset=offset, shape=(sym_job_count(n),))
+
+
+class PackedFileWriterSink(ResultSink):
+    """``ResultSink`` streaming each pass into an ``LPCR`` file (fileio.py:233-274).
+
+    Header and zero-filled payload are created up front; every consumed pass
+    scatters only the cells its tiles own (coordinate-driven), through a
+    memory map of the payload.
+    """
+
+    def __init__(self, path, geom: TileGeometry, zero_variance: frozenset[int] = frozenset()):
+        self.geom = geom
+        self._map = _create_result_file(path, geom.n, zero_variance)
+
+    def consume(self, pass_range, blocks) -> None:
+        flat = getattr(blocks, "flat", None)
+        t2 = self.geom.t * self.geom.t
+        if flat is not None and blocks and flat.shape[0] == len(blocks) * t2:
+            _scatter_host(self._map, np.asarray(flat), blocks[0].tile_id, len(blocks), self.geom)
+            return
+        for block in blocks:
+            _scatter_host(self._map, np.ascontiguousarray(block.values, dtype=np.float64), block.tile_id, 1, self.geom)
+
+    def close(self) -> None:
+        self._map.flush()
+        del self._map
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc_info):
+        self.close()
+
+
+def allpairs_to_file(dataset: Dataset, path, device=None) -> frozenset[int]:
+    """All-pairs PCC of ``dataset`` written straight to an ``LPCR`` file.
+
+    The zero-variance set (needed for the header, which precedes the
+    payload) comes from one normalisation pass; the streamed engine then
+    downloads finished packed rows directly into the file's memory map.
+    Returns the zero-variance set.
+    """
+    import torch
+
+    from . import _lib
+    from ._device import as_device_f64, resolve_devices
+    from .stream import run_stream
+    from .transform import normalize_device
+
+    dev = resolve_devices(None if device is None else [device])[0]
+    n, l = dataset.n, dataset.l
+    with torch.cuda.device(dev):
+        x = as_device_f64(dataset.values, dev)
+        _, flags = normalize_device(x)
+        zv = frozenset(np.flatnonzero(flags.cpu().numpy()).tolist())
+        payload = _create_result_file(path, n, zv)
+        T = int(_lib.lib().pcc_gpu_tile_count(n))
+        packed = torch.empty(sym_job_count(n), dtype=torch.float64, device=dev)
+        run_stream(x, n, l, dev, 0, T, packed, 0, torch.from_numpy(payload), 0)
+        payload.flush()
+        del payload
+    return zv

@@ -73,10 +73,12 @@ class StreamPlan:
     passes: tuple[tuple[int, int, int, int], ...]
 
 
-def plan_stream(n: int, tile_begin: int, tile_end: int, wave: int, chunk_rows: int = 4, mid: int = 8) -> StreamPlan:
+def plan_stream(n: int, tile_begin: int, tile_end: int, wave: int, chunk_rows: int = 8, mid: int = 8) -> StreamPlan:
     """Plan the streamed execution of GPU tiles ``[tile_begin, tile_end)``.
 
-    X arrives bottom-up in chunks of ``chunk_rows`` GPU tile rows.  Each
+    X arrives bottom-up in chunks of GPU tile rows -- 2, 2, 4, 4 rows first
+    (the contraction can start early), then ``chunk_rows`` (large copies run
+    at full PCIe rate).  Each
     chunk releases the tiles whose row band it completes (tile row Y needs
     bands >= Y only) as one pass; passes run on rotating streams, so the
     small early ones share the GPU instead of queueing behind each other.
@@ -90,10 +92,12 @@ def plan_stream(n: int, tile_begin: int, tile_end: int, wave: int, chunk_rows: i
     row_lo = y_first * T_G
     chunk_rows = max(1, chunk_rows)
     # bottom-up row chunks aligned to the GPU tile (the lowest one may be short)
+    ramp = [r for r in (2, 2, 4, 4) if r < chunk_rows]
     bands = []
     top = mg
     while top > y_first:
-        b = max(y_first, top - chunk_rows)
+        size = ramp[len(bands)] if len(bands) < len(ramp) else chunk_rows
+        b = max(y_first, top - size)
         bands.append((b, top))
         top = b
     chunks = tuple((b * T_G, min(n, t * T_G)) for b, t in bands)
@@ -131,7 +135,7 @@ def plan_stream(n: int, tile_begin: int, tile_end: int, wave: int, chunk_rows: i
 
 def run_stream(x, n: int, l: int, device: torch.device, tile_begin: int, tile_end: int,
                out_dev: torch.Tensor, out_base: int, host_out: torch.Tensor | None,
-               host_base: int = 0, chunk_rows: int = 4, trace: list | None = None):
+               host_base: int = 0, chunk_rows: int = 8, trace: list | None = None):
     """Execute GPU tiles ``[tile_begin, tile_end)`` with overlapped upload,
     normalisation, contraction and download.
 
@@ -168,73 +172,78 @@ def run_stream(x, n: int, l: int, device: torch.device, tile_begin: int, tile_en
         if on_device:
             xd = x if x.dtype == torch.float64 else x.to(torch.float64)
             xd = xd.contiguous()
-            up_events = None
         else:
             xh = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64))
-            pinned = xh.is_pinned()
+            pinned_in = xh.is_pinned()
             xd = torch.empty((n, l), dtype=torch.float64, device=device)
             copy_in = torch.cuda.Stream(device)
             copy_in.wait_stream(compute)  # xd's memory is free from the compute stream's view
-            up_events = []
-            with torch.cuda.stream(copy_in):
-                for lo, hi in plan.chunks:
-                    xd[lo:hi].copy_(xh[lo:hi], non_blocking=pinned)
-                    ev = torch.cuda.Event()
-                    ev.record(copy_in)
-                    up_events.append(ev)
-                    mark(f"upload rows [{lo},{hi})", copy_in)
+        pinned_out = host_out is not None and host_out.is_pinned()
         if host_out is not None:
             copy_out = torch.cuda.Stream(device)
-            pinned_out = host_out.is_pinned()
 
         span_lo = out_base
         span_hi = out_base + out_dev.numel()
         workers = [torch.cuda.Stream(device) for _ in range(min(4, max(1, len(plan.passes))))]
         for w in workers:
             w.wait_stream(compute)  # u / out_dev allocations precede every pass
-        norm_done = []  # event after chunk i is normalised (compute stream)
+        pass_done = []  # (event, done_row) per launched pass, in plan order
+        copied = [n]  # packed rows >= copied[0] are downloaded
 
-        def normalise_through(count):
-            while len(norm_done) < count:
-                i = len(norm_done)
-                lo, hi = plan.chunks[i]
-                if up_events is not None:
-                    compute.wait_event(up_events[i])
-                _lib.check(L.pcc_normalize_rows_f64(ptr(xd), xd.stride(0), ptr(u), ldu, ptr(flags), l, lo, hi, s),
-                           "normalize")
-                ev = torch.cuda.Event()
-                ev.record(compute)
-                norm_done.append(ev)
-
-        copied_to_row = n  # packed rows >= this are already downloaded
-        for k, (p_lo, p_hi, need, done_row) in enumerate(plan.passes):
-            normalise_through(need)
-            ws = workers[k % len(workers)]
-            ws.wait_event(norm_done[need - 1])
-            _lib.check(L.pcc_syrk_f64(ptr(u), n, l, ldu, p_lo, p_hi, _lib.LAYOUT_PACKED, ptr(out_dev), 0, out_base,
-                                      0, 0, 0, stream_handle(ws)), "syrk")
-            done = torch.cuda.Event()
-            done.record(ws)
-            mark(f"pass tiles [{p_lo},{p_hi})", ws)
-            if host_out is not None:
-                copy_out.wait_event(done)  # in-order: every earlier pass is waited on too
-                if done_row < copied_to_row:
+        def download(upto: int) -> None:
+            # copies for passes [len(done so far) .. upto): in-order waits keep every earlier pass covered
+            while download.k < upto:
+                ev, done_row = pass_done[download.k]
+                download.k += 1
+                copy_out.wait_event(ev)
+                if done_row < copied[0]:
                     a = max(span_lo, _F(n, done_row))
-                    b = min(span_hi, _F(n, copied_to_row))
+                    b = min(span_hi, _F(n, copied[0]))
                     if b > a:
                         with torch.cuda.stream(copy_out):
                             host_out[a - host_base:b - host_base].copy_(out_dev[a - out_base:b - out_base],
                                                                         non_blocking=pinned_out)
                         mark(f"download {8 * (b - a) / 1e6:.0f} MB", copy_out)
-                    copied_to_row = done_row
-        # chunks no pass needed (rows above the range's first tile row are not uploaded;
-        # the range's own first partial row is covered by its chunk)
-        normalise_through(len(plan.chunks))
+                    copied[0] = done_row
+
+        download.k = 0
+        k = 0
+        for c, (lo, hi) in enumerate(plan.chunks):
+            # upload (pageable sources block here while the GPU runs earlier passes)
+            if not on_device:
+                with torch.cuda.stream(copy_in):
+                    xd[lo:hi].copy_(xh[lo:hi], non_blocking=pinned_in)
+                    up = torch.cuda.Event()
+                    up.record(copy_in)
+                    mark(f"upload rows [{lo},{hi})", copy_in)
+                compute.wait_event(up)
+            _lib.check(L.pcc_normalize_rows_f64(ptr(xd), xd.stride(0), ptr(u), ldu, ptr(flags), l, lo, hi, s),
+                       "normalize")
+            normed = torch.cuda.Event()
+            normed.record(compute)
+            # every pass this chunk releases; the last chunk's passes (the
+            # ramp-down) share one stream so they finish -- and download -- in order
+            last = c == len(plan.chunks) - 1
+            while k < len(plan.passes) and plan.passes[k][2] == c + 1:
+                p_lo, p_hi, _, done_row = plan.passes[k]
+                ws = workers[0] if last else workers[k % len(workers)]
+                ws.wait_event(normed)
+                _lib.check(L.pcc_syrk_f64(ptr(u), n, l, ldu, p_lo, p_hi, _lib.LAYOUT_PACKED, ptr(out_dev), 0,
+                                          out_base, 0, 0, 0, stream_handle(ws)), "syrk")
+                done = torch.cuda.Event()
+                done.record(ws)
+                mark(f"pass tiles [{p_lo},{p_hi})", ws)
+                pass_done.append((done, done_row))
+                k += 1
+            if pinned_out:
+                download(len(pass_done))
+        assert k == len(plan.passes)
         for w in workers:
             compute.wait_stream(w)
         if host_out is not None:
+            download(len(pass_done))  # pageable destinations: blocking copies once all work is queued
             a = span_lo
-            b = min(span_hi, _F(n, copied_to_row))
+            b = min(span_hi, _F(n, copied[0]))
             if b > a:
                 copy_out.wait_stream(compute)
                 with torch.cuda.stream(copy_out):

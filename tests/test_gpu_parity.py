@@ -389,3 +389,22 @@ def test_verify_full_c3_against_gpu_oracle():
     rep = pc.verify(d, res, tolerance=1e-12)
     assert rep.ok, rep
     assert rep.pairs_checked == x.shape[0] * (x.shape[0] + 1) // 2
+
+
+def test_streaming_to_file_and_pageable_output(tmp_path, rng):
+    x = random_values(rng, 777, 29, special_rows=True)
+    d = pc.Dataset(values=x)
+    ref = pc.allpairs(d).packed
+    zv = pc.allpairs_to_file(d, tmp_path / "r.lpcr")
+    back = pc.load_result(tmp_path / "r.lpcr")
+    assert np.array_equal(back.packed, ref) and back.zero_variance == zv == frozenset({1})
+    assert pc.query_pair(tmp_path / "r.lpcr", 5, 700) == ref[pc.sym_job_id(777, 5, 700)]
+    out = np.full(ref.size, np.nan)               # pageable caller-owned buffer
+    r2 = pc.allpairs(d, out=out)
+    assert r2.packed is out and np.array_equal(out, ref)
+    # the reference's bounded pipeline feeding the streaming file sink
+    nd = pc.normalize(d)
+    g = pc.TileGeometry(n=777, t=4)
+    with pc.PackedFileWriterSink(tmp_path / "p.lpcr", g, nd.zero_variance) as sink:
+        pc.run_pipeline(nd, g, pc.plan_passes(0, g.total_tiles, 5000), sink)
+    assert np.array_equal(pc.load_result(tmp_path / "p.lpcr").packed, ref)

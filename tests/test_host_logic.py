@@ -304,3 +304,24 @@ def test_workloads_shapes_and_determinism():
     assert u.shape == (3, 4) and (0 <= u).all() and (u < 1).all()
     assert math.isclose(float(gen_uniform_splitmix64(1, 1, seed=0)[0, 0]),
                         float(gen_uniform_splitmix64(2, 2, seed=0)[0, 0]))
+
+
+def test_packed_file_writer_sink_streams_passes(tmp_path, rng):
+    """The reference's streaming sink (fileio.py:233-274): passes of tile
+    blocks, in any split, land at their bijection offsets in the LPCR file."""
+    x = random_values(rng, 41, 9, special_rows=True)
+    u, zv = oracle.normalize(x)
+    ref, _ = oracle.allpairs(x)
+    g = pc.TileGeometry(n=41, t=4)
+    path = tmp_path / "s.lpcr"
+    with pc.PackedFileWriterSink(path, g, frozenset({1})) as sink:
+        for lo, hi in pc.plan_passes(0, g.total_tiles, 17).passes:
+            flat = oracle.compute_pass(u, 4, lo, hi)
+            blocks = pc.BlockList(pc.TileBlock(lo + k, flat[k * 16:(k + 1) * 16]) for k in range(hi - lo))
+            blocks.flat = flat
+            sink.consume((lo, hi), blocks)
+    back = pc.load_result(path)
+    assert np.array_equal(back.packed, ref) and back.zero_variance == {1}
+    with pc.PackedResultReader(path) as r:
+        assert r.query(3, 0) == ref[pc.sym_job_id(41, 0, 3)]
+        assert np.array_equal(r.read_all(), ref)
