@@ -16,8 +16,13 @@ identical for any worker count.
 
 from __future__ import annotations
 
+import os
+import subprocess
+import sys
+import tempfile
 import threading
 from dataclasses import dataclass, field
+from pathlib import Path
 
 import numpy as np
 import torch
@@ -33,6 +38,8 @@ from .transform import Dataset, normalize_device
 __all__ = [
     "BACKENDS",
     "WorkerAssignment",
+    "WorkerReport",
+    "merge",
     "Shard",
     "ShardedResult",
     "partition",
@@ -70,6 +77,17 @@ class WorkerAssignment:
     @property
     def tile_count(self) -> int:
         return self.stop - self.start
+
+
+@dataclass
+class WorkerReport:
+    """Blocks a worker delivered (distributed.py:67-73), for ``merge``."""
+
+    worker_index: int
+    tiles_done: int = 0
+    blocks: list = field(default_factory=list)
+    status: str = "ok"
+    message: str = ""
 
 
 def gpu_geometry(n: int) -> TileGeometry:
@@ -195,6 +213,124 @@ def check_coverage(spans: list[tuple[int, int, int]], total: int) -> None:
         raise IntegrityError(f"covered {covered} tiles of {total}")
 
 
+def merge(reports: list[WorkerReport], geom: TileGeometry, zero_variance: frozenset[int] = frozenset()) -> CorrelationResult:
+    """Assemble retained worker blocks, demanding every tile exactly once (distributed.py:338-373)."""
+    from .tiles import empty_result, scatter
+
+    for r in reports:
+        if r.status != "ok":
+            raise WorkerError(f"cannot merge: worker {r.worker_index} status {r.status!r}: {r.message}",
+                              worker_index=r.worker_index)
+    total = geom.total_tiles
+    seen = np.zeros(total, dtype=np.int64)
+    for r in reports:
+        for b in r.blocks:
+            if not 0 <= b.tile_id < total:
+                raise IntegrityError(f"tile id {b.tile_id} out of range [0, {total})")
+            seen[b.tile_id] += 1
+    dup = np.flatnonzero(seen > 1)
+    if dup.size:
+        raise IntegrityError(f"duplicated tiles: {dup.tolist()[:20]}")
+    missing = np.flatnonzero(seen == 0)
+    if missing.size:
+        raise IntegrityError(f"missing tiles: {missing.tolist()[:20]}")
+    result = empty_result(geom.n, zero_variance)
+    for r in reports:
+        scatter(r.blocks, geom, result)
+    return result
+
+
+def _run_subprocess(dataset: Dataset, dataset_path: str, geom: TileGeometry, p: int, capacity: int,
+                    threads: int, devs: list[torch.device]) -> CorrelationResult:
+    """One GPU worker process per assignment, the reference's wire protocol
+    (distributed.py:209-318): BLOCKS frames are scattered into one packed
+    result as they arrive; a failing worker raises ``WorkerError`` with its
+    undelivered range."""
+    from . import protocol
+    from .tiles import _scatter_host, empty_result
+
+    assignments = make_assignments(geom, p, capacity)
+    with torch.cuda.device(devs[0]):
+        _, flags = normalize_device(as_device_f64(dataset.values, devs[0]))
+        zv = frozenset(np.flatnonzero(flags.cpu().numpy()).tolist())
+    result = empty_result(geom.n, zv)
+    lock = threading.Lock()
+    cursors = [a.start for a in assignments]
+    errors: list[WorkerError | None] = [None] * len(assignments)
+    root = str(Path(__file__).resolve().parent.parent)
+
+    def reader(a: WorkerAssignment, proc: subprocess.Popen) -> None:
+        i = a.worker_index
+        try:
+            done = False
+            while True:
+                frame = protocol.read_frame(proc.stdout)
+                if frame is None:
+                    if not done:
+                        raise protocol.ProtocolError("worker exited before DONE")
+                    break
+                kind, payload = frame
+                if kind == protocol.FRAME_BLOCKS:
+                    first, count, values = protocol.decode_blocks(payload, geom.t)
+                    if first != cursors[i]:
+                        raise IntegrityError(f"worker {i} sent tiles from {first}, expected {cursors[i]}")
+                    if first + count > a.stop:
+                        raise IntegrityError(f"worker {i} overran its range: [{first}, {first + count})")
+                    with lock:
+                        _scatter_host(result.packed, values, first, count, geom)
+                    cursors[i] = first + count
+                elif kind == protocol.FRAME_DONE:
+                    n_done = protocol.decode_done(payload)
+                    if n_done != a.tile_count or cursors[i] != a.stop:
+                        raise IntegrityError(f"worker {i} reported {n_done} tiles done but delivered up to "
+                                             f"{cursors[i]} of [{a.start}, {a.stop})")
+                    done = True
+                elif kind == protocol.FRAME_ERROR:
+                    raise WorkerError(f"worker {i} reported: {protocol.decode_error(payload)}", worker_index=i,
+                                      unfinished_range=(cursors[i], a.stop))
+                else:
+                    raise protocol.ProtocolError(f"unexpected frame type 0x{kind:02x} from worker {i}")
+        except WorkerError as err:
+            errors[i] = err
+        except Exception as exc:  # noqa: BLE001
+            errors[i] = WorkerError(f"worker {i} failed with tiles [{cursors[i]}, {a.stop}) unassembled: {exc}",
+                                    worker_index=i, unfinished_range=(cursors[i], a.stop))
+
+    procs, readers = [], []
+    try:
+        for a in assignments:
+            env = dict(os.environ, PAIRCORR_THREADS=str(threads),
+                       PCC_DEVICE=str(devs[a.worker_index % len(devs)].index),
+                       PYTHONPATH=root + os.pathsep + os.environ.get("PYTHONPATH", ""))
+            procs.append(subprocess.Popen([sys.executable, "-m", "paper_1605_01584_b200.worker"],
+                                          stdin=subprocess.PIPE, stdout=subprocess.PIPE,
+                                          stderr=subprocess.DEVNULL, env=env))
+        for a, proc in zip(assignments, procs):
+            try:
+                protocol.write_frame(proc.stdin, protocol.FRAME_ASSIGN,
+                                     protocol.encode_assign(a.start, a.stop, geom.t, a.capacity, dataset_path))
+                proc.stdin.close()
+            except OSError:
+                pass  # the reader reports the early exit
+            t = threading.Thread(target=reader, args=(a, proc), daemon=True)
+            t.start()
+            readers.append(t)
+        for t in readers:
+            t.join()
+        for proc in procs:
+            proc.wait()
+    finally:
+        for proc in procs:
+            if proc.poll() is None:
+                proc.kill()
+                proc.wait()
+    for err in errors:
+        if err is not None:
+            raise err
+    check_coverage([(a.start, cursors[a.worker_index], a.stop) for a in assignments], geom.total_tiles)
+    return result
+
+
 def compute_shard(x_host, n: int, l: int, a: WorkerAssignment, device: torch.device,
                   x_device: torch.Tensor | None = None) -> tuple[Shard, torch.Tensor]:
     """Worker body: upload, normalise everything, contract ``a``'s tile range.
@@ -267,23 +403,44 @@ def run_workers(
     gather: bool = True,
     out=None,
 ):
-    """Partition the GPU tile range across ``p`` workers on ``devices`` (distributed.py:117-151).
+    """Partition the work across ``p`` workers on ``devices`` (distributed.py:117-151).
 
-    Worker ``i`` runs on ``devices[i % len(devices)]`` with its own host
-    thread.  ``geom`` (the caller's reference tiling) only fixes ``n``: the
-    result never depends on it.  Returns a gathered ``CorrelationResult``
-    (``gather=True``) or the device-resident ``ShardedResult``.  A failing
-    worker raises ``WorkerError`` carrying its index and unfinished range.
+    ``backend="in_process"`` / ``"cuda"``: worker ``i`` is a host thread
+    driving ``devices[i % len(devices)]`` over a contiguous range of GPU
+    tiles; ``geom`` (the caller's reference tiling) only fixes ``n``.
+    Returns a gathered ``CorrelationResult`` (``gather=True``) or the
+    device-resident ``ShardedResult``.  ``backend="subprocess"``: one GPU
+    worker process per range of the caller's t x t tiles, speaking the
+    reference's framed protocol (``worker.py``), gathered on the host.  A
+    failing worker raises ``WorkerError`` with its index and unfinished range.
     """
     if backend not in BACKENDS:
         raise ValueError(f"unknown backend {backend!r}, expected one of {BACKENDS}")
+    dataset_path = None
     if not isinstance(dataset, Dataset):
         from .fileio import load_dataset
 
+        dataset_path = str(dataset)
         dataset = load_dataset(dataset)
     if geom is not None and dataset.n != geom.n:
         raise ValueError(f"geometry is for n={geom.n} but dataset has n={dataset.n}")
     devs = resolve_devices(devices)
+    if backend == "subprocess":
+        # the reference's worker-process model: reference t x t tiles over the wire
+        from .engine import default_capacity
+        from .fileio import save_dataset
+
+        geom = geom if geom is not None else TileGeometry(n=dataset.n)
+        capacity = default_capacity(geom.t) if capacity is None else capacity
+        if dataset_path is not None:
+            return _run_subprocess(dataset, dataset_path, geom, p, capacity, threads, devs)
+        with tempfile.NamedTemporaryFile(suffix=".lpcc", delete=False) as tmp:
+            tmp_path = tmp.name
+        try:
+            save_dataset(tmp_path, dataset)
+            return _run_subprocess(dataset, tmp_path, geom, p, capacity, threads, devs)
+        finally:
+            os.unlink(tmp_path)
     n, l = dataset.n, dataset.l
     assignments = make_assignments(gpu_geometry(n), p)
     shards: list[Shard | None] = [None] * p

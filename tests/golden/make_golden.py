@@ -155,6 +155,20 @@ def main() -> None:
         parts[f"{T},{p}"] = pc.partition(T, p)
     (HERE / "partition.json").write_text(json.dumps(parts, sort_keys=True))
 
+    # wire-protocol frames, byte for byte (protocol.py:54-147)
+    from paircorr import protocol as rp
+
+    vals = np.arange(2 * 16, dtype=np.float64) / 7.0
+    frames = {
+        "assign": rp.encode_assign(3, 17, 4, 1000, "/data/expr.lpcc").hex(),
+        "assign_unicode": rp.encode_assign(0, 0, 1, 1, "d\u00e9j\u00e0.lpcc").hex(),
+        "blocks": rp.encode_blocks(12, vals, 4).hex(),
+        "done": rp.encode_done(123456789).hex(),
+        "error": rp.encode_error("ValueError: boom").hex(),
+        "blocks_values": vals.tolist(),
+    }
+    (HERE / "protocol_frames.json").write_text(json.dumps(frames, indent=1))
+
     digests = {}
     threads = len(os.sched_getaffinity(0))
     for name in ("c1", "c3"):

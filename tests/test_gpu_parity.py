@@ -408,3 +408,47 @@ def test_streaming_to_file_and_pageable_output(tmp_path, rng):
     with pc.PackedFileWriterSink(tmp_path / "p.lpcr", g, nd.zero_variance) as sink:
         pc.run_pipeline(nd, g, pc.plan_passes(0, g.total_tiles, 5000), sink)
     assert np.array_equal(pc.load_result(tmp_path / "p.lpcr").packed, ref)
+
+
+def test_gpu_worker_serves_assignment_over_the_protocol(tmp_path, rng):
+    import io
+
+    from paper_1605_01584_b200 import protocol
+    from paper_1605_01584_b200.worker import serve
+
+    x = random_values(rng, 45, 13, special_rows=True)
+    path = tmp_path / "d.lpcc"
+    pc.save_dataset(path, pc.Dataset(values=x))
+    u_ref, _ = oracle.normalize(x)
+    buf = io.BytesIO()
+    protocol.write_frame(buf, protocol.FRAME_ASSIGN, protocol.encode_assign(3, 40, 4, 10, str(path)))
+    buf.seek(0)
+    out = io.BytesIO()
+    assert serve(buf, out, device=0) == 0
+    out.seek(0)
+    frames = []
+    while (f := protocol.read_frame(out)) is not None:
+        frames.append(f)
+    assert [k for k, _ in frames] == [protocol.FRAME_BLOCKS] * 4 + [protocol.FRAME_DONE]
+    cursor = 3
+    for kind, payload in frames[:-1]:
+        first, count, vals = protocol.decode_blocks(payload, 4)
+        assert first == cursor
+        assert np.abs(vals - oracle.compute_pass(u_ref, 4, first, first + count)).max() <= TOL
+        cursor += count
+    assert protocol.decode_done(frames[-1][1]) == 37
+
+
+def test_subprocess_gpu_workers_match_single_engine(rng, monkeypatch):
+    x = random_values(rng, 333, 21, special_rows=True)
+    d = pc.Dataset(values=x)
+    ref = pc.allpairs(d).packed
+    geom = pc.TileGeometry(n=333, t=4)
+    for p in (1, 3):
+        res = pc.run_workers(d, geom, p, backend="subprocess", capacity=700)
+        assert np.array_equal(res.packed, ref) and res.zero_variance == frozenset({1})
+    monkeypatch.setenv("PAIRCORR_FAIL_AFTER_PASSES", "1")
+    with pytest.raises(pc.WorkerError) as ei:
+        pc.run_workers(d, geom, 2, backend="subprocess", capacity=700)
+    lo, hi = ei.value.unfinished_range
+    assert hi - lo > 0 and ei.value.worker_index in (0, 1)
