@@ -65,8 +65,8 @@ using V6 = pcc::SyrkCfg<2, 4, 8, 4, 16, 7>;  // TMA, BK 16 x 7 stages
 using V7 = pcc::SyrkCfg<2, 4, 8, 4, 32, 3>;  // TMA, BK 32 x 3 stages
 using V8 = pcc::SyrkCfg<4, 2, 4, 8, 16, 6>;  // TMA, 8 warps 32x64
 using V9 = pcc::SyrkCfg<4, 4, 4, 4, 16, 6>;  // TMA, 16 warps 32x32
-using V10 = pcc::SyrkCfg<2, 4, 8, 4, 16, 6, 4>;  // TMA, producer 4 steps ahead
-using V11 = pcc::SyrkCfg<2, 4, 8, 4, 16, 6, 2>;  // TMA, producer 2 steps ahead
+using V10 = pcc::SyrkCfg<2, 4, 8, 4, 16, 6, 5>;  // TMA, producer 5 steps ahead
+using V11 = pcc::SyrkCfg<2, 4, 8, 4, 16, 6, 6>;  // TMA, producer 6 steps ahead (ring-limited)
 // V12 = V0 visiting tiles in the grouped L2-locality order
 constexpr int kNumVariants = 13;
 
