@@ -67,33 +67,48 @@ def wave_plan(waves: int, mid: int = 8) -> list[int]:
 class StreamPlan:
     row_lo: int                          # first job row the range needs (upload/normalise [row_lo, n))
     chunks: tuple[tuple[int, int], ...]  # upload/normalise order: bottom-up row chunks
-    # launch order: (tile_lo, tile_hi, chunks_needed, done_row); the pass may
-    # start once the first `chunks_needed` chunks are normalised; after it
-    # (and every earlier pass) packed rows >= done_row are final
-    passes: tuple[tuple[int, int, int, int], ...]
+    # launch order: (tile_lo, tile_hi, chunks_needed, dl_row_lo, dl_row_hi, phase):
+    # the pass may start once the first `chunks_needed` chunks are
+    # normalised; once it and every earlier pass are done, job rows
+    # [dl_row_lo, dl_row_hi) are final (empty when dl_row_lo >= dl_row_hi)
+    passes: tuple[tuple[int, int, int, int, int, int], ...]
 
 
-def plan_stream(n: int, tile_begin: int, tile_end: int, wave: int, chunk_rows: int = 8, mid: int = 8) -> StreamPlan:
+def lead_fraction(n: int, resident: bool = False) -> float:
+    """Share of the range's work done bottom-up while X is still uploading.
+
+    Upload time / contraction time ~= 8 B * FP64 rate / (n * PCIe rate)
+    (~35 TFLOP/s vs ~50 GB/s on a B200 box); the bottom-up phase should just
+    outlast the upload so the top-down phase never waits for data.
+    """
+    if resident:
+        return 0.05
+    return min(0.95, max(0.05, 1.15 * 8 * 35e12 / (n * 50e9)))
+
+
+def plan_stream(n: int, tile_begin: int, tile_end: int, wave: int, chunk_rows: int = 8, mid: int = 8,
+                lead: float | None = None) -> StreamPlan:
     """Plan the streamed execution of GPU tiles ``[tile_begin, tile_end)``.
 
     X arrives bottom-up in chunks of GPU tile rows -- 2, 2, 4, 4 rows first
-    (the contraction can start early), then ``chunk_rows`` (large copies run
-    at full PCIe rate).  Each
-    chunk releases the tiles whose row band it completes (tile row Y needs
-    bands >= Y only) as one pass; passes run on rotating streams, so the
-    small early ones share the GPU instead of queueing behind each other.
-    The last chunk's tiles end in a ramp-down of whole waves (..., 2, 1, 1)
-    so little download remains exposed after the final pass.
+    (the contraction can start early), then ``chunk_rows``.  Phase 1 (the
+    last ``lead`` share of the range's tiles, bottom rows): each chunk
+    releases the tiles whose row bands it completes (tile row Y needs bands
+    >= Y only) as one pass, on rotating streams so small early passes share
+    the GPU.  Phase 2 (the rest, after the upload): ``mid``-wave passes from
+    the TOP row downwards on one stream, ending in a ramp (4, 2, 1, 1 waves), so the
+    rows finishing last -- and the download left after the final pass --
+    are short middle rows instead of the longest top rows.
     """
     mg = -(-n // T_G)
     if tile_end <= tile_begin:
         return StreamPlan(n, (), ())
+    lead = lead_fraction(n) if lead is None else lead
     y_first = sym_job_coord(mg, tile_begin).y
     row_lo = y_first * T_G
     chunk_rows = max(1, chunk_rows)
-    # bottom-up row chunks aligned to the GPU tile (the lowest one may be short)
     ramp = [r for r in (2, 2, 4, 4) if r < chunk_rows]
-    bands = []
+    bands = []  # bottom-up tile-row bands [b, t)
     top = mg
     while top > y_first:
         size = ramp[len(bands)] if len(bands) < len(ramp) else chunk_rows
@@ -101,35 +116,52 @@ def plan_stream(n: int, tile_begin: int, tile_end: int, wave: int, chunk_rows: i
         bands.append((b, top))
         top = b
     chunks = tuple((b * T_G, min(n, t * T_G)) for b, t in bands)
-    groups = []  # (tile_lo, tile_hi, chunks_needed) per chunk, descending tiles
-    for c, (b, t) in enumerate(bands):
-        lo = max(tile_begin, _F(mg, b))
-        hi = min(tile_end, _F(mg, t))
-        if hi > lo:
-            groups.append((lo, hi, c + 1))
+
+    def chunk_of(y: int) -> int:  # 1-based count of chunks needed for rows >= y * 128
+        for c, (b, t) in enumerate(bands):
+            if b <= y < t:
+                return c + 1
+        return len(bands)
+
+    total = tile_end - tile_begin
+    split = tile_end - min(total, max(0, int(round(lead * total))))  # phase 1 = [split, tile_end)
     passes = []
-
-    def add(lo, hi, need):
-        y_lo = sym_job_coord(mg, lo).y
-        done_y = y_lo if lo == _F(mg, y_lo) else y_lo + 1
-        passes.append((lo, hi, need, min(n, done_y * T_G)))
-
-    for i, (lo, hi, need) in enumerate(groups):
-        if i < len(groups) - 1:
-            add(lo, hi, need)
+    # phase 1: bottom-up, one pass per released chunk
+    prev_row = n
+    for c, (b, t) in enumerate(bands):
+        lo = max(split, tile_begin, _F(mg, b))
+        hi = min(tile_end, _F(mg, t))
+        if hi <= lo:
             continue
-        # last group: ramp down so the final passes (and their downloads) are short
-        ramp = [w * wave for w in reversed([1, 1, 2, 4, mid])]
-        tail = []
-        h = lo
-        for r in reversed(ramp):  # 1, 1, 2, 4, mid waves from the bottom of the id range
-            if hi - h - r < wave:
-                break
-            tail.append((h, h + r))
-            h += r
-        add(h, hi, need)
-        for a, b in reversed(tail):
-            add(a, b, need)
+        y_lo = sym_job_coord(mg, lo).y
+        done_row = min(n, (y_lo if lo == _F(mg, y_lo) else y_lo + 1) * T_G)
+        passes.append((lo, hi, c + 1, done_row, prev_row, 1))
+        prev_row = min(prev_row, done_row)
+    # phase 2: top-down whole waves over [tile_begin, split), ramp at the end
+    if split > tile_begin:
+        waves = -(-(split - tile_begin) // wave)
+        # mid-sized passes, then a ramp down (..., 4, 2, 1, 1 waves)
+        tail = [w for w in (4, 2, 1, 1) if w < mid]
+        sizes = []
+        left = waves
+        for w in reversed(tail):
+            if left - w >= 1:
+                sizes.insert(0, w)
+                left -= w
+        sizes = [mid] * (left // mid) + ([left % mid] if left % mid else []) + sizes
+        sizes = [w * wave for w in sizes]
+        excess = sum(sizes) - (split - tile_begin)
+        sizes[0] -= excess
+        sizes = [s for s in sizes if s > 0]
+        lo = tile_begin
+        top_row = row_lo
+        for s_ in sizes:
+            hi = lo + s_
+            y_h = sym_job_coord(mg, hi).y if hi < _F(mg, mg) else mg
+            comp_row = min(n, y_h * T_G)  # rows above the first unprocessed tile's row are final
+            passes.append((lo, hi, chunk_of(sym_job_coord(mg, lo).y), top_row, comp_row, 2))
+            top_row = max(top_row, comp_row)
+            lo = hi
     return StreamPlan(row_lo, chunks, tuple(passes))
 
 
@@ -187,24 +219,27 @@ def run_stream(x, n: int, l: int, device: torch.device, tile_begin: int, tile_en
         workers = [torch.cuda.Stream(device) for _ in range(min(4, max(1, len(plan.passes))))]
         for w in workers:
             w.wait_stream(compute)  # u / out_dev allocations precede every pass
-        pass_done = []  # (event, done_row) per launched pass, in plan order
-        copied = [n]  # packed rows >= copied[0] are downloaded
+        pass_done = []  # (event, dl_row_lo, dl_row_hi) per launched pass, in plan order
+        downloaded = []  # job-row intervals already copied
+
+        def copy_rows(r_lo: int, r_hi: int, label: str) -> None:
+            a = max(span_lo, _F(n, r_lo))
+            b = min(span_hi, _F(n, r_hi))
+            if b > a:
+                with torch.cuda.stream(copy_out):
+                    host_out[a - host_base:b - host_base].copy_(out_dev[a - out_base:b - out_base],
+                                                                non_blocking=pinned_out)
+                mark(f"download {8 * (b - a) / 1e6:.0f} MB{label}", copy_out)
+            downloaded.append((r_lo, r_hi))
 
         def download(upto: int) -> None:
-            # copies for passes [len(done so far) .. upto): in-order waits keep every earlier pass covered
+            # in-order waits: a copy runs only after its pass and every earlier pass
             while download.k < upto:
-                ev, done_row = pass_done[download.k]
+                ev, r_lo, r_hi = pass_done[download.k]
                 download.k += 1
                 copy_out.wait_event(ev)
-                if done_row < copied[0]:
-                    a = max(span_lo, _F(n, done_row))
-                    b = min(span_hi, _F(n, copied[0]))
-                    if b > a:
-                        with torch.cuda.stream(copy_out):
-                            host_out[a - host_base:b - host_base].copy_(out_dev[a - out_base:b - out_base],
-                                                                        non_blocking=pinned_out)
-                        mark(f"download {8 * (b - a) / 1e6:.0f} MB", copy_out)
-                    copied[0] = done_row
+                if r_hi > r_lo:
+                    copy_rows(r_lo, r_hi, "")
 
         download.k = 0
         k = 0
@@ -221,19 +256,21 @@ def run_stream(x, n: int, l: int, device: torch.device, tile_begin: int, tile_en
                        "normalize")
             normed = torch.cuda.Event()
             normed.record(compute)
-            # every pass this chunk releases; the last chunk's passes (the
-            # ramp-down) share one stream so they finish -- and download -- in order
-            last = c == len(plan.chunks) - 1
-            while k < len(plan.passes) and plan.passes[k][2] == c + 1:
-                p_lo, p_hi, _, done_row = plan.passes[k]
-                ws = workers[0] if last else workers[k % len(workers)]
+            # every pass whose rows are now normalised, in plan order
+            while k < len(plan.passes) and plan.passes[k][2] <= c + 1:
+                p_lo, p_hi, _, dl_lo, dl_hi, phase = plan.passes[k]
+                # phase 1 (upload-limited, small passes): rotating streams run them
+                # side by side; phase 2: one stream, so passes -- and their
+                # downloads -- complete in order
+                ws = workers[k % len(workers)] if phase == 1 else workers[0]
                 ws.wait_event(normed)
+                mark(f"  start [{p_lo},{p_hi})", ws)
                 _lib.check(L.pcc_syrk_f64(ptr(u), n, l, ldu, p_lo, p_hi, _lib.LAYOUT_PACKED, ptr(out_dev), 0,
                                           out_base, 0, 0, 0, stream_handle(ws)), "syrk")
                 done = torch.cuda.Event()
                 done.record(ws)
                 mark(f"pass tiles [{p_lo},{p_hi})", ws)
-                pass_done.append((done, done_row))
+                pass_done.append((done, dl_lo, dl_hi))
                 k += 1
             if pinned_out:
                 download(len(pass_done))
@@ -242,14 +279,13 @@ def run_stream(x, n: int, l: int, device: torch.device, tile_begin: int, tile_en
             compute.wait_stream(w)
         if host_out is not None:
             download(len(pass_done))  # pageable destinations: blocking copies once all work is queued
-            a = span_lo
-            b = min(span_hi, _F(n, copied[0]))
-            if b > a:
-                copy_out.wait_stream(compute)
-                with torch.cuda.stream(copy_out):
-                    host_out[a - host_base:b - host_base].copy_(out_dev[a - out_base:b - out_base],
-                                                                non_blocking=pinned_out)
-                mark(f"download {8 * (b - a) / 1e6:.0f} MB (final)", copy_out)
+            copy_out.wait_stream(compute)
+            # rows no pass completed on its own (a row split between the two phases)
+            cur = plan.row_lo
+            for a, b in sorted(downloaded) + [(n, n)]:
+                if a > cur:
+                    copy_rows(cur, a, " (final)")
+                cur = max(cur, b)
             copy_out.synchronize()
         compute.synchronize()
         return u, flags, xd

@@ -123,30 +123,36 @@ def test_plan_passes():
 
 
 @pytest.mark.parametrize("n", [1, 127, 128, 129, 2000, 10007, 16384, 65536])
-@pytest.mark.parametrize("chunk_rows", [1, 3, 4, 64])
+@pytest.mark.parametrize("chunk_rows", [1, 3, 8, 64])
 @pytest.mark.parametrize("p", [1, 3])
-def test_stream_plan_covers_range_and_respects_dependencies(n, chunk_rows, p):
+@pytest.mark.parametrize("lead", [None, 0.0, 0.5, 1.0])
+def test_stream_plan_covers_range_and_respects_dependencies(n, chunk_rows, p, lead):
     """Streamed passes (stream.plan_stream) tile each partition range exactly
-    once, in descending id order, never before the chunk holding their first
-    tile row is normalised, and the rows they mark final are complete."""
+    once, never run before the chunk holding their first tile row is
+    normalised, and every row they declare final has all its range tiles done."""
     mg = -(-n // 128)
     T = mg * (mg + 1) // 2
+    F = lambda y: (y * (2 * mg + 1 - y)) // 2  # noqa: E731
     for tb, te in partition(T, p):
-        sp = plan_stream(n, tb, te, 148, chunk_rows)
+        sp = plan_stream(n, tb, te, 148, chunk_rows, lead=lead)
         if te == tb:
             assert sp.passes == ()
             continue
-        assert sp.passes[0][1] == te and sp.passes[-1][0] == tb
-        for a, b in zip(sp.passes, sp.passes[1:]):
-            assert a[0] == b[1]
-        assert all(c[0] < c[1] for c in sp.chunks)
+        cov = sorted((q[0], q[1]) for q in sp.passes)
+        assert cov[0][0] == tb and cov[-1][1] == te
+        assert all(a[1] == b[0] and a[0] < a[1] for a, b in zip(cov, cov[1:]))
         assert sp.chunks[0][1] == n and sp.chunks[-1][0] == sp.row_lo
-        for lo, hi, need, done in sp.passes:
+        assert all(c[0] < c[1] for c in sp.chunks)
+        done = np.zeros(T, dtype=bool)
+        for lo, hi, need, dl_lo, dl_hi, phase in sp.passes:
+            assert phase in (1, 2)
             y = pc.sym_job_coord(mg, lo).y
-            assert sp.chunks[need - 1][0] <= y * 128  # needed rows are normalised
-            # every tile of a row >= done_row // 128 lies in [lo, te)
-            if done < n:
-                assert pc.row_prefix(mg, done // 128) >= lo
+            assert sp.chunks[need - 1][0] <= y * 128  # the pass's rows are normalised first
+            done[lo:hi] = True
+            for r in range(dl_lo, dl_hi, 128):
+                Y = r // 128
+                a, b = max(tb, F(Y)), min(te, F(Y + 1))
+                assert done[a:b].all(), (lo, hi, dl_lo, dl_hi, Y)
 
 
 @pytest.mark.parametrize("n", [1, 5, 128, 129, 300, 1000])
