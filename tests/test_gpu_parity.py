@@ -452,3 +452,43 @@ def test_subprocess_gpu_workers_match_single_engine(rng, monkeypatch):
         pc.run_workers(d, geom, 2, backend="subprocess", capacity=700)
     lo, hi = ei.value.unfinished_range
     assert hi - lo > 0 and ei.value.worker_index in (0, 1)
+
+
+def test_acceptance_criterion_2_random_datasets_vs_naive_oracle():
+    """The reference's acceptance criterion 2 (test_acceptance.py:88-113):
+    50 random datasets with planted constant / negated / affine rows, random
+    n, l and scheduling knobs; engine vs the definition oracle <= 1e-10, equal
+    zero-variance sets -- here also <= 1e-12 vs the reference engine's order."""
+    rng = np.random.default_rng(2)
+    worst = 0.0
+    for trial in range(50):
+        n = int(rng.integers(1, 257))
+        l = int(rng.integers(2, 129))
+        x = random_values(rng, n, l, special_rows=True)
+        t = [1, 2, 3, 4, 5, 8, 16][trial % 7]
+        res = pc.allpairs(pc.Dataset(values=x), tile_size=t, threads=int(rng.integers(1, 5)),
+                          chunk_rows=int(rng.integers(1, 9)))
+        naive, zv = oracle.allpairs_naive(x)
+        ref, _ = oracle.allpairs(x, t=4)
+        worst = max(worst, float(np.abs(res.packed - naive).max()))
+        assert np.abs(res.packed - ref).max() <= TOL
+        assert res.zero_variance == frozenset(np.flatnonzero(zv).tolist())
+    assert worst <= 1e-10
+
+
+from hypothesis import given, settings  # noqa: E402
+from hypothesis import strategies as st  # noqa: E402
+from hypothesis.extra.numpy import arrays  # noqa: E402
+
+
+@given(arrays(np.float64, st.tuples(st.integers(1, 5), st.integers(2, 70)),
+              elements=st.floats(min_value=-1e6, max_value=1e6, allow_nan=False, width=64)))
+@settings(max_examples=150, deadline=None)
+def test_normalize_property_bit_exact(x):
+    """Hypothesis-generated rows (the reference's test_normalize_row_invariants
+    domain, test_transform.py:66-88): K1 equals the reference order bit for bit."""
+    u, zv = _abi_normalize(x)
+    u_ref, zv_ref = oracle.normalize(x)
+    n, l = x.shape
+    assert np.array_equal(u.cpu().numpy()[:n, :l], u_ref)
+    assert np.array_equal(zv.cpu().numpy().astype(bool), zv_ref)
