@@ -68,7 +68,8 @@ using V9 = pcc::SyrkCfg<4, 4, 4, 4, 16, 6>;  // TMA, 16 warps 32x32
 using V10 = pcc::SyrkCfg<2, 4, 8, 4, 16, 6, 5>;  // TMA, producer 5 steps ahead
 using V11 = pcc::SyrkCfg<2, 4, 8, 4, 16, 6, 6>;  // TMA, producer 6 steps ahead (ring-limited)
 // V12 = V0 visiting tiles in the grouped L2-locality order
-constexpr int kNumVariants = 13;
+// V13 = V0 with half-stage skew between the two warps of each SMSP
+constexpr int kNumVariants = 14;
 
 template <class C, int LAYOUT>
 int configure_tma_one(int *ctas) {
@@ -181,6 +182,10 @@ int device_config(const DeviceConfig **out, int device = -1) {
       PCC_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, TL::kSmemBytes), "attr(V12)");
       PCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.variant_ctas[12], kfn, TL::kThreads, TL::kSmemBytes),
                "occupancy(V12)");
+      auto kfn13 = pcc::syrk_tma_kernel<V0, pcc::kLayoutPacked, false, true>;
+      PCC_CUDA(cudaFuncSetAttribute(kfn13, cudaFuncAttributeMaxDynamicSharedMemorySize, TL::kSmemBytes), "attr(V13)");
+      PCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.variant_ctas[13], kfn13, TL::kThreads, TL::kSmemBytes),
+               "occupancy(V13)");
     }
     if (prev != device) cudaSetDevice(prev);
     if (rc != PCC_OK) return rc;
@@ -220,7 +225,7 @@ int launch_cfg(const double *u, int64_t n, int64_t l, int64_t ldu, uint64_t tb, 
   return PCC_OK;
 }
 
-template <class C, int LAYOUT, bool GROUPED = false>
+template <class C, int LAYOUT, bool GROUPED = false, bool SKEW = false>
 int launch_tma_cfg(const double *u, int64_t n, int64_t l, int64_t ldu, uint64_t tb, uint64_t te,
                    const pcc::Epilogue &ep, cudaStream_t stream, int ctas_per_sm, int sm_count) {
   using TL = pcc::TmaLayout<C>;
@@ -238,7 +243,7 @@ int launch_tma_cfg(const double *u, int64_t n, int64_t l, int64_t ldu, uint64_t 
   while ((group + 1) * (group + 1) <= grid) ++group;
   const pcc::TileOrder order =
       GROUPED ? pcc::make_tile_order(m_g, tb, te, group) : pcc::TileOrder{tb, te, 0, 0, 0, te, te, te - tb, 1};
-  pcc::syrk_tma_kernel<C, LAYOUT, GROUPED>
+  pcc::syrk_tma_kernel<C, LAYOUT, GROUPED, SKEW>
       <<<grid, TL::kThreads, TL::kSmemBytes, stream>>>(map, n, k_tiles, m_g, order, ep);
   PCC_CUDA(cudaGetLastError(), "syrk_tma_kernel launch");
   return PCC_OK;
@@ -269,6 +274,7 @@ int launch_syrk(const double *u, int64_t n, int64_t l, int64_t ldu, uint64_t tb,
     case 10: return launch_tma_cfg<V10, pcc::kLayoutPacked>(u, n, l, ldu, tb, te, ep, stream, vc[10], sms);
     case 11: return launch_tma_cfg<V11, pcc::kLayoutPacked>(u, n, l, ldu, tb, te, ep, stream, vc[11], sms);
     case 12: return launch_tma_cfg<V0, pcc::kLayoutPacked, true>(u, n, l, ldu, tb, te, ep, stream, vc[12], sms);
+    case 13: return launch_tma_cfg<V0, pcc::kLayoutPacked, false, true>(u, n, l, ldu, tb, te, ep, stream, vc[13], sms);
     default: return fail(PCC_EINVAL, "unknown contraction variant %d (0..%d)", variant, kNumVariants - 1);
   }
 }

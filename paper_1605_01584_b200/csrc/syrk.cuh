@@ -221,7 +221,7 @@ __device__ __forceinline__ void slot_tile(const TileOrder &o, uint64_t m, uint64
   }
 }
 
-template <class C, int LAYOUT, bool GROUPED = false>
+template <class C, int LAYOUT, bool GROUPED = false, bool SKEW = false>
 __global__ void __launch_bounds__(C::kThreads, 1)
 syrk_tma_kernel(const __grid_constant__ CUtensorMap umap, int64_t n, int k_tiles, uint64_t m_g, TileOrder order,
                 Epilogue ep) {
@@ -309,34 +309,59 @@ syrk_tma_kernel(const __grid_constant__ CUtensorMap umap, int64_t n, int k_tiles
 #pragma unroll
       for (int ni = 0; ni < C::NI; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
 
-    for (int kt = 0; kt < k_tiles; ++kt, ++c_step) {
-      if (tid == 0) produce(c_step);
-      mbar_wait(full0 + 8 * stage, phase);
-      const double *sA = smem + stage * C::kStageDoubles + (wm * C::MI * 8 + g) * kSlab + tig * 2;
-      const double *sB = smem + stage * C::kStageDoubles + C::kOpDoubles + (wn * C::NI * 8 + g) * kSlab + tig * 2;
+    // One 8-deep K slab of stage `st`: 12 fragment loads, 64 DMMAs.
+    auto slab_mma = [&](int st, int slab) {
+      const double *sA = smem + st * C::kStageDoubles + (wm * C::MI * 8 + g) * kSlab + tig * 2 + slab * kTile * kSlab;
+      const double *sB =
+          smem + st * C::kStageDoubles + C::kOpDoubles + (wn * C::NI * 8 + g) * kSlab + tig * 2 + slab * kTile * kSlab;
+      double2 a[C::MI], b[C::NI];
 #pragma unroll
-      for (int slab = 0; slab < C::kSlabs; ++slab) {
-        double2 a[C::MI], b[C::NI];
+      for (int mi = 0; mi < C::MI; ++mi) a[mi] = *reinterpret_cast<const double2 *>(sA + mi * 8 * kSlab);
 #pragma unroll
-        for (int mi = 0; mi < C::MI; ++mi)
-          a[mi] = *reinterpret_cast<const double2 *>(sA + slab * kTile * kSlab + mi * 8 * kSlab);
+      for (int ni = 0; ni < C::NI; ++ni) b[ni] = *reinterpret_cast<const double2 *>(sB + ni * 8 * kSlab);
 #pragma unroll
-        for (int ni = 0; ni < C::NI; ++ni)
-          b[ni] = *reinterpret_cast<const double2 *>(sB + slab * kTile * kSlab + ni * 8 * kSlab);
+      for (int mi = 0; mi < C::MI; ++mi)
 #pragma unroll
-        for (int mi = 0; mi < C::MI; ++mi)
+        for (int ni = 0; ni < C::NI; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], a[mi].x, b[ni].x);
 #pragma unroll
-          for (int ni = 0; ni < C::NI; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], a[mi].x, b[ni].x);
+      for (int mi = 0; mi < C::MI; ++mi)
 #pragma unroll
-        for (int mi = 0; mi < C::MI; ++mi)
-#pragma unroll
-          for (int ni = 0; ni < C::NI; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], a[mi].y, b[ni].y);
+        for (int ni = 0; ni < C::NI; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], a[mi].y, b[ni].y);
+    };
+    auto advance = [](int &st, uint32_t &ph) {
+      if (++st == C::STAGES) {
+        st = 0;
+        ph ^= 1;
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(empty0 + 8 * stage);
-      if (++stage == C::STAGES) {
-        stage = 0;
-        phase ^= 1;
+    };
+
+    if (SKEW && wm == 1) {
+      // Half-stage skew: these warps share SMSPs with warps wm == 0 (warp w and
+      // w + 4) and run their stage waits and fragment loads between the other
+      // warps' slab boundaries, so the two warps never stall together.  Each
+      // accumulator still sees slab 0 then slab 1 of every stage, in order.
+      static_assert(!SKEW || C::kSlabs == 2, "skew needs two slabs per stage");
+      mbar_wait(full0 + 8 * stage, phase);
+      slab_mma(stage, 0);
+      for (int kt = 0; kt < k_tiles; ++kt) {
+        const int cur = stage;
+        advance(stage, phase);
+        if (kt + 1 < k_tiles) mbar_wait(full0 + 8 * stage, phase);
+        slab_mma(cur, 1);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty0 + 8 * cur);
+        if (kt + 1 < k_tiles) slab_mma(stage, 0);
+      }
+      c_step += k_tiles;
+    } else {
+      for (int kt = 0; kt < k_tiles; ++kt, ++c_step) {
+        if (tid == 0) produce(c_step);
+        mbar_wait(full0 + 8 * stage, phase);
+#pragma unroll
+        for (int slab = 0; slab < C::kSlabs; ++slab) slab_mma(stage, slab);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty0 + 8 * stage);
+        advance(stage, phase);
       }
     }
 
