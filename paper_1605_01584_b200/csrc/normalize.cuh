@@ -75,6 +75,39 @@ __device__ __forceinline__ double lane_chain(const double *p, int64_t nsteps64, 
   return s;
 }
 
+// Pure lane chains over already-prepared values (stride 8): SQUARE = false
+// sums v, SQUARE = true sums RN(v*v) -- the sum8 / ssd8 lane accumulations
+// once the constancy test and the centring (d = x - mean) have been done by
+// all threads in parallel.  One FP64 add (and one multiply) per step on the
+// dependent chain; loads run PF steps ahead.
+template <bool SQUARE, int PF>
+__device__ __forceinline__ double lane_sum(const double *p, int nsteps) {
+  const int full = (nsteps / PF) * PF;
+  double s = 0.0;
+  double nxt[PF];
+  if (full > 0) {
+#pragma unroll
+    for (int i = 0; i < PF; ++i) nxt[i] = p[8 * i];
+  }
+  int t = 0;
+  for (; t < full; t += PF) {
+    double cur[PF];
+#pragma unroll
+    for (int i = 0; i < PF; ++i) cur[i] = nxt[i];
+    if (t + PF < full) {
+#pragma unroll
+      for (int i = 0; i < PF; ++i) nxt[i] = p[8 * (t + PF + i)];
+    }
+#pragma unroll
+    for (int i = 0; i < PF; ++i) s = __dadd_rn(s, SQUARE ? __dmul_rn(cur[i], cur[i]) : cur[i]);
+  }
+  for (; t < nsteps; ++t) {
+    const double v = p[8 * t];
+    s = __dadd_rn(s, SQUARE ? __dmul_rn(v, v) : v);
+  }
+  return s;
+}
+
 constexpr int kNormThreads = 256;
 constexpr int kNormRowsPerCta = kNormThreads / 8;
 
@@ -174,54 +207,70 @@ normalize_rows_smem_kernel(const double *__restrict__ x, int64_t ldx, double *__
   cp_async_wait<0>();
   __syncthreads();
 
-  // 2. lane chains: thread (row = tid / 8, lane8 = tid % 8)
+  // 2a. exact constancy test (every element equals the first), all threads
+  for (int r = 0; r < rows; ++r) {
+    const double *xs = srow + (int64_t)r * l;
+    const double first = xs[0];
+    bool v = false;
+    for (int64_t k = tid; k < l; k += kNormSmemThreads) v |= (xs[k] != first);
+    const int varies = __syncthreads_or(v);
+    if (tid == 0) s_zero[r] = !varies;
+  }
+  __syncthreads();
+
+  // 2b. sum8 lane chains: thread (row = tid / 8, lane8 = tid % 8)
   const int lane8 = tid & 7;
   const int row = tid >> 3;
   const bool active = row < rows;
-  const double *sr = srow + (int64_t)(active ? row : 0) * l;
-  const int64_t nsteps = (l - lane8 + 7) >> 3;
-  bool varies = false;
-  double s = lane_chain<false, 8>(sr + lane8, nsteps, sr[0], varies);
+  const bool work = active && !s_zero[row];
+  double *sr = srow + (int64_t)(active ? row : 0) * l;
+  const int nsteps = (int)((l - lane8 + 7) >> 3);
+  double s = work ? lane_sum<false, 8>(sr + lane8, nsteps) : 0.0;
   s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 1));
   s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 2));
   s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 4));
-  const unsigned vb = __ballot_sync(0xffffffffu, varies);
-  const bool constant = (vb & (0xffu << (tid & 24))) == 0u;
-  double mean = 0.0, ssd = 0.0;
-  if (!constant) {
-    mean = __ddiv_rn(s, (double)l);
-    bool unused = false;
-    ssd = lane_chain<true, 8>(sr + lane8, nsteps, mean, unused);
+  if (work && lane8 == 0) s_mean[row] = __ddiv_rn(s, (double)l);
+  __syncthreads();
+
+  // 2c. centre in place, all threads: d = x - mean (the reference's a[k] - mean)
+  for (int r = 0; r < rows; ++r) {
+    if (s_zero[r]) continue;
+    double *xs = srow + (int64_t)r * l;
+    const double m = s_mean[r];
+    for (int64_t k = tid; k < l; k += kNormSmemThreads) xs[k] = __dsub_rn(xs[k], m);
   }
-  ssd = __dadd_rn(ssd, __shfl_xor_sync(0xffffffffu, ssd, 1));
-  ssd = __dadd_rn(ssd, __shfl_xor_sync(0xffffffffu, ssd, 2));
-  ssd = __dadd_rn(ssd, __shfl_xor_sync(0xffffffffu, ssd, 4));
+  __syncthreads();
+
+  // 2d. ssd8 lane chains over d*d
+  double q = work ? lane_sum<true, 8>(sr + lane8, nsteps) : 0.0;
+  q = __dadd_rn(q, __shfl_xor_sync(0xffffffffu, q, 1));
+  q = __dadd_rn(q, __shfl_xor_sync(0xffffffffu, q, 2));
+  q = __dadd_rn(q, __shfl_xor_sync(0xffffffffu, q, 4));
   if (active && lane8 == 0) {
-    const bool zero = constant || ssd == 0.0;
+    const bool zero = !work || q == 0.0;
     s_zero[row] = zero;
-    s_mean[row] = mean;
-    s_scale[row] = zero ? 0.0 : __dsqrt_rn(ssd);
+    s_scale[row] = zero ? 0.0 : __dsqrt_rn(q);
     zero_variance[r0 + row] = zero ? 1 : 0;
   }
   __syncthreads();
 
-  // 3. write U rows (coalesced), zero rows for zero variance, zero K padding
+  // 3. write U rows (coalesced): u = d / scale, zero rows for zero variance,
+  //    zero K padding
   for (int r = 0; r < rows; ++r) {
     double *ur = u + (r0 + r) * ldu;
-    const double *xs = srow + (int64_t)r * l;
+    const double *ds = srow + (int64_t)r * l;
     if (s_zero[r]) {
       for (int64_t k = tid; k < ldu; k += kNormSmemThreads) ur[k] = 0.0;
     } else {
-      const double m = s_mean[r], sc = s_scale[r];
+      const double sc = s_scale[r];
       // two independent divisions per iteration keep more of their latency in flight
       int64_t k = tid;
       for (; k + kNormSmemThreads < l; k += 2 * kNormSmemThreads) {
-        const double a0 = __dsub_rn(xs[k], m), a1 = __dsub_rn(xs[k + kNormSmemThreads], m);
-        const double q0 = __ddiv_rn(a0, sc), q1 = __ddiv_rn(a1, sc);
+        const double q0 = __ddiv_rn(ds[k], sc), q1 = __ddiv_rn(ds[k + kNormSmemThreads], sc);
         ur[k] = q0;
         ur[k + kNormSmemThreads] = q1;
       }
-      if (k < l) ur[k] = __ddiv_rn(__dsub_rn(xs[k], m), sc);
+      if (k < l) ur[k] = __ddiv_rn(ds[k], sc);
       for (k = l + tid; k < ldu; k += kNormSmemThreads) ur[k] = 0.0;
     }
   }

@@ -329,14 +329,30 @@ int pcc_normalize_rows_f64(const double *x, int64_t ldx, double *u, int64_t ldu,
   if (!x || !u || !zero_variance) return fail(PCC_EINVAL, "null pointer");
   const uint64_t rows = (uint64_t)(row_hi - row_lo);
   const int64_t row_bytes = l * (int64_t)sizeof(double);
-  // Shared-memory staging: as many 64-thread CTAs per SM as rows allow
-  // (4, 3, 2, then 1 CTA/SM), up to 8 rows per CTA.
   constexpr int64_t kSmPerSmem = 224 * 1024;
+  static const int mode = [] {
+    // tuning knob: PCC_NORMALIZE_KERNEL = global forces the 3-pass kernel
+    const char *e = getenv("PCC_NORMALIZE_KERNEL");
+    return (e && strcmp(e, "global") == 0) ? 0 : 1;
+  }();
+  static std::once_flag attr_once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(attr_once, [] {
+    const void *fns[] = {(const void *)pcc::normalize_rows_smem_kernel<64>,
+                         (const void *)pcc::normalize_rows_smem_kernel<128>,
+                         (const void *)pcc::normalize_rows_smem_kernel<256>};
+    for (const void *f : fns)
+      if (attr_err == cudaSuccess)
+        attr_err = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmPerSmem);
+  });
+  if (attr_err != cudaSuccess) return cuda_fail(attr_err, "cudaFuncSetAttribute(normalize smem)");
+  // Shared-memory staging in natural order: as many CTAs per SM as rows allow
+  // (4, 3, 2, then 1 CTA/SM), up to 8 rows per CTA.
   int per_cta = 0;
   size_t smem = 0;
-  // Measured (round 1, profiles/r01_normalize.log): staging wins up to
-  // 32 KB rows (c2: 390 vs 470 us), the 3-pass kernel wins at 64 KB (c4).
-  constexpr int64_t kMaxStagedRow = 48 * 1024;
+  // Measured (round 1, profiles/r01_normalize.log): staging beats the
+  // 3-pass kernel at every BASELINE row size (c4, 64 KB rows: 1.41 vs 1.82 ms).
+  constexpr int64_t kMaxStagedRow = 110 * 1024;
   for (int ctas = 4; ctas >= 1 && per_cta == 0 && row_bytes <= kMaxStagedRow; --ctas) {
     const int64_t budget = kSmPerSmem / ctas - 1024;
     if (row_bytes <= budget) {
@@ -344,28 +360,32 @@ int pcc_normalize_rows_f64(const double *x, int64_t ldx, double *u, int64_t ldu,
       smem = (size_t)per_cta * (size_t)row_bytes;
     }
   }
-  static const bool force_global = [] {
-    const char *e = getenv("PCC_NORMALIZE_KERNEL");  // tuning knob: "global" forces the 3-pass kernel
-    return e != nullptr && strcmp(e, "global") == 0;
-  }();
-  if (per_cta >= 1 && !force_global) {
-    // Measured (profiles/r01_normalize.log): 64-thread CTAs for rows > 16 KB
-    // (c2), 128-thread CTAs below (c3, c5) where the division-heavy write
-    // phase benefits from more warps.
-    const bool wide = row_bytes <= 16 * 1024;
-    static std::once_flag attr_once;
-    static cudaError_t attr_err = cudaSuccess;
-    std::call_once(attr_once, [] {
-      attr_err = cudaFuncSetAttribute(pcc::normalize_rows_smem_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)kSmPerSmem);
-      if (attr_err == cudaSuccess)
-        attr_err = cudaFuncSetAttribute(pcc::normalize_rows_smem_kernel<128>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmPerSmem);
-    });
-    if (attr_err != cudaSuccess) return cuda_fail(attr_err, "cudaFuncSetAttribute(normalize smem)");
+  if (per_cta >= 1 && mode == 1) {
+    static const int width = [] {  // tuning knob: PCC_NORMALIZE_THREADS = 64 | 128 | 256
+      const char *e = getenv("PCC_NORMALIZE_THREADS");
+      return e ? atoi(e) : 0;
+    }();
+    // Widest CTA whose register footprint still lets every smem-resident CTA
+    // run (measured, profiles/r01_normalize.log: c2 -> 128, c4 -> 256).
+    static int regs = 0;
+    if (regs == 0) {
+      cudaFuncAttributes fa;
+      regs = cudaFuncGetAttributes(&fa, pcc::normalize_rows_smem_kernel<256>) == cudaSuccess ? fa.numRegs : 72;
+    }
+    const int64_t occ_smem = (228 * 1024) / ((int64_t)smem + 1024);
+    int threads = 64;
+    for (int t : {256, 128})
+      if (occ_smem * t * regs <= 65536) {
+        threads = t;
+        break;
+      }
+    if (width) threads = width;
     const uint64_t grid = ceil_div(rows, (uint64_t)per_cta);
     if (grid > 0x7FFFFFFFull) return fail(PCC_EINVAL, "too many rows");
-    if (wide)
+    if (threads == 256)
+      pcc::normalize_rows_smem_kernel<256><<<(unsigned)grid, 256, smem, (cudaStream_t)stream>>>(
+          x, ldx, u, ldu, zero_variance, l, row_lo, row_hi, per_cta);
+    else if (threads == 128)
       pcc::normalize_rows_smem_kernel<128><<<(unsigned)grid, 128, smem, (cudaStream_t)stream>>>(
           x, ldx, u, ldu, zero_variance, l, row_lo, row_hi, per_cta);
     else
