@@ -44,6 +44,7 @@ struct DeviceConfig {
   int max_smem_optin = 0;
   int syrk_ctas_per_sm = 0;
   int variant_ctas[16] = {0};
+  int quad_ctas = 0;
   size_t total_mem = 0;
 };
 
@@ -70,6 +71,9 @@ using V11 = pcc::SyrkCfg<2, 4, 8, 4, 16, 6, 6>;  // TMA, producer 6 steps ahead 
 // V12 = V0 visiting tiles in the grouped L2-locality order
 // V13 = V0 with half-stage skew between the two warps of each SMSP
 constexpr int kNumVariants = 14;
+// Tail kernel: 64 x 64 quadrants of the GPU tiles of the last partial wave,
+// 4 warps (32 x 32 each), two CTAs per SM -- same per-cell arithmetic.
+using VQ = pcc::SyrkCfg<2, 2, 4, 4, 16, 6>;
 
 template <class C, int LAYOUT>
 int configure_tma_one(int *ctas) {
@@ -98,7 +102,7 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t
                                   const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-int encode_umap(const double *u, int64_t ldu, int64_t rows, CUtensorMap *map) {
+int encode_umap(const double *u, int64_t ldu, int64_t rows, CUtensorMap *map, int box_rows = pcc::kTile) {
   static EncodeTiledFn fn = nullptr;
   static std::once_flag once;
   static cudaError_t once_err = cudaSuccess;
@@ -111,7 +115,7 @@ int encode_umap(const double *u, int64_t ldu, int64_t rows, CUtensorMap *map) {
   if (fn == nullptr) return fail(PCC_ECUDA, "cuTensorMapEncodeTiled unavailable (%s)", cudaGetErrorString(once_err));
   const cuuint64_t dims[2] = {(cuuint64_t)ldu, (cuuint64_t)rows};
   const cuuint64_t strides[1] = {(cuuint64_t)ldu * sizeof(double)};
-  const cuuint32_t box[2] = {(cuuint32_t)pcc::kSlab, (cuuint32_t)pcc::kTile};
+  const cuuint32_t box[2] = {(cuuint32_t)pcc::kSlab, (cuuint32_t)box_rows};
   const cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(u), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -165,6 +169,7 @@ int device_config(const DeviceConfig **out, int device = -1) {
                   p.major, p.minor);
     }
     int rc = configure_tma_variant<V0>(&c.variant_ctas[0]);
+    if (rc == PCC_OK) rc = configure_tma_variant<VQ>(&c.quad_ctas);
     if (rc == PCC_OK) rc = configure_one<V1, pcc::kLayoutPacked>(&c.variant_ctas[1]);
     if (rc == PCC_OK) rc = configure_one<V2, pcc::kLayoutPacked>(&c.variant_ctas[2]);
     if (rc == PCC_OK) rc = configure_one<V3, pcc::kLayoutPacked>(&c.variant_ctas[3]);
@@ -227,7 +232,8 @@ int launch_cfg(const double *u, int64_t n, int64_t l, int64_t ldu, uint64_t tb, 
 
 template <class C, int LAYOUT, bool GROUPED = false, bool SKEW = false>
 int launch_tma_cfg(const double *u, int64_t n, int64_t l, int64_t ldu, uint64_t tb, uint64_t te,
-                   const pcc::Epilogue &ep, cudaStream_t stream, int ctas_per_sm, int sm_count) {
+                   const pcc::Epilogue &ep, cudaStream_t stream, int ctas_per_sm, int sm_count,
+                   int quad_ctas_per_sm = 0) {
   using TL = pcc::TmaLayout<C>;
   CUtensorMap map;
   int rc = encode_umap(u, ldu, pcc_rows_padded(n), &map);
@@ -235,17 +241,39 @@ int launch_tma_cfg(const double *u, int64_t n, int64_t l, int64_t ldu, uint64_t 
   const uint64_t m_g = ceil_div((uint64_t)n, pcc::kTile);
   const int k_tiles = (int)ceil_div((uint64_t)l, C::BK);
   const uint64_t resident = (uint64_t)sm_count * (uint64_t)ctas_per_sm;
+  // Tail split: a last partial wave (tiles % resident) small enough to fit
+  // one round of the tail kernel (64 x 64 quadrants, quad_ctas_per_sm CTAs
+  // per SM) finishes in quad_ctas_per_sm / 4 of a tile time instead of a
+  // whole one.  Larger remainders gain nothing and stay in the main kernel.
   const uint64_t tiles = te - tb;
-  const unsigned grid = (unsigned)(tiles < resident ? tiles : resident);
-  // Row-group height of the tile order: ~sqrt(wave) rows x ~sqrt(wave)
-  // columns per wave minimises the distinct operand bands in flight.
-  uint32_t group = 1;
-  while ((group + 1) * (group + 1) <= grid) ++group;
-  const pcc::TileOrder order =
-      GROUPED ? pcc::make_tile_order(m_g, tb, te, group) : pcc::TileOrder{tb, te, 0, 0, 0, te, te, te - tb, 1};
-  pcc::syrk_tma_kernel<C, LAYOUT, GROUPED, SKEW>
-      <<<grid, TL::kThreads, TL::kSmemBytes, stream>>>(map, n, k_tiles, m_g, order, ep);
-  PCC_CUDA(cudaGetLastError(), "syrk_tma_kernel launch");
+  uint64_t tail = quad_ctas_per_sm > 0 ? tiles % resident : 0;
+  if (tail > 0 && 4 * tail > (uint64_t)sm_count * (uint64_t)quad_ctas_per_sm) tail = 0;
+  const uint64_t main_end = te - tail;
+  if (main_end > tb) {
+    const uint64_t mt = main_end - tb;
+    const unsigned grid = (unsigned)(mt < resident ? mt : resident);
+    // Row-group height of the (optional) grouped order: ~sqrt(wave) rows.
+    uint32_t group = 1;
+    while ((group + 1) * (group + 1) <= grid) ++group;
+    const pcc::TileOrder order = GROUPED ? pcc::make_tile_order(m_g, tb, main_end, group)
+                                         : pcc::TileOrder{tb, main_end, 0, 0, 0, main_end, main_end, mt, 1};
+    pcc::syrk_tma_kernel<C, LAYOUT, GROUPED, SKEW>
+        <<<grid, TL::kThreads, TL::kSmemBytes, stream>>>(map, n, k_tiles, m_g, order, ep);
+    PCC_CUDA(cudaGetLastError(), "syrk_tma_kernel launch");
+  }
+  if (tail > 0) {
+    using TQ = pcc::TmaLayout<VQ>;
+    CUtensorMap qmap;
+    rc = encode_umap(u, ldu, pcc_rows_padded(n), &qmap, VQ::kEdge);
+    if (rc) return rc;
+    const uint64_t jobs = 4 * tail;
+    const uint64_t qres = (uint64_t)sm_count * (uint64_t)quad_ctas_per_sm;
+    const unsigned grid = (unsigned)(jobs < qres ? jobs : qres);
+    const pcc::TileOrder order{main_end, te, 0, 0, 0, te, te, jobs, 1};
+    pcc::syrk_tma_kernel<VQ, LAYOUT><<<grid, TQ::kThreads, TQ::kSmemBytes, stream>>>(
+        qmap, n, (int)ceil_div((uint64_t)l, VQ::BK), m_g, order, ep);
+    PCC_CUDA(cudaGetLastError(), "syrk_tma_kernel<quadrants> launch");
+  }
   return PCC_OK;
 }
 
@@ -258,7 +286,7 @@ int launch_syrk(const double *u, int64_t n, int64_t l, int64_t ldu, uint64_t tb,
   if (rc) return rc;
   const int sms = dc->sm_count;
   const int *vc = dc->variant_ctas;
-  if (variant == 0) return launch_tma_cfg<V0, LAYOUT>(u, n, l, ldu, tb, te, ep, stream, vc[0], sms);
+  if (variant == 0) return launch_tma_cfg<V0, LAYOUT>(u, n, l, ldu, tb, te, ep, stream, vc[0], sms, dc->quad_ctas);
   if (LAYOUT != pcc::kLayoutPacked)
     return fail(PCC_EINVAL, "contraction variant %d is only built for the packed layout", variant);
   switch (variant) {

@@ -39,22 +39,24 @@ constexpr int kSlab = 8;    // doubles per smem row-slab (one DMMA k8 pair)
 enum : int { kLayoutPacked = 0, kLayoutDense = 1, kLayoutTiles = 2 };
 
 // Kernel shape: WARPS_M x WARPS_N warps, each owning MI x NI DMMA 8x8
-// accumulators (CTA tile 128 x 128), K staged BK doubles per stage through
-// a STAGES-deep cp.async ring.
+// accumulators (CTA tile kEdge x kEdge: the 128 x 128 GPU tile, or one 64 x 64
+// quadrant of it for the tail kernel), K staged BK doubles per stage
+// through a STAGES-deep ring.
 template <int WARPS_M_, int WARPS_N_, int MI_, int NI_, int BK_, int STAGES_, int AHEAD_ = STAGES_ / 2>
 struct SyrkCfg {
   static constexpr int WARPS_M = WARPS_M_, WARPS_N = WARPS_N_, MI = MI_, NI = NI_, BK = BK_, STAGES = STAGES_;
   static constexpr int AHEAD = AHEAD_;  // TMA producer lead (K steps) over warp 0
   static constexpr int kThreads = 32 * WARPS_M * WARPS_N;
+  static constexpr int kEdge = WARPS_M * MI * 8;  // CTA tile edge (rows == cols)
   static constexpr int kSlabs = BK / kSlab;
-  static constexpr int kOpDoubles = kSlabs * kTile * kSlab;
+  static constexpr int kOpDoubles = kSlabs * kEdge * kSlab;
   static constexpr int kStageDoubles = 2 * kOpDoubles;
   static constexpr int kSmemBytes = STAGES * kStageDoubles * (int)sizeof(double);
   static constexpr int kChunksPerRow = BK / 2;                 // 16-byte chunks
   static constexpr int kRowsPerPass = kThreads / kChunksPerRow;
-  static constexpr int kPasses = kTile / kRowsPerPass;
-  static_assert(WARPS_M * MI * 8 == kTile && WARPS_N * NI * 8 == kTile, "CTA tile must be 128 x 128");
-  static_assert(BK % kSlab == 0 && kThreads % kChunksPerRow == 0 && kTile % kRowsPerPass == 0, "bad shape");
+  static constexpr int kPasses = kEdge / kRowsPerPass;
+  static_assert(kEdge == WARPS_N * NI * 8 && (kEdge == kTile || 2 * kEdge == kTile), "CTA tile: 128^2 or a 64^2 quadrant");
+  static_assert(BK % kSlab == 0 && kThreads % kChunksPerRow == 0 && kEdge % kRowsPerPass == 0, "bad shape");
 };
 
 struct Epilogue {
@@ -88,6 +90,7 @@ template <class C, int LAYOUT>
 __global__ void __launch_bounds__(C::kThreads, 1)
 syrk_kernel(const double *__restrict__ u, int64_t n, int64_t ldu, int k_tiles, uint64_t m_g,
             uint64_t tile_begin, uint64_t tile_end, Epilogue ep) {
+  static_assert(C::kEdge == kTile, "the cp.async kernels compute whole 128 x 128 tiles");
   extern __shared__ __align__(128) double smem[];
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
@@ -205,7 +208,7 @@ struct TmaLayout {
   static constexpr int kThreads = C::kThreads;
   static constexpr int kAhead = C::AHEAD;
   static constexpr uint32_t kStageBytes = (uint32_t)(C::kStageDoubles * sizeof(double));
-  static constexpr uint32_t kSlabBytes = (uint32_t)(kTile * kSlab * sizeof(double));
+  static constexpr uint32_t kSlabBytes = (uint32_t)(C::kEdge * kSlab * sizeof(double));
 };
 
 // Schedule slot s -> tile (Y, X): plain bijection id order (production) or
@@ -218,6 +221,24 @@ __device__ __forceinline__ void slot_tile(const TileOrder &o, uint64_t m, uint64
     const uint64_t J = o.tb + s;
     Y = tile_row(m, J);
     X = J + Y - row_prefix(m, Y);
+  }
+}
+
+// Schedule slot -> origin (row0, col0) of the CTA tile.  Quadrant mode (the
+// tail kernel, 64 x 64 CTA tiles): slot s is quadrant s % 4 of GPU tile
+// order.tb + s / 4 -- the same cells, the same per-cell K order, four CTAs.
+template <class C, bool GROUPED>
+__device__ __forceinline__ void slot_origin(const TileOrder &o, uint64_t m, uint64_t s, uint64_t &row0,
+                                            uint64_t &col0) {
+  uint64_t Y, X;
+  if (C::kEdge == kTile) {
+    slot_tile<GROUPED>(o, m, s, Y, X);
+    row0 = Y * kTile;
+    col0 = X * kTile;
+  } else {
+    slot_tile<false>(o, m, s >> 2, Y, X);
+    row0 = Y * kTile + ((s >> 1) & 1) * C::kEdge;
+    col0 = X * kTile + (s & 1) * C::kEdge;
   }
 }
 
@@ -254,10 +275,10 @@ syrk_tma_kernel(const __grid_constant__ CUtensorMap umap, int64_t n, int k_tiles
   uint64_t p_s = first;
   int32_t p_ya = 0, p_xb = 0;
   if (tid == 0 && my_tiles) {
-    uint64_t Y, X;
-    slot_tile<GROUPED>(order, m_g, p_s, Y, X);
-    p_ya = (int32_t)(Y * kTile);
-    p_xb = (int32_t)(X * kTile);
+    uint64_t r0, c0;
+    slot_origin<C, GROUPED>(order, m_g, p_s, r0, c0);
+    p_ya = (int32_t)r0;
+    p_xb = (int32_t)c0;
   }
   // Issue loads while the cursor is less than `want` steps ahead; block on a
   // busy slot only if the consumer would otherwise find the ring empty.
@@ -286,10 +307,10 @@ syrk_tma_kernel(const __grid_constant__ CUtensorMap umap, int64_t n, int k_tiles
       if (++p_kt == k_tiles && p_step < total_steps) {
         p_kt = 0;
         p_s += gridDim.x;
-        uint64_t Y, X;
-        slot_tile<GROUPED>(order, m_g, p_s, Y, X);
-        p_ya = (int32_t)(Y * kTile);
-        p_xb = (int32_t)(X * kTile);
+        uint64_t r0, c0;
+        slot_origin<C, GROUPED>(order, m_g, p_s, r0, c0);
+        p_ya = (int32_t)r0;
+        p_xb = (int32_t)c0;
       }
     }
   };
@@ -300,8 +321,8 @@ syrk_tma_kernel(const __grid_constant__ CUtensorMap umap, int64_t n, int k_tiles
   int stage = 0;
   uint32_t phase = 0;
   for (uint64_t si = first; si < order.total; si += gridDim.x) {
-    uint64_t Y, X;
-    slot_tile<GROUPED>(order, m_g, si, Y, X);
+    uint64_t row0, col0;
+    slot_origin<C, GROUPED>(order, m_g, si, row0, col0);
 
     double acc[C::MI][C::NI][2];
 #pragma unroll
@@ -311,9 +332,10 @@ syrk_tma_kernel(const __grid_constant__ CUtensorMap umap, int64_t n, int k_tiles
 
     // One 8-deep K slab of stage `st`: 12 fragment loads, 64 DMMAs.
     auto slab_mma = [&](int st, int slab) {
-      const double *sA = smem + st * C::kStageDoubles + (wm * C::MI * 8 + g) * kSlab + tig * 2 + slab * kTile * kSlab;
-      const double *sB =
-          smem + st * C::kStageDoubles + C::kOpDoubles + (wn * C::NI * 8 + g) * kSlab + tig * 2 + slab * kTile * kSlab;
+      const double *sA =
+          smem + st * C::kStageDoubles + (wm * C::MI * 8 + g) * kSlab + tig * 2 + slab * C::kEdge * kSlab;
+      const double *sB = smem + st * C::kStageDoubles + C::kOpDoubles + (wn * C::NI * 8 + g) * kSlab + tig * 2 +
+                         slab * C::kEdge * kSlab;
       double2 a[C::MI], b[C::NI];
 #pragma unroll
       for (int mi = 0; mi < C::MI; ++mi) a[mi] = *reinterpret_cast<const double2 *>(sA + mi * 8 * kSlab);
@@ -366,8 +388,8 @@ syrk_tma_kernel(const __grid_constant__ CUtensorMap umap, int64_t n, int k_tiles
     }
 
     const uint64_t un = (uint64_t)n;
-    const uint64_t y0 = Y * kTile + wm * C::MI * 8 + g;
-    const uint64_t x0 = X * kTile + wn * C::NI * 8 + 2 * tig;
+    const uint64_t y0 = row0 + wm * C::MI * 8 + g;
+    const uint64_t x0 = col0 + wn * C::NI * 8 + 2 * tig;
 #pragma unroll
     for (int mi = 0; mi < C::MI; ++mi) {
       const uint64_t y = y0 + mi * 8;
