@@ -44,10 +44,6 @@ def default_capacity(t: int, buffer_budget: int | None = None) -> int:
     return max(1, budget // (2 * t * t * 8))
 
 
-def _F(n: int, y: int) -> int:
-    return (y * (2 * n + 1 - y)) >> 1
-
-
 def _host_out(out, total: int) -> torch.Tensor:
     if out is None:
         return torch.from_numpy(np.empty(total, dtype=np.float64))

@@ -331,3 +331,12 @@ def test_packed_file_writer_sink_streams_passes(tmp_path, rng):
     with pc.PackedResultReader(path) as r:
         assert r.query(3, 0) == ref[pc.sym_job_id(41, 0, 3)]
         assert np.array_equal(r.read_all(), ref)
+
+
+def test_triangle_indexer_value_object():
+    ti = pc.TriangleIndexer(5)
+    assert ti.sym_count == 15 and ti.nonsym_count == 25
+    assert ti.row_prefix(2) == 9 and ti.job_id(1, 3) == 7 and ti.coord(7) == pc.Coord(1, 3)
+    assert ti.nonsym_job_id(2, 1) == 11 and ti.nonsym_coord(11) == pc.Coord(2, 1)
+    with pytest.raises(ValueError):
+        pc.TriangleIndexer(0)
