@@ -73,7 +73,7 @@ template <int LAYOUT>
 __device__ __forceinline__ void store_cell(const Epilogue &ep, uint64_t y, uint64_t x, uint64_t packed_row_base,
                                            double v) {
   if (LAYOUT == kLayoutPacked) {
-    ep.out[packed_row_base + x] = v;
+    __stcs(ep.out + packed_row_base + x, v);  // streaming: the result is never re-read here, keep L2 for U
   } else if (LAYOUT == kLayoutDense) {
     ep.out[y * (uint64_t)ep.ld_out + x] = v;
     if (x != y) ep.out[x * (uint64_t)ep.ld_out + y] = v;
