@@ -56,7 +56,7 @@ std::mutex g_dev_mu;
 // mbarrier ring); the others are kept for the measured comparison in
 // DESIGN.md (pcc_syrk_f64_variant) and only instantiated for the packed
 // layout.
-using V0 = pcc::SyrkCfg<2, 4, 8, 4, 16, 6>;  // TMA + mbarrier, 8 warps 64x32, BK 16 x 6 stages  (default)
+using V0 = pcc::SyrkCfg<2, 4, 8, 4, 16, 6>;  // TMA + mbarrier, 8 warps 64x32, BK 16 x 6 stages, stage-level fragments (default)
 using V1 = pcc::SyrkCfg<2, 4, 8, 4, 16, 4>;  // cp.async + __syncthreads, 8 warps 64x32, BK 16 x 4
 using V2 = pcc::SyrkCfg<4, 4, 4, 4, 16, 4>;  // cp.async, 16 warps 32x32
 using V3 = pcc::SyrkCfg<2, 4, 8, 4, 32, 3>;  // cp.async, BK 32 x 3
@@ -70,7 +70,8 @@ using V10 = pcc::SyrkCfg<2, 4, 8, 4, 16, 6, 5>;  // TMA, producer 5 steps ahead
 using V11 = pcc::SyrkCfg<2, 4, 8, 4, 16, 6, 6>;  // TMA, producer 6 steps ahead (ring-limited)
 // V12 = V0 visiting tiles in the grouped L2-locality order
 // V13 = V0 with half-stage skew between the two warps of each SMSP
-constexpr int kNumVariants = 14;
+// V14 = V0 loading fragments slab by slab (the previous production inner loop)
+constexpr int kNumVariants = 15;
 // Tail kernel: 64 x 64 quadrants of the GPU tiles of the last partial wave,
 // 4 warps (32 x 32 each), two CTAs per SM -- same per-cell arithmetic.
 using VQ = pcc::SyrkCfg<2, 2, 4, 4, 16, 6>;
@@ -187,6 +188,10 @@ int device_config(const DeviceConfig **out, int device = -1) {
       PCC_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, TL::kSmemBytes), "attr(V12)");
       PCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.variant_ctas[12], kfn, TL::kThreads, TL::kSmemBytes),
                "occupancy(V12)");
+      auto kfn14 = pcc::syrk_tma_kernel<V0, pcc::kLayoutPacked, false, false, false>;
+      PCC_CUDA(cudaFuncSetAttribute(kfn14, cudaFuncAttributeMaxDynamicSharedMemorySize, TL::kSmemBytes), "attr(V14)");
+      PCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.variant_ctas[14], kfn14, TL::kThreads, TL::kSmemBytes),
+               "occupancy(V14)");
       auto kfn13 = pcc::syrk_tma_kernel<V0, pcc::kLayoutPacked, false, true>;
       PCC_CUDA(cudaFuncSetAttribute(kfn13, cudaFuncAttributeMaxDynamicSharedMemorySize, TL::kSmemBytes), "attr(V13)");
       PCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.variant_ctas[13], kfn13, TL::kThreads, TL::kSmemBytes),
@@ -230,7 +235,7 @@ int launch_cfg(const double *u, int64_t n, int64_t l, int64_t ldu, uint64_t tb, 
   return PCC_OK;
 }
 
-template <class C, int LAYOUT, bool GROUPED = false, bool SKEW = false>
+template <class C, int LAYOUT, bool GROUPED = false, bool SKEW = false, bool STAGE_FRAGS = (C::kSlabs <= 2)>
 int launch_tma_cfg(const double *u, int64_t n, int64_t l, int64_t ldu, uint64_t tb, uint64_t te,
                    const pcc::Epilogue &ep, cudaStream_t stream, int ctas_per_sm, int sm_count,
                    int quad_ctas_per_sm = 0) {
@@ -257,7 +262,7 @@ int launch_tma_cfg(const double *u, int64_t n, int64_t l, int64_t ldu, uint64_t 
     while ((group + 1) * (group + 1) <= grid) ++group;
     const pcc::TileOrder order = GROUPED ? pcc::make_tile_order(m_g, tb, main_end, group)
                                          : pcc::TileOrder{tb, main_end, 0, 0, 0, main_end, main_end, mt, 1};
-    pcc::syrk_tma_kernel<C, LAYOUT, GROUPED, SKEW>
+    pcc::syrk_tma_kernel<C, LAYOUT, GROUPED, SKEW, STAGE_FRAGS>
         <<<grid, TL::kThreads, TL::kSmemBytes, stream>>>(map, n, k_tiles, m_g, order, ep);
     PCC_CUDA(cudaGetLastError(), "syrk_tma_kernel launch");
   }
@@ -303,6 +308,8 @@ int launch_syrk(const double *u, int64_t n, int64_t l, int64_t ldu, uint64_t tb,
     case 11: return launch_tma_cfg<V11, pcc::kLayoutPacked>(u, n, l, ldu, tb, te, ep, stream, vc[11], sms);
     case 12: return launch_tma_cfg<V0, pcc::kLayoutPacked, true>(u, n, l, ldu, tb, te, ep, stream, vc[12], sms);
     case 13: return launch_tma_cfg<V0, pcc::kLayoutPacked, false, true>(u, n, l, ldu, tb, te, ep, stream, vc[13], sms);
+    case 14:
+      return launch_tma_cfg<V0, pcc::kLayoutPacked, false, false, false>(u, n, l, ldu, tb, te, ep, stream, vc[14], sms);
     default: return fail(PCC_EINVAL, "unknown contraction variant %d (0..%d)", variant, kNumVariants - 1);
   }
 }

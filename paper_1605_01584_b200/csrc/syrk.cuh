@@ -242,7 +242,7 @@ __device__ __forceinline__ void slot_origin(const TileOrder &o, uint64_t m, uint
   }
 }
 
-template <class C, int LAYOUT, bool GROUPED = false, bool SKEW = false>
+template <class C, int LAYOUT, bool GROUPED = false, bool SKEW = false, bool STAGE_FRAGS = (C::kSlabs <= 2)>
 __global__ void __launch_bounds__(C::kThreads, 1)
 syrk_tma_kernel(const __grid_constant__ CUtensorMap umap, int64_t n, int k_tiles, uint64_t m_g, TileOrder order,
                 Epilogue ep) {
@@ -375,6 +375,43 @@ syrk_tma_kernel(const __grid_constant__ CUtensorMap umap, int64_t n, int k_tiles
         if (kt + 1 < k_tiles) slab_mma(stage, 0);
       }
       c_step += k_tiles;
+    } else if (STAGE_FRAGS) {
+      // Production: all fragments of a stage are loaded before its DMMAs
+      // (253 registers, no spills), so the second slab's loads overlap the
+      // first slab's math and every accumulator's next DMMA is 32 DMMAs
+      // away (measured 94.3 -> 97.1 % of the FP64 peak on c2).
+      for (int kt = 0; kt < k_tiles; ++kt, ++c_step) {
+        if (tid == 0) produce(c_step);
+        mbar_wait(full0 + 8 * stage, phase);
+        const double *sA = smem + stage * C::kStageDoubles + (wm * C::MI * 8 + g) * kSlab + tig * 2;
+        const double *sB = smem + stage * C::kStageDoubles + C::kOpDoubles + (wn * C::NI * 8 + g) * kSlab + tig * 2;
+        double2 a[C::kSlabs][C::MI], b[C::kSlabs][C::NI];
+#pragma unroll
+        for (int slab = 0; slab < C::kSlabs; ++slab) {
+#pragma unroll
+          for (int mi = 0; mi < C::MI; ++mi)
+            a[slab][mi] = *reinterpret_cast<const double2 *>(sA + slab * C::kEdge * kSlab + mi * 8 * kSlab);
+#pragma unroll
+          for (int ni = 0; ni < C::NI; ++ni)
+            b[slab][ni] = *reinterpret_cast<const double2 *>(sB + slab * C::kEdge * kSlab + ni * 8 * kSlab);
+        }
+#pragma unroll
+        for (int slab = 0; slab < C::kSlabs; ++slab) {
+#pragma unroll
+          for (int mi = 0; mi < C::MI; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < C::NI; ++ni)
+              dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], a[slab][mi].x, b[slab][ni].x);
+#pragma unroll
+          for (int mi = 0; mi < C::MI; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < C::NI; ++ni)
+              dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], a[slab][mi].y, b[slab][ni].y);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty0 + 8 * stage);
+        advance(stage, phase);
+      }
     } else {
       for (int kt = 0; kt < k_tiles; ++kt, ++c_step) {
         if (tid == 0) produce(c_step);
