@@ -13,7 +13,9 @@ needed between steps.  Timing is CUDA events on the launching stream, W
 untimed warm-up steps, K timed steps between barrier+synchronize, max over
 ranks.  ``e2e`` times the public API (``allpairs`` / the per-worker shard
 call) with the pinned-host upload of X and the download of this rank's
-packed cells inside the timed region.
+packed cells inside the timed region; for N > 1 each rank uploads only its
+row block of X and the normalised blocks are all-gathered over NCCL
+(distributed.exchange_normalize) before the contraction.
 
 ``--impl reference`` times the reference algorithm's CPU implementation
 (the bit-exact C port under oracle/, all host threads) on a bounded sample
@@ -151,7 +153,9 @@ def _config_dict(cfg: str, world: int) -> dict:
         "l": spec.l,
         "seed": spec.seed,
         "global_batch": spec.n,
-        "parallelism": f"tile-range partition over {world} GPU(s), no collective in the data path",
+        "parallelism": (f"tile-range partition over {world} GPU(s); device step: every rank normalises the "
+                        "rows it needs from its resident X, no collective"
+                        + ("; e2e: row-block upload + NCCL all-gather of U" if world > 1 else "")),
         "l2_policy": "inputs larger than L2 (X and U >= 537 MB vs 126 MB L2); no flush",
         "output": "packed upper triangle n(n+1)/2 f64, sharded per GPU range, kept on device",
     }
@@ -338,8 +342,12 @@ def run_b200(args, rank: int, world: int, local_rank: int) -> None:
         def api_call():
             return pc.allpairs(ds, out=host_out)
     else:
+        # U exchange for the e2e leg: NCCL between distinct GPUs; ranks sharing
+        # one GPU (functional runs only) exchange through host memory (gloo)
+        exch_group = dist.new_group(backend="nccl") if ndev >= world else dist.group.WORLD
+
         def api_call():
-            return compute_worker(ds, world, rank, dev, out=host_out)
+            return compute_worker(ds, world, rank, dev, out=host_out, group=exch_group)
     api_call()  # warm-up
     barrier()
     wall = []
@@ -350,7 +358,7 @@ def run_b200(args, rank: int, world: int, local_rank: int) -> None:
         r = api_call()
         wall.append(time.perf_counter() - a)
     e2e_s = max_over_ranks(statistics.median(wall))
-    h2d = n * l * 8 * world
+    h2d = n * l * 8  # world == 1: all of X; N > 1: one row block of X per rank
     d2h = total_pairs * 8
     if world == 1:
         # sanity: the API result matches the device-timed shard bit for bit
@@ -390,7 +398,9 @@ def run_b200(args, rank: int, world: int, local_rank: int) -> None:
             "vs_baseline": None,
             "dtype": "f64",
             "data": "synthetic",
-            "config": _config_dict(args.config, world),
+            "config": dict(_config_dict(args.config, world),
+                           **({"u_exchange": "nccl all_gather_into_tensor" if ndev >= world
+                               else "gloo via host (ranks share one GPU: functional run)"} if world > 1 else {})),
             "gflops": float(n) * n * l / (ms_step * 1e-3) / 1e9,
             "roofline_fp64_frac_of_step": (float(n) * n * l / world / (ms_step * 1e-3) / 1e12) / peak,
             "syrk_ms": syrk_avg_ms,

@@ -49,6 +49,9 @@ __all__ = [
     "run_workers",
     "compute_worker",
     "check_coverage",
+    "row_slices",
+    "exchange_rows",
+    "exchange_normalize",
 ]
 
 BACKENDS = ("in_process", "subprocess", "cuda")
@@ -367,7 +370,75 @@ def stream_shard(x_host, n: int, l: int, a: WorkerAssignment, device: torch.devi
     return Shard(a.worker_index, device, a.start, a.stop, lo, vals), flags
 
 
-def compute_worker(dataset: Dataset, p: int, worker_index: int, device=None, out=None):
+def row_slices(n: int, p: int) -> tuple[list[tuple[int, int]], int]:
+    """Rows ``[lo, hi)`` each of ``p`` ranks uploads and normalises in exchange
+    mode, and the padded block size ``S`` of the all-gather.
+
+    Blocks are whole 128-row GPU tile bands, ``S = ceil(m_g / p) * 128`` rows
+    each, so rank r owns rows ``[r S, (r+1) S)`` of a ``p S``-row U (clipped to
+    ``n``; trailing ranks may own only pad rows).
+    """
+    if p < 1:
+        raise ValueError(f"rank count must be >= 1, got {p}")
+    T = _lib.GPU_TILE
+    mg = -(-n // T)
+    S = -(-mg // p) * T
+    return [(min(n, r * S), min(n, (r + 1) * S)) for r in range(p)], S
+
+
+def exchange_rows(u: torch.Tensor, flags: torch.Tensor, S: int, rank: int, world: int, group=None) -> None:
+    """All-gather every rank's ``S``-row block of ``u`` (rows ``[rank S, (rank+1) S)``)
+    and of the zero-variance ``flags`` into all ranks, in place.
+
+    NCCL (one GPU per rank): ``all_gather_into_tensor`` straight between the
+    devices over NVLink.  Any other backend (gloo: CPU tests, or functional
+    runs with several ranks sharing one GPU) stages through host memory.
+    """
+    import torch.distributed as dist
+
+    if world == 1:
+        return
+    backend = dist.get_backend(group)
+    blk = slice(rank * S, (rank + 1) * S)
+    if backend == "nccl":
+        dist.all_gather_into_tensor(u, u[blk].clone(), group=group)
+        dist.all_gather_into_tensor(flags, flags[blk].clone(), group=group)
+        return
+    for t in (u, flags):
+        host = t.cpu() if t.is_cuda else t
+        dist.all_gather_into_tensor(host, host[blk].clone(), group=group)
+        if t.is_cuda:
+            t.copy_(host)
+
+
+def exchange_normalize(x_host, n: int, l: int, rank: int, world: int, device: torch.device, group=None):
+    """Exchange-mode K1: this rank uploads and normalises only its row block
+    (``row_slices``), then the blocks are all-gathered so every rank holds
+    all of U -- 1/p of X over each GPU's own PCIe link instead of (almost)
+    all of it, and the rest over NVLink.  Returns ``(u, flags)`` with
+    ``u`` of ``p S`` rows (pad rows zero) and ``flags`` of ``p S`` entries.
+    """
+    L = _lib.lib()
+    slices, S = row_slices(n, world)
+    r0, r1 = slices[rank]
+    ldu = int(L.pcc_ldu(l))
+    with torch.cuda.device(device):
+        s = stream_handle()
+        u = torch.empty((world * S, ldu), dtype=torch.float64, device=device)
+        flags = torch.zeros(world * S, dtype=torch.uint8, device=device)
+        if r1 > r0:
+            xh = x_host if isinstance(x_host, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x_host))
+            xd = torch.empty((r1 - r0, l), dtype=torch.float64, device=device)
+            xd.copy_(xh[r0:r1], non_blocking=xh.is_pinned())
+            _lib.check(L.pcc_normalize_rows_f64(ptr(xd), l, ptr(u) + 8 * r0 * ldu, ldu, ptr(flags) + r0, l, 0,
+                                                r1 - r0, s), f"rank {rank} normalize")
+        pad_lo = max(n, rank * S)
+        _lib.check(L.pcc_zero_rows_f64(ptr(u), ldu, min(pad_lo, (rank + 1) * S), (rank + 1) * S, s), "pad rows")
+        exchange_rows(u, flags, S, rank, world, group)
+    return u, flags
+
+
+def compute_worker(dataset: Dataset, p: int, worker_index: int, device=None, out=None, group=None):
     """Run worker ``worker_index`` of a ``p``-way split as a standalone call.
 
     The one-process-per-GPU form of ``run_workers`` (torchrun ranks): upload,
@@ -375,6 +446,11 @@ def compute_worker(dataset: Dataset, p: int, worker_index: int, device=None, out
     float64 buffer of ``shard_span`` size, pinned for async copies) its owned
     packed cells are downloaded to ``out[index - span_lo]``.  Returns the
     device ``Shard``; ``Shard.zero_variance`` holds the constant rows.
+
+    ``group``: a ``torch.distributed`` group of the ``p`` workers (rank =
+    ``worker_index``).  With it, X is not uploaded whole by every worker:
+    each uploads and normalises its ``row_slices`` block and the blocks are
+    all-gathered (``exchange_normalize``) before the contraction.
     """
     if not 0 <= worker_index < p:
         raise ValueError(f"worker index {worker_index} outside [0, {p})")
@@ -387,7 +463,16 @@ def compute_worker(dataset: Dataset, p: int, worker_index: int, device=None, out
         lo_span, hi_span = shard_span(n, a.start, a.stop)
         if host.numel() < hi_span - lo_span:
             raise ValueError(f"out holds {host.numel()} values, shard needs {hi_span - lo_span}")
-    shard, flags = stream_shard(dataset.values, n, l, a, dev, host)
+    if group is not None and p > 1:
+        u, flags = exchange_normalize(dataset.values, n, l, worker_index, p, dev, group)
+        lo, hi = shard_span(n, a.start, a.stop)
+        with torch.cuda.device(dev):
+            vals = torch.empty(max(hi - lo, 1), dtype=torch.float64, device=dev)
+            run_stream(None, n, l, dev, a.start, a.stop, vals, lo, host, lo, resident=(u, flags))
+        shard = Shard(a.worker_index, dev, a.start, a.stop, lo, vals)
+        flags = flags[:n]
+    else:
+        shard, flags = stream_shard(dataset.values, n, l, a, dev, host)
     shard.zero_variance = frozenset(np.flatnonzero(flags.cpu().numpy()).tolist())
     return shard
 

@@ -167,7 +167,7 @@ def plan_stream(n: int, tile_begin: int, tile_end: int, wave: int, chunk_rows: i
 
 def run_stream(x, n: int, l: int, device: torch.device, tile_begin: int, tile_end: int,
                out_dev: torch.Tensor, out_base: int, host_out: torch.Tensor | None,
-               host_base: int = 0, chunk_rows: int = 8, trace: list | None = None):
+               host_base: int = 0, chunk_rows: int = 8, trace: list | None = None, resident=None):
     """Execute GPU tiles ``[tile_begin, tile_end)`` with overlapped upload,
     normalisation, contraction and download.
 
@@ -177,7 +177,11 @@ def run_stream(x, n: int, l: int, device: torch.device, tile_begin: int, tile_en
     ``host_out[i - host_base]`` receives every packed cell of the range's span.
     ``trace``: if a list is given, ``(label, cuda.Event)`` pairs are appended
     for the upload, pass and download milestones (tools/trace_stream.py).
-    Returns ``(u, flags, x_device)`` after the host has synchronised.
+    ``resident``: ``(u, flags)`` already normalised on ``device`` (e.g. after
+    the multi-GPU row exchange); ``x`` is then ignored and only the
+    contraction passes and downloads run (top-down, no upload phase).
+    Returns ``(u, flags, x_device)`` after the host has synchronised
+    (``x_device`` is None with ``resident``).
     """
 
     def mark(label, stream):
@@ -190,18 +194,24 @@ def run_stream(x, n: int, l: int, device: torch.device, tile_begin: int, tile_en
     with torch.cuda.device(device):
         info = _lib.device_info(device.index)
         wave = info.sm_count * info.syrk_ctas_per_sm
-        plan = plan_stream(n, tile_begin, tile_end, wave, chunk_rows)
+        plan = plan_stream(n, tile_begin, tile_end, wave, chunk_rows, lead=0.0 if resident is not None else None)
         compute = torch.cuda.current_stream()
         s = stream_handle(compute)
-        rows_pad = int(L.pcc_rows_padded(n))
-        ldu = int(L.pcc_ldu(l))
-        u = torch.empty((rows_pad, ldu), dtype=torch.float64, device=device)
-        flags = torch.zeros(n, dtype=torch.uint8, device=device)
         mark("start", compute)
-        _lib.check(L.pcc_zero_rows_f64(ptr(u), ldu, n, rows_pad, s), "pad rows")
+        if resident is not None:
+            u, flags = resident
+            ldu = int(u.shape[1])
+        else:
+            rows_pad = int(L.pcc_rows_padded(n))
+            ldu = int(L.pcc_ldu(l))
+            u = torch.empty((rows_pad, ldu), dtype=torch.float64, device=device)
+            flags = torch.zeros(n, dtype=torch.uint8, device=device)
+            _lib.check(L.pcc_zero_rows_f64(ptr(u), ldu, n, rows_pad, s), "pad rows")
 
-        on_device = isinstance(x, torch.Tensor) and x.is_cuda
-        if on_device:
+        on_device = resident is not None or (isinstance(x, torch.Tensor) and x.is_cuda)
+        if resident is not None:
+            xd = None
+        elif on_device:
             xd = x if x.dtype == torch.float64 else x.to(torch.float64)
             xd = xd.contiguous()
         else:
@@ -252,8 +262,9 @@ def run_stream(x, n: int, l: int, device: torch.device, tile_begin: int, tile_en
                     up.record(copy_in)
                     mark(f"upload rows [{lo},{hi})", copy_in)
                 compute.wait_event(up)
-            _lib.check(L.pcc_normalize_rows_f64(ptr(xd), xd.stride(0), ptr(u), ldu, ptr(flags), l, lo, hi, s),
-                       "normalize")
+            if resident is None:
+                _lib.check(L.pcc_normalize_rows_f64(ptr(xd), xd.stride(0), ptr(u), ldu, ptr(flags), l, lo, hi, s),
+                           "normalize")
             normed = torch.cuda.Event()
             normed.record(compute)
             # every pass whose rows are now normalised, in plan order

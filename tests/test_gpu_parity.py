@@ -299,6 +299,64 @@ def test_compute_worker_streamed_shards_match_single(rng):
                 assert sh.zero_variance == frozenset({1})
 
 
+def _exchange_rank(rank, world, port, x, q):
+    import os
+
+    import torch.distributed as dist
+
+    from paper_1605_01584_b200.distributed import compute_worker, owned_runs, partition, shard_span
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n = x.shape[0]
+        mg = -(-n // 128)
+        lo_t, hi_t = partition(mg * (mg + 1) // 2, world)[rank]
+        lo, hi = shard_span(n, lo_t, hi_t)
+        host = torch.full((max(1, hi - lo),), float("nan"), dtype=torch.float64).pin_memory()
+        sh = compute_worker(pc.Dataset(values=torch.from_numpy(x).pin_memory()), world, rank, 0, out=host,
+                            group=dist.group.WORLD)
+        q.put((rank, [(a, b, host[a - lo:b - lo].numpy().copy()) for a, b in owned_runs(n, lo_t, hi_t)],
+               sorted(sh.zero_variance)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n,l", [(2, 1100, 23), (3, 700, 40), (3, 200, 9)])
+def test_exchange_mode_workers_match_single(world, n, l):
+    """compute_worker(group=...): row-block upload + K1 per rank, U all-gathered
+    (here over gloo: the ranks share this box's one GPU, each rank's kernels
+    independent), then each rank's contraction -- reassembled bit for bit
+    equal to the CPU oracle's packed result, zero-variance set complete on
+    every rank."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    x = random_values(np.random.default_rng(11), n, l, special_rows=True)
+    ref, zv = oracle.allpairs(x, t=4)
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_exchange_rank, args=(r, world, port, x, q)) for r in range(world)]
+    for p_ in procs:
+        p_.start()
+    got = [q.get(timeout=300) for _ in range(world)]
+    for p_ in procs:
+        p_.join(timeout=120)
+        assert p_.exitcode == 0
+    packed = np.full(ref.size, np.nan)
+    for _, runs, zvs in got:
+        assert zvs == sorted(np.flatnonzero(zv).tolist())
+        for a, b, v in runs:
+            packed[a:b] = v
+    assert np.max(np.abs(packed - ref)) <= 1e-12
+    assert np.array_equal(packed, pc.allpairs(pc.Dataset(values=x)).packed)
+
+
 def test_streamed_upload_from_pageable_and_device_inputs(rng):
     x = random_values(rng, 900, 64, special_rows=True)
     ref, zv = oracle.allpairs(x, t=4)
