@@ -327,7 +327,7 @@ def run_b200(args, rank: int, world: int, local_rank: int) -> None:
         "unit": "TFLOP/s",
         "frac": achieved / peak if peak else None,
         "traffic": _load_traffic(args.config),
-        "kernel": "syrk_kernel<packed> (DMMA.8x8x4 FP64)",
+        "kernel": "syrk_tma_kernel<SyrkCfg<2,4,8,4,16,6>, packed, grouped tile order> (TMA ring, DMMA.8x8x4 FP64)",
         "peak_source": "measured live: register-resident mma.sync f64 probe (pcc_probe_fp64_peak); "
                        "MEASURED_PEAKS.json has no FP64 entry",
         "algorithmic_flops_per_launch": flops_launch,

@@ -56,7 +56,8 @@ std::mutex g_dev_mu;
 // mbarrier ring); the others are kept for the measured comparison in
 // DESIGN.md (pcc_syrk_f64_variant) and only instantiated for the packed
 // layout.
-using V0 = pcc::SyrkCfg<2, 4, 8, 4, 16, 6>;  // TMA + mbarrier, 8 warps 64x32, BK 16 x 6 stages, stage-level fragments (default)
+using V0 = pcc::SyrkCfg<2, 4, 8, 4, 16, 6>;  // TMA + mbarrier, 8 warps 64x32, BK 16 x 6 stages, stage-level fragments,
+                                              // grouped tile order (default)
 using V1 = pcc::SyrkCfg<2, 4, 8, 4, 16, 4>;  // cp.async + __syncthreads, 8 warps 64x32, BK 16 x 4
 using V2 = pcc::SyrkCfg<4, 4, 4, 4, 16, 4>;  // cp.async, 16 warps 32x32
 using V3 = pcc::SyrkCfg<2, 4, 8, 4, 32, 3>;  // cp.async, BK 32 x 3
@@ -68,7 +69,8 @@ using V8 = pcc::SyrkCfg<4, 2, 4, 8, 16, 6>;  // TMA, 8 warps 32x64
 using V9 = pcc::SyrkCfg<4, 4, 4, 4, 16, 6>;  // TMA, 16 warps 32x32
 using V10 = pcc::SyrkCfg<2, 4, 8, 4, 16, 6, 5>;  // TMA, producer 5 steps ahead
 using V11 = pcc::SyrkCfg<2, 4, 8, 4, 16, 6, 6>;  // TMA, producer 6 steps ahead (ring-limited)
-// V12 = V0 visiting tiles in the grouped L2-locality order
+// V12 = V0 visiting tiles in plain bijection id order (the previous default;
+//       production visits them in the grouped L2-locality order)
 // V13 = V0 with half-stage skew between the two warps of each SMSP
 // V14 = V0 loading fragments slab by slab (the previous production inner loop)
 constexpr int kNumVariants = 15;
@@ -76,24 +78,24 @@ constexpr int kNumVariants = 15;
 // 4 warps (32 x 32 each), two CTAs per SM -- same per-cell arithmetic.
 using VQ = pcc::SyrkCfg<2, 2, 4, 4, 16, 6>;
 
-template <class C, int LAYOUT>
+template <class C, int LAYOUT, bool GROUPED = false>
 int configure_tma_one(int *ctas) {
   using TL = pcc::TmaLayout<C>;
-  PCC_CUDA(cudaFuncSetAttribute(pcc::syrk_tma_kernel<C, LAYOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  PCC_CUDA(cudaFuncSetAttribute(pcc::syrk_tma_kernel<C, LAYOUT, GROUPED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 TL::kSmemBytes),
            "cudaFuncSetAttribute(syrk_tma smem)");
-  PCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas, pcc::syrk_tma_kernel<C, LAYOUT>, TL::kThreads,
+  PCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas, pcc::syrk_tma_kernel<C, LAYOUT, GROUPED>, TL::kThreads,
                                                          TL::kSmemBytes),
            "cudaOccupancyMaxActiveBlocksPerMultiprocessor(tma)");
   return PCC_OK;
 }
 
-template <class C>
+template <class C, bool GROUPED = false>
 int configure_tma_variant(int *ctas) {
   int c0 = 0, c1 = 0, c2 = 0;
-  int rc = configure_tma_one<C, pcc::kLayoutPacked>(&c0);
-  if (rc == PCC_OK) rc = configure_tma_one<C, pcc::kLayoutDense>(&c1);
-  if (rc == PCC_OK) rc = configure_tma_one<C, pcc::kLayoutTiles>(&c2);
+  int rc = configure_tma_one<C, pcc::kLayoutPacked, GROUPED>(&c0);
+  if (rc == PCC_OK) rc = configure_tma_one<C, pcc::kLayoutDense, GROUPED>(&c1);
+  if (rc == PCC_OK) rc = configure_tma_one<C, pcc::kLayoutTiles, GROUPED>(&c2);
   *ctas = c0 < c1 ? (c0 < c2 ? c0 : c2) : (c1 < c2 ? c1 : c2);
   return rc;
 }
@@ -169,7 +171,8 @@ int device_config(const DeviceConfig **out, int device = -1) {
       return fail(PCC_ECUDA, "device %d is sm_%d%d; this library is built for sm_100a (B200) only", device,
                   p.major, p.minor);
     }
-    int rc = configure_tma_variant<V0>(&c.variant_ctas[0]);
+    int rc = configure_tma_variant<V0, true>(&c.variant_ctas[0]);
+    if (rc == PCC_OK) rc = configure_tma_variant<V0, false>(&c.variant_ctas[12]);
     if (rc == PCC_OK) rc = configure_tma_variant<VQ>(&c.quad_ctas);
     if (rc == PCC_OK) rc = configure_one<V1, pcc::kLayoutPacked>(&c.variant_ctas[1]);
     if (rc == PCC_OK) rc = configure_one<V2, pcc::kLayoutPacked>(&c.variant_ctas[2]);
@@ -184,7 +187,7 @@ int device_config(const DeviceConfig **out, int device = -1) {
     if (rc == PCC_OK) rc = configure_tma_one<V11, pcc::kLayoutPacked>(&c.variant_ctas[11]);
     if (rc == PCC_OK) {
       using TL = pcc::TmaLayout<V0>;
-      auto kfn = pcc::syrk_tma_kernel<V0, pcc::kLayoutPacked, true>;
+      auto kfn = pcc::syrk_tma_kernel<V0, pcc::kLayoutPacked, false>;
       PCC_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, TL::kSmemBytes), "attr(V12)");
       PCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.variant_ctas[12], kfn, TL::kThreads, TL::kSmemBytes),
                "occupancy(V12)");
@@ -291,7 +294,14 @@ int launch_syrk(const double *u, int64_t n, int64_t l, int64_t ldu, uint64_t tb,
   if (rc) return rc;
   const int sms = dc->sm_count;
   const int *vc = dc->variant_ctas;
-  if (variant == 0) return launch_tma_cfg<V0, LAYOUT>(u, n, l, ldu, tb, te, ep, stream, vc[0], sms, dc->quad_ctas);
+  if (variant == 0) {
+    static const bool id_order = [] {  // A/B knob for the tile order, read once
+      const char *e = getenv("PCC_SYRK_ORDER");
+      return e != nullptr && strcmp(e, "id") == 0;
+    }();
+    if (id_order) return launch_tma_cfg<V0, LAYOUT, false>(u, n, l, ldu, tb, te, ep, stream, vc[0], sms, dc->quad_ctas);
+    return launch_tma_cfg<V0, LAYOUT, true>(u, n, l, ldu, tb, te, ep, stream, vc[0], sms, dc->quad_ctas);
+  }
   if (LAYOUT != pcc::kLayoutPacked)
     return fail(PCC_EINVAL, "contraction variant %d is only built for the packed layout", variant);
   switch (variant) {
@@ -306,7 +316,9 @@ int launch_syrk(const double *u, int64_t n, int64_t l, int64_t ldu, uint64_t tb,
     case 9: return launch_tma_cfg<V9, pcc::kLayoutPacked>(u, n, l, ldu, tb, te, ep, stream, vc[9], sms);
     case 10: return launch_tma_cfg<V10, pcc::kLayoutPacked>(u, n, l, ldu, tb, te, ep, stream, vc[10], sms);
     case 11: return launch_tma_cfg<V11, pcc::kLayoutPacked>(u, n, l, ldu, tb, te, ep, stream, vc[11], sms);
-    case 12: return launch_tma_cfg<V0, pcc::kLayoutPacked, true>(u, n, l, ldu, tb, te, ep, stream, vc[12], sms);
+    case 12:
+      return launch_tma_cfg<V0, pcc::kLayoutPacked, false>(u, n, l, ldu, tb, te, ep, stream, vc[12], sms,
+                                                           dc->quad_ctas);
     case 13: return launch_tma_cfg<V0, pcc::kLayoutPacked, false, true>(u, n, l, ldu, tb, te, ep, stream, vc[13], sms);
     case 14:
       return launch_tma_cfg<V0, pcc::kLayoutPacked, false, false, false>(u, n, l, ldu, tb, te, ep, stream, vc[14], sms);

