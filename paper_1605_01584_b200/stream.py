@@ -87,7 +87,7 @@ def lead_fraction(n: int, resident: bool = False) -> float:
 
 
 def plan_stream(n: int, tile_begin: int, tile_end: int, wave: int, chunk_rows: int = 8, mid: int = 8,
-                lead: float | None = None) -> StreamPlan:
+                lead: float | None = None, half_tail: bool = True) -> StreamPlan:
     """Plan the streamed execution of GPU tiles ``[tile_begin, tile_end)``.
 
     X arrives bottom-up in chunks of GPU tile rows -- 2, 2, 4, 4 rows first
@@ -96,9 +96,9 @@ def plan_stream(n: int, tile_begin: int, tile_end: int, wave: int, chunk_rows: i
     releases the tiles whose row bands it completes (tile row Y needs bands
     >= Y only) as one pass, on rotating streams so small early passes share
     the GPU.  Phase 2 (the rest, after the upload): ``mid``-wave passes from
-    the TOP row downwards on one stream, ending in a ramp (4, 2, 1, 1 waves), so the
-    rows finishing last -- and the download left after the final pass --
-    are short middle rows instead of the longest top rows.
+    the TOP row downwards on one stream, ending in a ramp (4, 2, 1, 1/2, 1/2
+    waves), so the rows finishing last -- and the download left after the
+    final pass -- are short middle rows instead of the longest top rows.
     """
     mg = -(-n // T_G)
     if tile_end <= tile_begin:
@@ -153,6 +153,11 @@ def plan_stream(n: int, tile_begin: int, tile_end: int, wave: int, chunk_rows: i
         excess = sum(sizes) - (split - tile_begin)
         sizes[0] -= excess
         sizes = [s for s in sizes if s > 0]
+        if half_tail and len(sizes) > 1 and sizes[-1] == wave and wave >= 2:
+            # last wave as two half-wave passes: each runs as one round of
+            # 64 x 64 quadrants (half a tile time, csrc/pcc_b200.cu tail
+            # kernel), so the download left after the final pass halves
+            sizes[-1:] = [wave // 2, wave - wave // 2]
         lo = tile_begin
         top_row = row_lo
         for s_ in sizes:
