@@ -383,6 +383,12 @@ def run_b200(args, rank: int, world: int, local_rank: int) -> None:
                        f"{res['seconds']:.2f} s"),
         }
 
+    # kernels of the timed region, all ranks: K1 + the contraction's 1-2 launches per step
+    launches = args.steps * (1 + (_lib.syrk_launches(n, tb, te) if te > tb else 0))
+    if world > 1:
+        t = torch.tensor([float(launches)], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        launches = int(t.item())
     value = total_pairs / (ms_step * 1e-3)
     if rank == 0:
         line = {
@@ -408,7 +414,7 @@ def run_b200(args, rank: int, world: int, local_rank: int) -> None:
             "cpu_baseline": cpu,
             "e2e": {"value": total_pairs / e2e_s, "unit": "pairs/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3, "steps": e2e_steps},
-            "gpu_launches": 2 * args.steps,
+            "gpu_launches": launches,
             "clocks": clock,
         }
         print(json.dumps(line), flush=True)

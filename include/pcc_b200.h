@@ -168,6 +168,12 @@ int pcc_naive_pairs_f64(const double *x, int64_t ldx, int64_t n, int64_t l, cons
 int pcc_tile_schedule(int64_t n, uint64_t tile_begin, uint64_t tile_end, uint32_t group, uint64_t *ys,
                       uint64_t *xs);
 
+/* Diagnostics: number of kernels pcc_syrk_f64 launches for the GPU tiles
+ * [tile_begin, tile_end) on the current device (the main persistent kernel
+ * and, when the last partial wave is small, the 64 x 64 quadrant tail
+ * kernel: 0, 1 or 2).  bench.py's gpu_launches count. */
+int pcc_syrk_launches(int64_t n, uint64_t tile_begin, uint64_t tile_end, int32_t *launches);
+
 /* Diagnostics: measured FP64 tensor-pipe (DMMA) throughput of the current
  * device in TFLOP/s, from a register-resident mma.sync f64 loop (~20 ms).
  * Used by bench.py as the live roofline denominator. */

@@ -55,6 +55,7 @@ EXPORTED_SYMBOLS = (
     "pcc_row_stats_f64",
     "pcc_naive_pairs_f64",
     "pcc_tile_schedule",
+    "pcc_syrk_launches",
     "pcc_probe_fp64_peak",
 )
 
@@ -98,6 +99,7 @@ def _bind(l: ctypes.CDLL) -> None:
         "pcc_row_stats_f64": (ctypes.c_int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp]),
         "pcc_naive_pairs_f64": (ctypes.c_int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _u64, _u64, _vp, _vp]),
         "pcc_tile_schedule": (ctypes.c_int, [_i64, _u64, _u64, ctypes.c_uint32, _vp, _vp]),
+        "pcc_syrk_launches": (ctypes.c_int, [_i64, _u64, _u64, ctypes.POINTER(ctypes.c_int32)]),
         "pcc_probe_fp64_peak": (ctypes.c_int, [ctypes.POINTER(ctypes.c_double)]),
     }
     for name, (res, args) in sig.items():
@@ -145,4 +147,11 @@ def probe_fp64_peak() -> float:
     """Measured DMMA (FP64 tensor pipe) TFLOP/s of the current device."""
     v = ctypes.c_double(0.0)
     check(lib().pcc_probe_fp64_peak(ctypes.byref(v)), "pcc_probe_fp64_peak")
+    return v.value
+
+
+def syrk_launches(n: int, tile_begin: int, tile_end: int) -> int:
+    """Kernels ``pcc_syrk_f64`` launches for GPU tiles ``[tile_begin, tile_end)`` on the current device."""
+    v = ctypes.c_int32(0)
+    check(lib().pcc_syrk_launches(n, tile_begin, tile_end, ctypes.byref(v)), "pcc_syrk_launches")
     return v.value

@@ -238,6 +238,13 @@ int launch_cfg(const double *u, int64_t n, int64_t l, int64_t ldu, uint64_t tb, 
   return PCC_OK;
 }
 
+// Tiles of a launch that go to the quadrant tail kernel (see launch_tma_cfg).
+uint64_t quad_tail(uint64_t tiles, uint64_t resident, int sm_count, int quad_ctas_per_sm) {
+  uint64_t tail = quad_ctas_per_sm > 0 ? tiles % resident : 0;
+  if (tail > 0 && 4 * tail > (uint64_t)sm_count * (uint64_t)quad_ctas_per_sm) tail = 0;
+  return tail;
+}
+
 template <class C, int LAYOUT, bool GROUPED = false, bool SKEW = false, bool STAGE_FRAGS = (C::kSlabs <= 2)>
 int launch_tma_cfg(const double *u, int64_t n, int64_t l, int64_t ldu, uint64_t tb, uint64_t te,
                    const pcc::Epilogue &ep, cudaStream_t stream, int ctas_per_sm, int sm_count,
@@ -253,9 +260,7 @@ int launch_tma_cfg(const double *u, int64_t n, int64_t l, int64_t ldu, uint64_t 
   // one round of the tail kernel (64 x 64 quadrants, quad_ctas_per_sm CTAs
   // per SM) finishes in quad_ctas_per_sm / 4 of a tile time instead of a
   // whole one.  Larger remainders gain nothing and stay in the main kernel.
-  const uint64_t tiles = te - tb;
-  uint64_t tail = quad_ctas_per_sm > 0 ? tiles % resident : 0;
-  if (tail > 0 && 4 * tail > (uint64_t)sm_count * (uint64_t)quad_ctas_per_sm) tail = 0;
+  const uint64_t tail = quad_tail(te - tb, resident, sm_count, quad_ctas_per_sm);
   const uint64_t main_end = te - tail;
   if (main_end > tb) {
     const uint64_t mt = main_end - tb;
@@ -595,6 +600,21 @@ int pcc_tile_schedule(int64_t n, uint64_t tile_begin, uint64_t tile_end, uint32_
   const uint64_t m = ceil_div((uint64_t)n, pcc::kTile);
   const pcc::TileOrder o = pcc::make_tile_order(m, tile_begin, tile_end, group);
   for (uint64_t s = 0; s < o.total; ++s) pcc::tile_at(o, m, s, ys[s], xs[s]);
+  return PCC_OK;
+}
+
+int pcc_syrk_launches(int64_t n, uint64_t tile_begin, uint64_t tile_end, int32_t *launches) {
+  if (!launches) return fail(PCC_EINVAL, "launches is NULL");
+  if (n < 1) return fail(PCC_EINVAL, "n must be >= 1");
+  if (tile_begin > tile_end || tile_end > pcc_gpu_tile_count(n))
+    return fail(PCC_EINVAL, "tile range outside the tile matrix");
+  const DeviceConfig *dc = nullptr;
+  int rc = device_config(&dc);
+  if (rc) return rc;
+  const uint64_t tiles = tile_end - tile_begin;
+  const uint64_t resident = (uint64_t)dc->sm_count * (uint64_t)dc->variant_ctas[0];
+  const uint64_t tail = quad_tail(tiles, resident, dc->sm_count, dc->quad_ctas);
+  *launches = (tiles > tail ? 1 : 0) + (tail > 0 ? 1 : 0);
   return PCC_OK;
 }
 
