@@ -176,6 +176,23 @@ __device__ __forceinline__ void cp_async_8(uint32_t dst, const void *src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src));
 }
 
+#ifdef PCC_K1_PHASES
+// tools/k1_phases.cu: per-phase clock totals of normalize_rows_smem_kernel
+__device__ unsigned long long g_k1_phase[8];
+#define K1_MARK(i)                                                              \
+  do {                                                                          \
+    if (threadIdx.x == 0) {                                                     \
+      const long long now_ = clock64();                                         \
+      atomicAdd(&g_k1_phase[i], (unsigned long long)(now_ - k1_t_));            \
+      k1_t_ = now_;                                                             \
+    }                                                                           \
+  } while (0)
+#else
+#define K1_MARK(i) \
+  do {             \
+  } while (0)
+#endif
+
 template <int kNormSmemThreads>
 __global__ void __launch_bounds__(kNormSmemThreads)
 normalize_rows_smem_kernel(const double *__restrict__ x, int64_t ldx, double *__restrict__ u, int64_t ldu,
@@ -188,6 +205,9 @@ normalize_rows_smem_kernel(const double *__restrict__ x, int64_t ldx, double *__
   const int64_t r0 = row_lo + (int64_t)blockIdx.x * rows_per_cta;
   const int rows = (int)((row_hi - r0) < (int64_t)rows_per_cta ? (row_hi - r0) : (int64_t)rows_per_cta);
   const uint32_t sbase = smem_u32(srow);
+#ifdef PCC_K1_PHASES
+  long long k1_t_ = clock64();
+#endif
 
   // 1. stage the rows (16-byte copies when source and destination rows are
   //    16-byte aligned, 8-byte copies otherwise)
@@ -206,74 +226,70 @@ normalize_rows_smem_kernel(const double *__restrict__ x, int64_t ldx, double *__
   cp_async_commit();
   cp_async_wait<0>();
   __syncthreads();
+  K1_MARK(0);
 
-  // 2a. exact constancy test (every element equals the first), all threads
-  for (int r = 0; r < rows; ++r) {
-    const double *xs = srow + (int64_t)r * l;
-    const double first = xs[0];
-    bool v = false;
-    for (int64_t k = tid; k < l; k += kNormSmemThreads) v |= (xs[k] != first);
-    const int varies = __syncthreads_or(v);
-    if (tid == 0) s_zero[r] = !varies;
-  }
-  __syncthreads();
-
-  // 2b. sum8 lane chains: thread (row = tid / 8, lane8 = tid % 8)
+  // 2. the 8 lanes of each row run the reference's chains back to back out
+  //    of shared memory: sum8 with the exact constancy test folded in
+  //    (every element vs the first; OR of the 8 lanes), the mean, then ssd8
+  //    with the centring d = x - mean inline (the subtract and square are off
+  //    the dependent add chain).  No CTA barrier between the phases.
   const int lane8 = tid & 7;
   const int row = tid >> 3;
   const bool active = row < rows;
-  const bool work = active && !s_zero[row];
-  double *sr = srow + (int64_t)(active ? row : 0) * l;
-  const int nsteps = (int)((l - lane8 + 7) >> 3);
-  double s = work ? lane_sum<false, 8>(sr + lane8, nsteps) : 0.0;
+  const double *sr = srow + (int64_t)(active ? row : 0) * l;
+  const int64_t nsteps = (l - lane8 + 7) >> 3;
+  bool varies = false;
+  double s = active ? lane_chain<false, 8>(sr + lane8, nsteps, sr[0], varies) : 0.0;
   s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 1));
   s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 2));
   s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 4));
-  if (work && lane8 == 0) s_mean[row] = __ddiv_rn(s, (double)l);
-  __syncthreads();
-
-  // 2c. centre in place, all threads: d = x - mean (the reference's a[k] - mean)
-  for (int r = 0; r < rows; ++r) {
-    if (s_zero[r]) continue;
-    double *xs = srow + (int64_t)r * l;
-    const double m = s_mean[r];
-    for (int64_t k = tid; k < l; k += kNormSmemThreads) xs[k] = __dsub_rn(xs[k], m);
+  const unsigned vb = __ballot_sync(0xffffffffu, varies);
+  const bool constant = (vb & (0xffu << (tid & 24))) == 0u;
+  double q = 0.0, mean = 0.0;
+  if (active && !constant) {  // uniform within the 8-lane group
+    mean = __ddiv_rn(s, (double)l);
+    bool unused = false;
+    q = lane_chain<true, 8>(sr + lane8, nsteps, mean, unused);
   }
-  __syncthreads();
-
-  // 2d. ssd8 lane chains over d*d
-  double q = work ? lane_sum<true, 8>(sr + lane8, nsteps) : 0.0;
   q = __dadd_rn(q, __shfl_xor_sync(0xffffffffu, q, 1));
   q = __dadd_rn(q, __shfl_xor_sync(0xffffffffu, q, 2));
   q = __dadd_rn(q, __shfl_xor_sync(0xffffffffu, q, 4));
   if (active && lane8 == 0) {
-    const bool zero = !work || q == 0.0;
+    const bool zero = constant || q == 0.0;
     s_zero[row] = zero;
+    s_mean[row] = mean;
     s_scale[row] = zero ? 0.0 : __dsqrt_rn(q);
     zero_variance[r0 + row] = zero ? 1 : 0;
   }
   __syncthreads();
+  K1_MARK(1);
 
-  // 3. write U rows (coalesced): u = d / scale, zero rows for zero variance,
-  //    zero K padding
+  // 3. write U rows (coalesced): u = (x - mean) / scale, zero rows for zero
+  //    variance, zero K padding
   for (int r = 0; r < rows; ++r) {
     double *ur = u + (r0 + r) * ldu;
     const double *ds = srow + (int64_t)r * l;
     if (s_zero[r]) {
       for (int64_t k = tid; k < ldu; k += kNormSmemThreads) ur[k] = 0.0;
     } else {
-      const double sc = s_scale[r];
-      // two independent divisions per iteration keep more of their latency in flight
+      const double sc = s_scale[r], m = s_mean[r];
+      // u = (x - mean) / scale; four independent divisions per iteration keep
+      // more of their latency in flight
+      constexpr int64_t T = kNormSmemThreads;
       int64_t k = tid;
-      for (; k + kNormSmemThreads < l; k += 2 * kNormSmemThreads) {
-        const double q0 = __ddiv_rn(ds[k], sc), q1 = __ddiv_rn(ds[k + kNormSmemThreads], sc);
+      for (; k + 3 * T < l; k += 4 * T) {
+        const double q0 = __ddiv_rn(__dsub_rn(ds[k], m), sc), q1 = __ddiv_rn(__dsub_rn(ds[k + T], m), sc);
+        const double q2 = __ddiv_rn(__dsub_rn(ds[k + 2 * T], m), sc), q3 = __ddiv_rn(__dsub_rn(ds[k + 3 * T], m), sc);
         ur[k] = q0;
-        ur[k + kNormSmemThreads] = q1;
+        ur[k + T] = q1;
+        ur[k + 2 * T] = q2;
+        ur[k + 3 * T] = q3;
       }
-      if (k < l) ur[k] = __ddiv_rn(ds[k], sc);
+      for (; k < l; k += T) ur[k] = __ddiv_rn(__dsub_rn(ds[k], m), sc);
       for (k = l + tid; k < ldu; k += kNormSmemThreads) ur[k] = 0.0;
     }
   }
+  K1_MARK(2);
 }
 
 }  // namespace pcc

@@ -550,3 +550,18 @@ def test_normalize_property_bit_exact(x):
     n, l = x.shape
     assert np.array_equal(u.cpu().numpy()[:n, :l], u_ref)
     assert np.array_equal(zv.cpu().numpy().astype(bool), zv_ref)
+
+
+def test_syrk_launch_count_matches_tail_rule():
+    info = _lib.device_info(0)
+    wave = info.sm_count * info.syrk_ctas_per_sm
+    for n in (16384, 10007, 2000, 129):
+        T = int(_lib.lib().pcc_gpu_tile_count(n))
+        tail = T % wave
+        want = (1 if T > tail or tail == 0 else 0) + (1 if 0 < tail <= wave // 2 else 0)
+        if tail > wave // 2:
+            want = 1
+        assert _lib.syrk_launches(n, 0, T) == want, n
+    assert _lib.syrk_launches(16384, 5, 5) == 0
+    with pytest.raises(ValueError):
+        _lib.syrk_launches(100, 0, 10**6)
