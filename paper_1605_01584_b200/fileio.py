@@ -29,10 +29,19 @@ from .tiles import CorrelationResult, TileGeometry, _scatter_host
 from .transform import Dataset
 
 __all__ = ["save_dataset", "load_dataset", "save_result", "load_result", "query_pair", "PackedResultReader",
-           "PackedFileWriterSink", "allpairs_to_file"]
+           "PackedFileWriterSink", "allpairs_to_file", "gen_synthetic"]
 
 _HDR = struct.Struct("<4sIQQ")
 _VERSION = 1
+
+
+def gen_synthetic(n: int, l: int, seed: int = 0) -> Dataset:
+    """Deterministic uniform [0, 1) dataset (fileio.py:295-305): element k of
+    the row-major array is splitmix64(seed + (k+1) * golden) >> 11 * 2^-53,
+    bit-identical to the reference (tests/golden/helpers.json)."""
+    from .workloads import gen_uniform_splitmix64
+
+    return Dataset(values=gen_uniform_splitmix64(n, l, seed))
 
 
 def save_dataset(path, dataset: Dataset) -> None:

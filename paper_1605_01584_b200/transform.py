@@ -32,6 +32,9 @@ __all__ = [
     "normalize",
     "normalize_device",
     "estimate_cost",
+    "pcc_normalized",
+    "pcc_naive",
+    "allpairs_naive",
 ]
 
 
@@ -172,3 +175,76 @@ def estimate_cost(n: int, l: int) -> int:
     if l < 1:
         raise ValueError(f"l must be >= 1, got {l}")
     return 5 * l * n + l * n * (n + 1) // 2
+
+
+# ---------------------------------------------------------------------------
+# The reference's per-pair helpers (transform.py:127-179), on the GPU.
+
+def _as_row(v) -> np.ndarray:
+    row = np.ascontiguousarray(v.cpu().numpy() if isinstance(v, torch.Tensor) else v, dtype=np.float64)
+    if row.ndim != 1:
+        raise ValueError("expected a 1-D vector")
+    return row
+
+
+class _Rows:
+    """Unvalidated ``n x l`` rows for the naive kernels (the reference's
+    per-pair helpers take raw vectors, not a ``Dataset``)."""
+
+    def __init__(self, values: np.ndarray):
+        self.values = values
+        self.n, self.l = int(values.shape[0]), int(values.shape[1])
+
+
+def pcc_normalized(u_i, u_j) -> float:
+    """Correlation of two already-normalised rows (transform.py:134-144): their
+    dot product, computed by the engine's own contraction (K2 on a two-row U)
+    -- within 1e-12 of the reference's fixed-order ``dot8``, like every engine
+    coefficient.  A zero-variance (all-zero) row gives 0.0."""
+    a, b = _as_row(u_i), _as_row(u_j)
+    if a.shape[0] != b.shape[0]:
+        raise ValueError(f"length mismatch: {a.shape[0]} vs {b.shape[0]}")
+    require_cuda()
+    L = _lib.lib()
+    l = int(a.shape[0])
+    if l == 0:
+        return 0.0
+    dev = torch.device("cuda", torch.cuda.current_device())
+    ldu = int(L.pcc_ldu(l))
+    u = torch.zeros((int(L.pcc_rows_padded(2)), ldu), dtype=torch.float64, device=dev)
+    u[0, :l] = torch.from_numpy(a).to(dev)
+    u[1, :l] = torch.from_numpy(b).to(dev)
+    out = torch.empty(3, dtype=torch.float64, device=dev)
+    _lib.check(L.pcc_syrk_f64(ptr(u), 2, l, ldu, 0, 1, _lib.LAYOUT_PACKED, ptr(out), 0, 0, 0, 0, 0, stream_handle()),
+               "pcc_normalized")
+    return float(out[1].item())
+
+
+def pcc_naive(u, v) -> float:
+    """Pearson correlation straight from the definition (transform.py:147-160),
+    evaluated by the GPU oracle kernel (csrc/verify.cuh) -- bit-identical to
+    the reference's ``pcc_naive_pair``; 0.0 if either vector is constant."""
+    from .verify import _Naive
+
+    a, b = _as_row(u), _as_row(v)
+    if a.shape[0] != b.shape[0]:
+        raise ValueError(f"length mismatch: {a.shape[0]} vs {b.shape[0]}")
+    if a.shape[0] < 2:
+        raise ValueError("need at least 2 samples")
+    return float(_Naive(_Rows(np.stack([a, b]))).pairs(1, 2)[0].item())
+
+
+def allpairs_naive(dataset: Dataset):
+    """Brute-force oracle (transform.py:163-179): every upper-triangle pair from
+    the definition, on the GPU (bit-identical to the reference's
+    ``naive_allpairs_packed``); ``zero_variance`` = ``constant_row_flags``
+    (_kernels.py:276-286: exactly constant, or ssd == 0.0), as in the reference."""
+    from .indexing import sym_job_count
+    from .tiles import CorrelationResult
+    from .verify import _Naive
+
+    if not isinstance(dataset, Dataset):
+        raise TypeError("allpairs_naive expects a Dataset")
+    nv = _Naive(dataset)
+    packed = nv.pairs(0, sym_job_count(nv.n)).cpu().numpy()
+    return CorrelationResult(n=nv.n, packed=packed, zero_variance=nv.zero_variance())

@@ -106,7 +106,34 @@ def small_cases() -> dict[str, np.ndarray]:
     return cases
 
 
+def extras() -> None:
+    """Reference-API helpers outside the engine path: gen_synthetic
+    (fileio.py:295-305) values and pcc_naive / pcc_normalized
+    (transform.py:134-160) on a few vector pairs, as exact hex floats."""
+    gens = {}
+    for n, l, seed in [(3, 5, 7), (1, 9, 0), (4, 3, 2**63 + 11)]:
+        gens[f"{n},{l},{seed}"] = [float(v).hex() for v in pc.gen_synthetic(n, l, seed=seed).values.ravel()]
+    rng = np.random.default_rng(99)
+    pairs = []
+    vecs = [(np.array([1.0, 2.0, 4.0]), np.array([1.0, 3.0, 5.0])),
+            (np.array([3.0, 3.0, 3.0, 3.0]), np.array([1.0, 2.0, 3.0, 4.0])),
+            (np.array([1e-160, 2e-160, 4e-160]), np.array([5.0, -1.0, 2.0])),
+            (rng.standard_normal(1001), rng.standard_normal(1001)),
+            (rng.lognormal(2.0, 1.0, 77), rng.lognormal(2.0, 1.0, 77))]
+    for a, b in vecs:
+        ua = pc.normalize(pc.Dataset(values=np.stack([a, b])), threads=1).u
+        pairs.append({"a": [float(v).hex() for v in a], "b": [float(v).hex() for v in b],
+                      "naive": float(pc.pcc_naive(a, b)).hex(),
+                      "normalized": float(pc.pcc_normalized(ua[0], ua[1])).hex()})
+    (HERE / "helpers.json").write_text(json.dumps({"gen_synthetic": gens, "pairs": pairs}, indent=1))
+
+
 def main() -> None:
+    if "--extras" in sys.argv:
+        extras()
+        print("helper fixtures written to", HERE)
+        return
+    extras()
     out = {}
     for name, x in small_cases().items():
         d = pc.Dataset(values=x)

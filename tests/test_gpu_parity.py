@@ -565,3 +565,35 @@ def test_syrk_launch_count_matches_tail_rule():
     assert _lib.syrk_launches(16384, 5, 5) == 0
     with pytest.raises(ValueError):
         _lib.syrk_launches(100, 0, 10**6)
+
+
+def test_reference_pair_helpers_match_reference_outputs():
+    """pcc_naive (GPU definition kernel) bit-identical to the reference's
+    pcc_naive; pcc_normalized (the engine's contraction on two rows) within
+    1e-12 of the reference's dot8 (tests/golden/helpers.json)."""
+    import json
+
+    from conftest import GOLDEN
+
+    pairs = json.loads((GOLDEN / "helpers.json").read_text())["pairs"]
+    for case in pairs:
+        a = np.array([float.fromhex(v) for v in case["a"]])
+        b = np.array([float.fromhex(v) for v in case["b"]])
+        assert float(pc.pcc_naive(a, b)).hex() == case["naive"]
+        u, _ = oracle.normalize(np.stack([a, b]))
+        assert abs(pc.pcc_normalized(u[0], u[1]) - float.fromhex(case["normalized"])) <= 1e-12
+    with pytest.raises(ValueError):
+        pc.pcc_naive([1.0, 2.0], [1.0, 2.0, 3.0])
+    with pytest.raises(ValueError):
+        pc.pcc_naive([1.0], [2.0])
+    with pytest.raises(ValueError):
+        pc.pcc_normalized([1.0, 2.0], [1.0])
+
+
+def test_allpairs_naive_bit_identical_to_reference_golden(golden_small):
+    assert len(golden_small) >= 30
+    for name, case in golden_small.items():
+        x = case["x"]
+        r = pc.allpairs_naive(pc.Dataset(values=x))
+        assert np.array_equal(r.packed, case["naive"]), name
+        assert r.zero_variance == frozenset(np.flatnonzero(oracle.constant_row_flags(x)).tolist())

@@ -340,3 +340,14 @@ def test_triangle_indexer_value_object():
     assert ti.nonsym_job_id(2, 1) == 11 and ti.nonsym_coord(11) == pc.Coord(2, 1)
     with pytest.raises(ValueError):
         pc.TriangleIndexer(0)
+
+
+def test_gen_synthetic_bit_identical_to_reference():
+    """fileio.gen_synthetic against the reference's own output (tests/golden/helpers.json)."""
+    g = json.loads((GOLDEN / "helpers.json").read_text())["gen_synthetic"]
+    for key, vals in g.items():
+        n, l, seed = (int(v) for v in key.split(","))
+        got = pc.gen_synthetic(n, l, seed=seed).values.ravel()
+        assert [float(v).hex() for v in got] == vals, key
+    with pytest.raises(ValueError):
+        pc.gen_synthetic(0, 3)
