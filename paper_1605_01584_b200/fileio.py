@@ -53,10 +53,17 @@ def save_dataset(path, dataset: Dataset) -> None:
 
 
 def load_dataset(path, format: str = "auto") -> Dataset:
-    """Read an ``LPCC`` dataset (fileio.py:65-99, binary container)."""
+    """Load a dataset (fileio.py:65-78): ``format`` is ``auto`` (magic bytes
+    decide), ``binary`` (the LPCC container) or ``tsv`` (whitespace-separated
+    text, optional label column)."""
     path = Path(path)
-    if format not in ("auto", "binary"):
-        raise ValueError(f"unsupported format {format!r} (this build reads the binary LPCC container)")
+    if format not in ("auto", "binary", "tsv"):
+        raise ValueError(f"unknown format {format!r}")
+    if format == "auto":
+        with open(path, "rb") as f:
+            format = "binary" if f.read(4) == b"LPCC" else "tsv"
+    if format == "tsv":
+        return _load_dataset_tsv(path)
     size = path.stat().st_size
     with open(path, "rb") as f:
         head = f.read(_HDR.size)
@@ -71,6 +78,55 @@ def load_dataset(path, format: str = "auto") -> Dataset:
             raise DataError(f"{path}: file is {size} bytes but header declares {_HDR.size + 8 * n * l}")
         values = np.fromfile(f, dtype="<f8", count=n * l)
     return Dataset(values=values.astype(np.float64, copy=False).reshape(n, l))
+
+
+def _is_number(text: str) -> bool:
+    try:
+        float(text)
+    except ValueError:
+        return False
+    return True
+
+
+def _load_dataset_tsv(path: Path) -> Dataset:
+    """Text rows of numbers, whitespace separated; a non-numeric first field
+    on the first row makes column 1 a label column for every row
+    (fileio.py:102-141, same checks and messages)."""
+    import math
+
+    rows: list[list[float]] = []
+    ids: list[str] = []
+    labeled = None
+    width = None
+    with open(path, "r", encoding="utf-8") as f:
+        for lineno, line in enumerate(f, start=1):
+            fields = line.split()
+            if not fields:
+                continue
+            if labeled is None:
+                labeled = not _is_number(fields[0])
+            if labeled:
+                if _is_number(fields[0]):
+                    raise DataError(f"{path}:{lineno}: expected a label in column 1, got {fields[0]!r}")
+                ids.append(fields[0])
+                fields = fields[1:]
+            row = []
+            for col, field in enumerate(fields, start=2 if labeled else 1):
+                try:
+                    value = float(field)
+                except ValueError:
+                    raise DataError(f"{path}:{lineno}: column {col}: {field!r} is not a number") from None
+                if not math.isfinite(value):
+                    raise DataError(f"{path}:{lineno}: column {col}: non-finite value {field!r}")
+                row.append(value)
+            if width is None:
+                width = len(row)
+            elif len(row) != width:
+                raise DataError(f"{path}:{lineno}: ragged row of {len(row)} samples, expected {width}")
+            rows.append(row)
+    if not rows:
+        raise DataError(f"{path}: empty dataset")
+    return Dataset(values=np.array(rows, dtype=np.float64), ids=ids if labeled else None)
 
 
 def save_result(path, result: CorrelationResult) -> None:

@@ -351,3 +351,22 @@ def test_gen_synthetic_bit_identical_to_reference():
         assert [float(v).hex() for v in got] == vals, key
     with pytest.raises(ValueError):
         pc.gen_synthetic(0, 3)
+
+
+def test_load_dataset_tsv_like_reference(tmp_path):
+    p = tmp_path / "d.tsv"
+    p.write_text("geneA 1 2 3\n\ngeneB 4.5 -1 2e3\n")
+    d = pc.load_dataset(p)
+    assert d.ids == ["geneA", "geneB"] and d.values.tolist() == [[1, 2, 3], [4.5, -1, 2000.0]]
+    p.write_text("1 2\n3 4\n")
+    assert pc.load_dataset(p, format="tsv").ids is None
+    for bad, msg in [("a 1 2\n3 4 5\n", "expected a label"), ("1 2\n3\n", "ragged"), ("1 x\n", "not a number"),
+                     ("1 inf\n", "non-finite"), ("\n\n", "empty")]:
+        p.write_text(bad)
+        with pytest.raises(pc.DataError, match=msg):
+            pc.load_dataset(p)
+    with pytest.raises(ValueError):
+        pc.load_dataset(p, format="csv")
+    b = tmp_path / "d.lpcc"
+    pc.save_dataset(b, pc.Dataset(values=np.arange(6.0).reshape(2, 3)))
+    assert pc.load_dataset(b).values.tolist() == [[0, 1, 2], [3, 4, 5]]
