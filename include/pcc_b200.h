@@ -117,10 +117,22 @@ int pcc_syrk_f64(const double *u, int64_t n, int64_t l, int64_t ldu, uint64_t ti
                  uint64_t tile_end, int32_t layout, double *out, int64_t ld_out, uint64_t out_base,
                  int32_t ref_t, uint64_t ref_begin, uint64_t ref_end, void *stream);
 
+/* The contraction in the reference's own arithmetic, bit-identical to
+ * _kernels.dot8 (_kernels.py:30-68) for every cell: eight lane sums of
+ * separately rounded products, k = j (mod 8) in increasing k, then the fixed
+ * tree.  Runs on the FP64 CUDA cores (about half the tensor path's speed);
+ * same arguments, layouts and errors as pcc_syrk_f64.  Same as
+ * pcc_syrk_f64_variant(PCC_VARIANT_EXACT, ...). */
+#define PCC_VARIANT_EXACT 100
+int pcc_syrk_exact_f64(const double *u, int64_t n, int64_t l, int64_t ldu, uint64_t tile_begin,
+                       uint64_t tile_end, int32_t layout, double *out, int64_t ld_out, uint64_t out_base,
+                       int32_t ref_t, uint64_t ref_begin, uint64_t ref_end, void *stream);
+
 /* Same as pcc_syrk_f64 with an explicit contraction kernel shape (0 = the
  * production default; 1..4 = the alternatives measured in DESIGN.md).  Every
  * shape computes each cell with the same K order, so all variants produce
- * bitwise identical results; this entry point exists for tuning. */
+ * bitwise identical results; this entry point exists for tuning.
+ * PCC_VARIANT_EXACT selects the bit-exact dot8 kernel (pcc_syrk_exact_f64). */
 int pcc_syrk_f64_variant(int32_t variant, const double *u, int64_t n, int64_t l, int64_t ldu,
                          uint64_t tile_begin, uint64_t tile_end, int32_t layout, double *out,
                          int64_t ld_out, uint64_t out_base, int32_t ref_t, uint64_t ref_begin,
@@ -133,6 +145,12 @@ int pcc_syrk_f64_variant(int32_t variant, const double *u, int64_t n, int64_t l,
  * (tiles.py:133-199).  Launches the GPU tiles that cover the range. */
 int pcc_compute_pass_f64(const double *u, int64_t n, int64_t l, int64_t ldu, int64_t t,
                          uint64_t j_lo, uint64_t j_hi, double *out, void *stream);
+
+/* pcc_compute_pass_f64 with the bit-exact contraction (pcc_syrk_exact_f64):
+ * the pass buffer equals the reference's compute_tile_range output bit for
+ * bit. */
+int pcc_compute_pass_exact_f64(const double *u, int64_t n, int64_t l, int64_t ldu, int64_t t,
+                               uint64_t j_lo, uint64_t j_hi, double *out, void *stream);
 
 /* Replaces _kernels.scatter_range(packed, values, first_tile, count, m, t, n)
  * (_kernels.py:322-348) on device: copies cells y <= x < n of `count`

@@ -36,6 +36,7 @@ PCC_OK, PCC_EINVAL, PCC_ECUDA = 0, 1, 2
 GPU_TILE = 128
 K_ALIGN = 32
 LAYOUT_PACKED, LAYOUT_DENSE, LAYOUT_TILES = 0, 1, 2
+VARIANT_EXACT = 100  # PCC_VARIANT_EXACT: the bit-exact dot8 contraction
 
 # Every symbol include/pcc_b200.h declares (tests check the .so exports them).
 EXPORTED_SYMBOLS = (
@@ -49,7 +50,9 @@ EXPORTED_SYMBOLS = (
     "pcc_zero_rows_f64",
     "pcc_syrk_f64",
     "pcc_syrk_f64_variant",
+    "pcc_syrk_exact_f64",
     "pcc_compute_pass_f64",
+    "pcc_compute_pass_exact_f64",
     "pcc_scatter_range_f64",
     "pcc_allpairs_f64",
     "pcc_row_stats_f64",
@@ -93,7 +96,9 @@ def _bind(l: ctypes.CDLL) -> None:
         "pcc_zero_rows_f64": (ctypes.c_int, [_vp, _i64, _i64, _i64, _vp]),
         "pcc_syrk_f64": (ctypes.c_int, [_vp, _i64, _i64, _i64, _u64, _u64, _i32, _vp, _i64, _u64, _i32, _u64, _u64, _vp]),
         "pcc_syrk_f64_variant": (ctypes.c_int, [_i32, _vp, _i64, _i64, _i64, _u64, _u64, _i32, _vp, _i64, _u64, _i32, _u64, _u64, _vp]),
+        "pcc_syrk_exact_f64": (ctypes.c_int, [_vp, _i64, _i64, _i64, _u64, _u64, _i32, _vp, _i64, _u64, _i32, _u64, _u64, _vp]),
         "pcc_compute_pass_f64": (ctypes.c_int, [_vp, _i64, _i64, _i64, _i64, _u64, _u64, _vp, _vp]),
+        "pcc_compute_pass_exact_f64": (ctypes.c_int, [_vp, _i64, _i64, _i64, _i64, _u64, _u64, _vp, _vp]),
         "pcc_scatter_range_f64": (ctypes.c_int, [_vp, _vp, _u64, _u64, _i64, _i64, _vp]),
         "pcc_allpairs_f64": (ctypes.c_int, [_vp, _i64, _i64, _i64, _vp, _i64, _vp, _u64, _u64, _i32, _vp, _i64, _u64, _vp]),
         "pcc_row_stats_f64": (ctypes.c_int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp]),
@@ -155,3 +160,9 @@ def syrk_launches(n: int, tile_begin: int, tile_end: int) -> int:
     v = ctypes.c_int32(0)
     check(lib().pcc_syrk_launches(n, tile_begin, tile_end, ctypes.byref(v)), "pcc_syrk_launches")
     return v.value
+
+
+def syrk_fn(exact: bool = False):
+    """The contraction entry point: the tensor-core path (``pcc_syrk_f64``) or
+    the bit-exact dot8 path (``pcc_syrk_exact_f64``); same arguments."""
+    return lib().pcc_syrk_exact_f64 if exact else lib().pcc_syrk_f64

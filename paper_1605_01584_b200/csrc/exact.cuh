@@ -1,0 +1,143 @@
+// exact.cuh -- K2x: the contraction in the reference's own arithmetic, bit for
+// bit.  Every coefficient is _kernels.dot8(u[y], u[x]) (_kernels.py:30-68):
+// eight lane sums, lane j adding RN(u[y][k] * u[x][k]) for k = j (mod 8) in
+// increasing k (separate multiply and add -- no FMA), then the fixed tree
+// ((s0+s1)+(s2+s3))+((s4+s5)+(s6+s7)).  It runs on the FP64 CUDA cores
+// (DMUL + DADD: two FP64 operations per term, vs one DMMA FMA lane-op on the
+// tensor path), so it is the bit-exact mode, not the fast one.
+//
+// Work unit = one 32 x 64 sub-block of a 128 x 128 GPU tile (8 per tile,
+// persistent grid-stride over [tile_begin, tile_end) x 8).  256 threads:
+// thread t is reference lane j = t & 7 for an 8 x 8 cell block, so each
+// thread carries 64 independent lane accumulators (the dependent add chains
+// overlap one another) and the 8 lanes of a cell sit in 8 consecutive
+// threads.  U's rows stream through a 4-stage cp.async ring of 32-column
+// K chunks (pitch 40 doubles; rows of odd 8-row blocks shifted by 8 doubles,
+// so the four 8-lane groups of a warp reading four different row blocks
+// pair up on opposite bank halves: the minimum two wavefronts per 64-bit
+// load).  Zero K padding only adds +0.0 to lane sums
+// that can never be -0.0, so the padded length changes no bit.  The tree is
+// three xor-shuffles (1, 2, 4), which pair the lanes exactly as the tree.
+#pragma once
+
+#include "syrk.cuh"
+
+namespace pcc {
+
+struct ExactCfg {
+  static constexpr int kThreads = 256;
+  static constexpr int BM = 32;      // sub-block rows (y)
+  static constexpr int BN = 64;      // sub-block columns (x)
+  static constexpr int BK = 32;      // K chunk (4 steps of each lane)
+  static constexpr int kPitch = 40;  // doubles per staged row
+  static constexpr int STAGES = 4;
+  static constexpr int kStageDoubles = (BM + BN) * kPitch;
+  static constexpr int kSmemBytes = STAGES * kStageDoubles * (int)sizeof(double);
+  static constexpr int kSubPerTile = (kTile / BM) * (kTile / BN);  // 8
+};
+
+// Staged row r of a chunk (0..BM-1: A rows, BM..: B rows) starts here.
+__device__ __forceinline__ int row_off(int r) { return r * ExactCfg::kPitch + ((r >> 3) & 1) * 8; }
+
+template <int LAYOUT>
+__global__ void __launch_bounds__(ExactCfg::kThreads, 1)
+syrk_exact_kernel(const double *__restrict__ u, int64_t n, int64_t ldu, int k_chunks, uint64_t m_g,
+                  uint64_t tile_begin, uint64_t tile_end, Epilogue ep) {
+  using C = ExactCfg;
+  extern __shared__ __align__(128) double smem[];
+  const int tid = threadIdx.x;
+  const int lane8 = tid & 7;
+  const int grp = tid >> 3;         // 0..31: which 8 x 8 cell block
+  const int bi = grp >> 3;          // 0..3  -> rows bi*8 .. +8 of the sub-block
+  const int bj = grp & 7;           // 0..7  -> cols bj*8 .. +8
+  const uint64_t un = (uint64_t)n;
+  const uint64_t units = (tile_end - tile_begin) * C::kSubPerTile;
+
+  for (uint64_t w = blockIdx.x; w < units; w += gridDim.x) {
+    const uint64_t J = tile_begin + w / C::kSubPerTile;
+    const int sub = (int)(w % C::kSubPerTile);
+    const uint64_t Y = tile_row(m_g, J);
+    const uint64_t X = J + Y - row_prefix(m_g, Y);
+    const uint64_t row0 = Y * kTile + (uint64_t)(sub >> 1) * C::BM;
+    const uint64_t col0 = X * kTile + (uint64_t)(sub & 1) * C::BN;
+    // nothing of the triangle / of [0, n) in this sub-block: skip it
+    if (row0 >= un || col0 >= un || col0 + C::BN - 1 < row0) continue;
+
+    auto load_chunk = [&](int stage, int kc) {
+      double *sa = smem + stage * C::kStageDoubles;
+      const int64_t k0 = (int64_t)kc * C::BK;
+      // (BM + BN) rows x 32 doubles = 8 x 16-byte pieces per row
+      for (int i = tid; i < (C::BM + C::BN) * (C::BK / 2); i += C::kThreads) {
+        const int r = i >> 4, piece = i & 15;
+        const uint64_t grow = r < C::BM ? row0 + r : col0 + (r - C::BM);
+        cp_async_16(smem_u32(sa + row_off(r) + piece * 2), u + grow * (uint64_t)ldu + k0 + piece * 2);
+      }
+    };
+
+    double acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) acc[i][c] = 0.0;
+
+#pragma unroll
+    for (int s = 0; s < C::STAGES - 1; ++s) {
+      if (s < k_chunks) load_chunk(s, s);
+      cp_async_commit();
+    }
+    for (int kc = 0; kc < k_chunks; ++kc) {
+      cp_async_wait<C::STAGES - 2>();
+      __syncthreads();
+      {
+        const int nxt = kc + C::STAGES - 1;
+        if (nxt < k_chunks) load_chunk(nxt % C::STAGES, nxt);
+        cp_async_commit();
+      }
+      const double *sa = smem + (kc % C::STAGES) * C::kStageDoubles + row_off(bi * 8) + lane8;
+      const double *sb = smem + (kc % C::STAGES) * C::kStageDoubles + row_off(C::BM + bj * 8) + lane8;
+#pragma unroll
+      for (int m = 0; m < C::BK / 8; ++m) {  // this lane's k = kc*32 + m*8 + lane8, increasing
+        double a[8], b[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) a[i] = sa[i * C::kPitch + m * 8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) b[c] = sb[c * C::kPitch + m * 8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          // all eight products of the row first: each add waits on a
+          // multiply issued eight FP64 instructions earlier
+          double p[8];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) p[c] = __dmul_rn(a[i], b[c]);
+#pragma unroll
+          for (int c = 0; c < 8; ++c) acc[i][c] = __dadd_rn(acc[i][c], p[c]);
+        }
+      }
+    }
+    cp_async_wait<0>();
+    __syncthreads();  // the ring is reloaded by the next unit
+
+    // the fixed tree across the 8 lanes of each cell, then lane j stores
+    // column j of the thread group's 8 x 8 block (8 consecutive cells per row)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      double mine = 0.0;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        double v = acc[i][c];
+        v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, 1));
+        v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, 2));
+        v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, 4));
+        if (c == lane8) mine = v;
+      }
+      const uint64_t y = row0 + bi * 8 + i;
+      const uint64_t x = col0 + bj * 8 + lane8;
+      if (y < un && x >= y && x < un) {
+        const uint64_t prb = (LAYOUT == kLayoutPacked) ? row_prefix(un, y) - y - ep.out_base : 0;
+        store_cell<LAYOUT>(ep, y, x, prb, mine);
+      }
+    }
+  }
+}
+
+}  // namespace pcc

@@ -12,6 +12,7 @@
 
 #include "../../include/pcc_b200.h"
 #include "normalize.cuh"
+#include "exact.cuh"
 #include "syrk.cuh"
 #include "verify.cuh"
 
@@ -45,6 +46,7 @@ struct DeviceConfig {
   int syrk_ctas_per_sm = 0;
   int variant_ctas[16] = {0};
   int quad_ctas = 0;
+  int exact_ctas = 0;
   size_t total_mem = 0;
 };
 
@@ -96,6 +98,27 @@ int configure_tma_variant(int *ctas) {
   int rc = configure_tma_one<C, pcc::kLayoutPacked, GROUPED>(&c0);
   if (rc == PCC_OK) rc = configure_tma_one<C, pcc::kLayoutDense, GROUPED>(&c1);
   if (rc == PCC_OK) rc = configure_tma_one<C, pcc::kLayoutTiles, GROUPED>(&c2);
+  *ctas = c0 < c1 ? (c0 < c2 ? c0 : c2) : (c1 < c2 ? c1 : c2);
+  return rc;
+}
+
+template <int LAYOUT>
+int configure_exact_one(int *ctas) {
+  using C = pcc::ExactCfg;
+  PCC_CUDA(cudaFuncSetAttribute(pcc::syrk_exact_kernel<LAYOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                C::kSmemBytes),
+           "cudaFuncSetAttribute(syrk_exact smem)");
+  PCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas, pcc::syrk_exact_kernel<LAYOUT>, C::kThreads,
+                                                         C::kSmemBytes),
+           "cudaOccupancyMaxActiveBlocksPerMultiprocessor(exact)");
+  return PCC_OK;
+}
+
+int configure_exact(int *ctas) {
+  int c0 = 0, c1 = 0, c2 = 0;
+  int rc = configure_exact_one<pcc::kLayoutPacked>(&c0);
+  if (rc == PCC_OK) rc = configure_exact_one<pcc::kLayoutDense>(&c1);
+  if (rc == PCC_OK) rc = configure_exact_one<pcc::kLayoutTiles>(&c2);
   *ctas = c0 < c1 ? (c0 < c2 ? c0 : c2) : (c1 < c2 ? c1 : c2);
   return rc;
 }
@@ -174,6 +197,7 @@ int device_config(const DeviceConfig **out, int device = -1) {
     int rc = configure_tma_variant<V0, true>(&c.variant_ctas[0]);
     if (rc == PCC_OK) rc = configure_tma_variant<V0, false>(&c.variant_ctas[12]);
     if (rc == PCC_OK) rc = configure_tma_variant<VQ>(&c.quad_ctas);
+    if (rc == PCC_OK) rc = configure_exact(&c.exact_ctas);
     if (rc == PCC_OK) rc = configure_one<V1, pcc::kLayoutPacked>(&c.variant_ctas[1]);
     if (rc == PCC_OK) rc = configure_one<V2, pcc::kLayoutPacked>(&c.variant_ctas[2]);
     if (rc == PCC_OK) rc = configure_one<V3, pcc::kLayoutPacked>(&c.variant_ctas[3]);
@@ -205,6 +229,7 @@ int device_config(const DeviceConfig **out, int device = -1) {
     c.syrk_ctas_per_sm = c.variant_ctas[0];
     for (int v = 0; v < kNumVariants; ++v)
       if (c.variant_ctas[v] < 1) return fail(PCC_ECUDA, "contraction variant %d cannot be resident on device %d", v, device);
+    if (c.exact_ctas < 1) return fail(PCC_ECUDA, "exact contraction cannot be resident on device %d", device);
     c.ready = true;
   }
   *out = &c;
@@ -291,12 +316,27 @@ int launch_tma_cfg(const double *u, int64_t n, int64_t l, int64_t ldu, uint64_t 
 }
 
 template <int LAYOUT>
+int launch_exact(const double *u, int64_t n, int64_t l, int64_t ldu, uint64_t tb, uint64_t te,
+                 const pcc::Epilogue &ep, cudaStream_t stream, const DeviceConfig *dc) {
+  using C = pcc::ExactCfg;
+  const uint64_t m_g = ceil_div((uint64_t)n, pcc::kTile);
+  const uint64_t units = (te - tb) * C::kSubPerTile;
+  const uint64_t resident = (uint64_t)dc->sm_count * (uint64_t)dc->exact_ctas;
+  const unsigned grid = (unsigned)(units < resident ? units : resident);
+  const int k_chunks = (int)ceil_div((uint64_t)l, (uint64_t)C::BK);
+  pcc::syrk_exact_kernel<LAYOUT><<<grid, C::kThreads, C::kSmemBytes, stream>>>(u, n, ldu, k_chunks, m_g, tb, te, ep);
+  PCC_CUDA(cudaGetLastError(), "syrk_exact_kernel launch");
+  return PCC_OK;
+}
+
+template <int LAYOUT>
 int launch_syrk(const double *u, int64_t n, int64_t l, int64_t ldu, uint64_t tb, uint64_t te,
                 const pcc::Epilogue &ep, cudaStream_t stream, int variant = 0) {
   if (te <= tb) return PCC_OK;
   const DeviceConfig *dc = nullptr;
   int rc = device_config(&dc);
   if (rc) return rc;
+  if (variant == PCC_VARIANT_EXACT) return launch_exact<LAYOUT>(u, n, l, ldu, tb, te, ep, stream, dc);
   const int sms = dc->sm_count;
   const int *vc = dc->variant_ctas;
   if (variant == 0) {
@@ -327,7 +367,8 @@ int launch_syrk(const double *u, int64_t n, int64_t l, int64_t ldu, uint64_t tb,
     case 13: return launch_tma_cfg<V0, pcc::kLayoutPacked, false, true>(u, n, l, ldu, tb, te, ep, stream, vc[13], sms);
     case 14:
       return launch_tma_cfg<V0, pcc::kLayoutPacked, false, false, false>(u, n, l, ldu, tb, te, ep, stream, vc[14], sms);
-    default: return fail(PCC_EINVAL, "unknown contraction variant %d (0..%d)", variant, kNumVariants - 1);
+    default:
+      return fail(PCC_EINVAL, "unknown contraction variant %d (0..%d, or PCC_VARIANT_EXACT)", variant, kNumVariants - 1);
   }
 }
 
@@ -503,8 +544,15 @@ int pcc_syrk_f64_variant(int32_t variant, const double *u, int64_t n, int64_t l,
   }
 }
 
-int pcc_compute_pass_f64(const double *u, int64_t n, int64_t l, int64_t ldu, int64_t t, uint64_t j_lo,
-                         uint64_t j_hi, double *out, void *stream) {
+int pcc_syrk_exact_f64(const double *u, int64_t n, int64_t l, int64_t ldu, uint64_t tile_begin, uint64_t tile_end,
+                       int32_t layout, double *out, int64_t ld_out, uint64_t out_base, int32_t ref_t,
+                       uint64_t ref_begin, uint64_t ref_end, void *stream) {
+  return pcc_syrk_f64_variant(PCC_VARIANT_EXACT, u, n, l, ldu, tile_begin, tile_end, layout, out, ld_out, out_base,
+                              ref_t, ref_begin, ref_end, stream);
+}
+
+static int compute_pass_impl(int32_t variant, const double *u, int64_t n, int64_t l, int64_t ldu, int64_t t,
+                             uint64_t j_lo, uint64_t j_hi, double *out, void *stream) {
   int rc = check_u(u, n, l, ldu);
   if (rc) return rc;
   if (t < 1) return fail(PCC_EINVAL, "tile size must be >= 1, got %lld", (long long)t);
@@ -527,7 +575,18 @@ int pcc_compute_pass_f64(const double *u, int64_t n, int64_t l, int64_t ldu, int
   const uint64_t m_g = ceil_div((uint64_t)n, pcc::kTile);
   const uint64_t Ya = y_a / pcc::kTile, Yb = (y_b - 1) / pcc::kTile;
   const uint64_t tb = pcc::row_prefix(m_g, Ya), te = pcc::row_prefix(m_g, Yb + 1);
-  return pcc_syrk_f64(u, n, l, ldu, tb, te, PCC_LAYOUT_TILES, out, 0, 0, (int32_t)t, j_lo, j_hi, stream);
+  return pcc_syrk_f64_variant(variant, u, n, l, ldu, tb, te, PCC_LAYOUT_TILES, out, 0, 0, (int32_t)t, j_lo, j_hi,
+                              stream);
+}
+
+int pcc_compute_pass_f64(const double *u, int64_t n, int64_t l, int64_t ldu, int64_t t, uint64_t j_lo,
+                         uint64_t j_hi, double *out, void *stream) {
+  return compute_pass_impl(0, u, n, l, ldu, t, j_lo, j_hi, out, stream);
+}
+
+int pcc_compute_pass_exact_f64(const double *u, int64_t n, int64_t l, int64_t ldu, int64_t t, uint64_t j_lo,
+                               uint64_t j_hi, double *out, void *stream) {
+  return compute_pass_impl(PCC_VARIANT_EXACT, u, n, l, ldu, t, j_lo, j_hi, out, stream);
 }
 
 int pcc_scatter_range_f64(double *packed, const double *values, uint64_t first_tile, uint64_t count, int64_t t,

@@ -244,7 +244,7 @@ def merge(reports: list[WorkerReport], geom: TileGeometry, zero_variance: frozen
 
 
 def _run_subprocess(dataset: Dataset, dataset_path: str, geom: TileGeometry, p: int, capacity: int,
-                    threads: int, devs: list[torch.device]) -> CorrelationResult:
+                    threads: int, devs: list[torch.device], exact: bool = False) -> CorrelationResult:
     """One GPU worker process per assignment, the reference's wire protocol
     (distributed.py:209-318): BLOCKS frames are scattered into one packed
     result as they arrive; a failing worker raises ``WorkerError`` with its
@@ -303,7 +303,7 @@ def _run_subprocess(dataset: Dataset, dataset_path: str, geom: TileGeometry, p: 
     try:
         for a in assignments:
             env = dict(os.environ, PAIRCORR_THREADS=str(threads),
-                       PCC_DEVICE=str(devs[a.worker_index % len(devs)].index),
+                       PCC_DEVICE=str(devs[a.worker_index % len(devs)].index), PCC_EXACT="1" if exact else "0",
                        PYTHONPATH=root + os.pathsep + os.environ.get("PYTHONPATH", ""))
             procs.append(subprocess.Popen([sys.executable, "-m", "paper_1605_01584_b200.worker"],
                                           stdin=subprocess.PIPE, stdout=subprocess.PIPE,
@@ -335,7 +335,7 @@ def _run_subprocess(dataset: Dataset, dataset_path: str, geom: TileGeometry, p: 
 
 
 def compute_shard(x_host, n: int, l: int, a: WorkerAssignment, device: torch.device,
-                  x_device: torch.Tensor | None = None) -> tuple[Shard, torch.Tensor]:
+                  x_device: torch.Tensor | None = None, exact: bool = False) -> tuple[Shard, torch.Tensor]:
     """Worker body: upload, normalise everything, contract ``a``'s tile range.
 
     Returns the shard and the device zero-variance flags; asynchronous on
@@ -348,14 +348,15 @@ def compute_shard(x_host, n: int, l: int, a: WorkerAssignment, device: torch.dev
         vals = torch.empty(max(hi - lo, 1), dtype=torch.float64, device=device)
         if a.stop > a.start:
             _lib.check(
-                _lib.lib().pcc_syrk_f64(ptr(u), n, l, u.shape[1], a.start, a.stop, _lib.LAYOUT_PACKED, ptr(vals), 0,
+                _lib.syrk_fn(exact)(ptr(u), n, l, u.shape[1], a.start, a.stop, _lib.LAYOUT_PACKED, ptr(vals), 0,
                                         lo, 0, 0, 0, stream_handle()),
                 f"worker {a.worker_index}",
             )
         return Shard(a.worker_index, device, a.start, a.stop, lo, vals), flags
 
 
-def stream_shard(x_host, n: int, l: int, a: WorkerAssignment, device: torch.device, host_out=None):
+def stream_shard(x_host, n: int, l: int, a: WorkerAssignment, device: torch.device, host_out=None,
+                 exact: bool = False):
     """Worker body with overlapped upload / contraction / download (stream.run_stream).
 
     Uploads and normalises only the rows the range touches (>= its first
@@ -366,7 +367,7 @@ def stream_shard(x_host, n: int, l: int, a: WorkerAssignment, device: torch.devi
     lo, hi = shard_span(n, a.start, a.stop)
     with torch.cuda.device(device):
         vals = torch.empty(max(hi - lo, 1), dtype=torch.float64, device=device)
-        _, flags, _ = run_stream(x_host, n, l, device, a.start, a.stop, vals, lo, host_out, lo)
+        _, flags, _ = run_stream(x_host, n, l, device, a.start, a.stop, vals, lo, host_out, lo, exact=exact)
     return Shard(a.worker_index, device, a.start, a.stop, lo, vals), flags
 
 
@@ -438,7 +439,8 @@ def exchange_normalize(x_host, n: int, l: int, rank: int, world: int, device: to
     return u, flags
 
 
-def compute_worker(dataset: Dataset, p: int, worker_index: int, device=None, out=None, group=None):
+def compute_worker(dataset: Dataset, p: int, worker_index: int, device=None, out=None, group=None,
+                   exact: bool = False):
     """Run worker ``worker_index`` of a ``p``-way split as a standalone call.
 
     The one-process-per-GPU form of ``run_workers`` (torchrun ranks): upload,
@@ -468,11 +470,11 @@ def compute_worker(dataset: Dataset, p: int, worker_index: int, device=None, out
         lo, hi = shard_span(n, a.start, a.stop)
         with torch.cuda.device(dev):
             vals = torch.empty(max(hi - lo, 1), dtype=torch.float64, device=dev)
-            run_stream(None, n, l, dev, a.start, a.stop, vals, lo, host, lo, resident=(u, flags))
+            run_stream(None, n, l, dev, a.start, a.stop, vals, lo, host, lo, resident=(u, flags), exact=exact)
         shard = Shard(a.worker_index, dev, a.start, a.stop, lo, vals)
         flags = flags[:n]
     else:
-        shard, flags = stream_shard(dataset.values, n, l, a, dev, host)
+        shard, flags = stream_shard(dataset.values, n, l, a, dev, host, exact=exact)
     shard.zero_variance = frozenset(np.flatnonzero(flags.cpu().numpy()).tolist())
     return shard
 
@@ -487,6 +489,7 @@ def run_workers(
     devices=None,
     gather: bool = True,
     out=None,
+    exact: bool = False,
 ):
     """Partition the work across ``p`` workers on ``devices`` (distributed.py:117-151).
 
@@ -498,6 +501,7 @@ def run_workers(
     worker process per range of the caller's t x t tiles, speaking the
     reference's framed protocol (``worker.py``), gathered on the host.  A
     failing worker raises ``WorkerError`` with its index and unfinished range.
+    ``exact``: the bit-exact dot8 contraction (see ``allpairs``).
     """
     if backend not in BACKENDS:
         raise ValueError(f"unknown backend {backend!r}, expected one of {BACKENDS}")
@@ -518,12 +522,12 @@ def run_workers(
         geom = geom if geom is not None else TileGeometry(n=dataset.n)
         capacity = default_capacity(geom.t) if capacity is None else capacity
         if dataset_path is not None:
-            return _run_subprocess(dataset, dataset_path, geom, p, capacity, threads, devs)
+            return _run_subprocess(dataset, dataset_path, geom, p, capacity, threads, devs, exact)
         with tempfile.NamedTemporaryFile(suffix=".lpcc", delete=False) as tmp:
             tmp_path = tmp.name
         try:
             save_dataset(tmp_path, dataset)
-            return _run_subprocess(dataset, tmp_path, geom, p, capacity, threads, devs)
+            return _run_subprocess(dataset, tmp_path, geom, p, capacity, threads, devs, exact)
         finally:
             os.unlink(tmp_path)
     n, l = dataset.n, dataset.l
@@ -535,7 +539,7 @@ def run_workers(
     def run_one(a: WorkerAssignment) -> None:
         dev = devs[a.worker_index % len(devs)]
         try:
-            shards[a.worker_index], flags[a.worker_index] = compute_shard(dataset.values, n, l, a, dev)
+            shards[a.worker_index], flags[a.worker_index] = compute_shard(dataset.values, n, l, a, dev, exact=exact)
             with torch.cuda.device(dev):
                 torch.cuda.current_stream().synchronize()
         except BaseException as exc:  # noqa: BLE001 - re-raised as WorkerError below

@@ -56,7 +56,7 @@ def _host_out(out, total: int) -> torch.Tensor:
 
 
 def _allpairs_one_device(dataset: Dataset, device: torch.device, keep_on_device: bool, out, chunk_rows: int,
-                         output: str):
+                         output: str, exact: bool = False):
     n, l = dataset.n, dataset.l
     L = _lib.lib()
     with torch.cuda.device(device):
@@ -66,7 +66,7 @@ def _allpairs_one_device(dataset: Dataset, device: torch.device, keep_on_device:
             u, flags = normalize_device(x)
             T = int(L.pcc_gpu_tile_count(n))
             dense = torch.empty((n, n), dtype=torch.float64, device=device)
-            _lib.check(L.pcc_syrk_f64(ptr(u), n, l, u.shape[1], 0, T, _lib.LAYOUT_DENSE, ptr(dense), n, 0, 0, 0, 0,
+            _lib.check(_lib.syrk_fn(exact)(ptr(u), n, l, u.shape[1], 0, T, _lib.LAYOUT_DENSE, ptr(dense), n, 0, 0, 0, 0,
                                       stream_handle(compute)), "allpairs(dense)")
             zv = frozenset(np.flatnonzero(flags.cpu().numpy()).tolist())
             return (dense if keep_on_device else dense.cpu().numpy()), zv
@@ -75,7 +75,8 @@ def _allpairs_one_device(dataset: Dataset, device: torch.device, keep_on_device:
         T = int(L.pcc_gpu_tile_count(n))
         packed = torch.empty(total, dtype=torch.float64, device=device)
         host = None if keep_on_device else _host_out(out, total)
-        _, flags, _ = run_stream(dataset.values, n, l, device, 0, T, packed, 0, host, 0, chunk_rows=chunk_rows)
+        _, flags, _ = run_stream(dataset.values, n, l, device, 0, T, packed, 0, host, 0, chunk_rows=chunk_rows,
+                                 exact=exact)
         zv = frozenset(np.flatnonzero(flags.cpu().numpy()).tolist())
         if keep_on_device:
             return packed, zv
@@ -96,6 +97,7 @@ def allpairs(
     keep_on_device: bool = False,
     out=None,
     chunk_rows: int = 8,
+    exact: bool = False,
 ):
     """All-pairs Pearson correlation of ``dataset`` on B200 GPUs (engine.py:23-56).
 
@@ -112,7 +114,12 @@ def allpairs(
     * ``out``: caller-owned host float64 buffer for the packed result (pinned
       memory makes the device-to-host copies asynchronous);
     * ``chunk_rows``: upload granularity in 128-row GPU tile rows; each
-      uploaded chunk releases one contraction pass (``stream.plan_stream``).
+      uploaded chunk releases one contraction pass (``stream.plan_stream``);
+    * ``exact``: compute every coefficient in the reference's own arithmetic
+      (``dot8``: separately rounded products, eight lane sums, fixed tree) on
+      the FP64 CUDA cores -- the packed result is bit-identical to
+      ``paircorr.allpairs`` -- instead of on the FP64 tensor cores (within
+      1e-12, about twice as fast).
     """
     if not isinstance(dataset, Dataset):
         from .fileio import load_dataset
@@ -131,11 +138,12 @@ def allpairs(
         raise ValueError(f"output must be 'packed' or 'dense', got {output!r}")
     devs = resolve_devices(devices)
     if (workers > 1 or len(devs) > 1) and output == "packed" and not keep_on_device:
-        return run_workers(dataset, geom, max(workers, len(devs)), backend="cuda", devices=devs, out=out)
+        return run_workers(dataset, geom, max(workers, len(devs)), backend="cuda", devices=devs, out=out,
+                           exact=exact)
     if workers > 1 or len(devs) > 1:
         raise ValueError("multi-worker runs support output='packed' gathered to host "
                          "(use run_workers(..., gather=False) for device-resident shards)")
-    res, zv = _allpairs_one_device(dataset, devs[0], keep_on_device, out, chunk_rows, output)
+    res, zv = _allpairs_one_device(dataset, devs[0], keep_on_device, out, chunk_rows, output, exact)
     if output == "dense":
         return res, zv
     return CorrelationResult(n=dataset.n, packed=res, zero_variance=zv)

@@ -172,7 +172,8 @@ def plan_stream(n: int, tile_begin: int, tile_end: int, wave: int, chunk_rows: i
 
 def run_stream(x, n: int, l: int, device: torch.device, tile_begin: int, tile_end: int,
                out_dev: torch.Tensor, out_base: int, host_out: torch.Tensor | None,
-               host_base: int = 0, chunk_rows: int = 8, trace: list | None = None, resident=None):
+               host_base: int = 0, chunk_rows: int = 8, trace: list | None = None, resident=None,
+               exact: bool = False):
     """Execute GPU tiles ``[tile_begin, tile_end)`` with overlapped upload,
     normalisation, contraction and download.
 
@@ -185,6 +186,7 @@ def run_stream(x, n: int, l: int, device: torch.device, tile_begin: int, tile_en
     ``resident``: ``(u, flags)`` already normalised on ``device`` (e.g. after
     the multi-GPU row exchange); ``x`` is then ignored and only the
     contraction passes and downloads run (top-down, no upload phase).
+    ``exact``: contract with the bit-exact dot8 kernel (``pcc_syrk_exact_f64``).
     Returns ``(u, flags, x_device)`` after the host has synchronised
     (``x_device`` is None with ``resident``).
     """
@@ -196,6 +198,7 @@ def run_stream(x, n: int, l: int, device: torch.device, tile_begin: int, tile_en
             trace.append((label, ev))
 
     L = _lib.lib()
+    syrk = _lib.syrk_fn(exact)
     with torch.cuda.device(device):
         info = _lib.device_info(device.index)
         wave = info.sm_count * info.syrk_ctas_per_sm
@@ -281,7 +284,7 @@ def run_stream(x, n: int, l: int, device: torch.device, tile_begin: int, tile_en
                 ws = workers[k % len(workers)] if phase == 1 else workers[0]
                 ws.wait_event(normed)
                 mark(f"  start [{p_lo},{p_hi})", ws)
-                _lib.check(L.pcc_syrk_f64(ptr(u), n, l, ldu, p_lo, p_hi, _lib.LAYOUT_PACKED, ptr(out_dev), 0,
+                _lib.check(syrk(ptr(u), n, l, ldu, p_lo, p_hi, _lib.LAYOUT_PACKED, ptr(out_dev), 0,
                                           out_base, 0, 0, 0, stream_handle(ws)), "syrk")
                 done = torch.cuda.Event()
                 done.record(ws)

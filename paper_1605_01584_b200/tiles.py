@@ -148,8 +148,9 @@ def _check_range(geom: TileGeometry, j_start: int, j_end: int) -> None:
 
 
 def compute_pass_device(u: NormalizedDataset, geom: TileGeometry, j_start: int, j_end: int,
-                        out: torch.Tensor, stream: torch.cuda.Stream | None = None) -> None:
-    """Fill the device buffer ``out`` with the pass layout of tiles ``[j_start, j_end)``."""
+                        out: torch.Tensor, stream: torch.cuda.Stream | None = None, exact: bool = False) -> None:
+    """Fill the device buffer ``out`` with the pass layout of tiles ``[j_start, j_end)``
+    (``exact``: bit-identical to the reference's ``compute_tile_range``)."""
     _check_range(geom, j_start, j_end)
     if geom.n != u.n:
         raise ValueError(f"geometry is for n={geom.n} but data has n={u.n}")
@@ -160,8 +161,8 @@ def compute_pass_device(u: NormalizedDataset, geom: TileGeometry, j_start: int, 
         return
     with torch.cuda.device(u.device):
         _lib.check(
-            _lib.lib().pcc_compute_pass_f64(ptr(u.u_device), u.n, u.l, u.ldu, geom.t, j_start, j_end,
-                                            ptr(out), stream_handle(stream)),
+            (_lib.lib().pcc_compute_pass_exact_f64 if exact else _lib.lib().pcc_compute_pass_f64)(
+                ptr(u.u_device), u.n, u.l, u.ldu, geom.t, j_start, j_end, ptr(out), stream_handle(stream)),
             "compute_pass",
         )
 
@@ -174,6 +175,8 @@ def compute_pass(
     threads: int = 1,
     out=None,
     pool=None,
+    *,
+    exact: bool = False,
 ) -> BlockList:
     """Compute tiles ``[j_start, j_end)`` on the GPU into a flat pass buffer (tiles.py:133-199).
 
@@ -181,6 +184,8 @@ def compute_pass(
     values) is filled in place, else a fresh one is returned; ``threads`` and
     ``pool`` are accepted for compatibility and change nothing.  Returns the
     reference's ``BlockList`` of per-tile views with ``flat`` set.
+    ``exact``: the bit-exact dot8 contraction (the reference's pass buffer,
+    bit for bit).
     """
     _check_range(geom, j_start, j_end)
     count = j_end - j_start
@@ -193,7 +198,7 @@ def compute_pass(
     if count == 0:
         return BlockList()
     dev = torch.empty(need, dtype=torch.float64, device=u.device)
-    compute_pass_device(u, geom, j_start, j_end, dev)
+    compute_pass_device(u, geom, j_start, j_end, dev, exact=exact)
     if isinstance(out, torch.Tensor):
         out[:need].copy_(dev)
         host = out

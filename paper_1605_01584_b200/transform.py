@@ -198,9 +198,9 @@ class _Rows:
 
 def pcc_normalized(u_i, u_j) -> float:
     """Correlation of two already-normalised rows (transform.py:134-144): their
-    dot product, computed by the engine's own contraction (K2 on a two-row U)
-    -- within 1e-12 of the reference's fixed-order ``dot8``, like every engine
-    coefficient.  A zero-variance (all-zero) row gives 0.0."""
+    fixed-order ``dot8``, computed by the engine's bit-exact contraction
+    (``pcc_syrk_exact_f64`` on a two-row U) -- bit-identical to the
+    reference.  A zero-variance (all-zero) row gives 0.0."""
     a, b = _as_row(u_i), _as_row(u_j)
     if a.shape[0] != b.shape[0]:
         raise ValueError(f"length mismatch: {a.shape[0]} vs {b.shape[0]}")
@@ -215,8 +215,8 @@ def pcc_normalized(u_i, u_j) -> float:
     u[0, :l] = torch.from_numpy(a).to(dev)
     u[1, :l] = torch.from_numpy(b).to(dev)
     out = torch.empty(3, dtype=torch.float64, device=dev)
-    _lib.check(L.pcc_syrk_f64(ptr(u), 2, l, ldu, 0, 1, _lib.LAYOUT_PACKED, ptr(out), 0, 0, 0, 0, 0, stream_handle()),
-               "pcc_normalized")
+    _lib.check(L.pcc_syrk_exact_f64(ptr(u), 2, l, ldu, 0, 1, _lib.LAYOUT_PACKED, ptr(out), 0, 0, 0, 0, 0,
+                                    stream_handle()), "pcc_normalized")
     return float(out[1].item())
 
 

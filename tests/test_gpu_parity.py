@@ -568,9 +568,9 @@ def test_syrk_launch_count_matches_tail_rule():
 
 
 def test_reference_pair_helpers_match_reference_outputs():
-    """pcc_naive (GPU definition kernel) bit-identical to the reference's
-    pcc_naive; pcc_normalized (the engine's contraction on two rows) within
-    1e-12 of the reference's dot8 (tests/golden/helpers.json)."""
+    """pcc_naive (GPU definition kernel) and pcc_normalized (the bit-exact
+    contraction on two rows) bit-identical to the reference's pcc_naive and
+    pcc_normalized (tests/golden/helpers.json)."""
     import json
 
     from conftest import GOLDEN
@@ -581,7 +581,7 @@ def test_reference_pair_helpers_match_reference_outputs():
         b = np.array([float.fromhex(v) for v in case["b"]])
         assert float(pc.pcc_naive(a, b)).hex() == case["naive"]
         u, _ = oracle.normalize(np.stack([a, b]))
-        assert abs(pc.pcc_normalized(u[0], u[1]) - float.fromhex(case["normalized"])) <= 1e-12
+        assert float(pc.pcc_normalized(u[0], u[1])).hex() == case["normalized"]
     with pytest.raises(ValueError):
         pc.pcc_naive([1.0, 2.0], [1.0, 2.0, 3.0])
     with pytest.raises(ValueError):
@@ -597,3 +597,70 @@ def test_allpairs_naive_bit_identical_to_reference_golden(golden_small):
         r = pc.allpairs_naive(pc.Dataset(values=x))
         assert np.array_equal(r.packed, case["naive"]), name
         assert r.zero_variance == frozenset(np.flatnonzero(oracle.constant_row_flags(x)).tolist())
+
+
+# ---------------------------------------------------------------------------
+# Exact mode: the dot8 contraction on the FP64 CUDA cores, bit-identical to
+# the reference's engine (csrc/exact.cuh).
+
+def test_exact_allpairs_bit_identical_to_reference_golden(golden_small):
+    assert len(golden_small) >= 30
+    for name, case in golden_small.items():
+        r = pc.allpairs(pc.Dataset(values=case["x"]), exact=True)
+        assert np.array_equal(r.packed.view(np.uint64), case["packed"].view(np.uint64)), name
+        assert r.zero_variance == frozenset(np.flatnonzero(case["zv"]).tolist()), name
+
+
+def test_exact_pass_buffers_bit_identical_to_reference(golden_small):
+    """compute_pass(..., exact=True) reproduces the reference's t = 3 pass
+    buffer (zeros outside the triangle included), bit for bit."""
+    for name, case in golden_small.items():
+        nd = pc.normalize(pc.Dataset(values=case["x"]))
+        geom = pc.TileGeometry(n=nd.n, t=3)
+        blocks = pc.compute_pass(nd, geom, 0, geom.total_tiles, exact=True)
+        flat = blocks.flat if len(blocks) else np.empty(0)
+        assert np.array_equal(np.asarray(flat).view(np.uint64), case["pass_t3"].view(np.uint64)), name
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c3"])
+def test_exact_full_config_matches_reference_sha256(cfg):
+    """The whole packed result of c1 / c3 hashes to the reference's own
+    (tests/golden/config_digests.json, made by running paircorr.allpairs)."""
+    import hashlib
+    import json
+
+    from conftest import GOLDEN
+
+    from paper_1605_01584_b200.workloads import make_config
+
+    g = json.loads((GOLDEN / "config_digests.json").read_text())[cfg]
+    x = make_config(cfg)
+    r = pc.allpairs(pc.Dataset(values=x), exact=True)
+    assert hashlib.sha256(np.ascontiguousarray(r.packed).tobytes()).hexdigest() == g["packed_sha256"]
+    assert sorted(r.zero_variance) == g["zero_variance"]
+
+
+@pytest.mark.parametrize("n,l", [(1, 2), (2, 3), (127, 5), (128, 8), (129, 9), (255, 31), (257, 33), (300, 77),
+                                 (130, 1531), (520, 64)])
+def test_exact_ragged_shapes_bit_identical_to_oracle(n, l, rng):
+    x = random_values(rng, n, l, special_rows=n > 3)
+    ref, zv = oracle.allpairs(x, t=4)
+    r = pc.allpairs(pc.Dataset(values=x), exact=True)
+    assert np.array_equal(r.packed.view(np.uint64), ref.view(np.uint64))
+    dense, _ = pc.allpairs(pc.Dataset(values=x), exact=True, output="dense")
+    iu = np.triu_indices(n)
+    assert np.array_equal(dense[iu], ref) and np.array_equal(dense, dense.T)
+
+
+def test_exact_schedule_invariance(rng):
+    """Exact results do not depend on passes, workers or the streamed plan."""
+    x = random_values(rng, 700, 45, special_rows=True)
+    ref, _ = oracle.allpairs(x, t=4)
+    d = pc.Dataset(values=x)
+    for kw in ({"workers": 3}, {"chunk_rows": 1}, {"workers": 2, "devices": 1}):
+        assert np.array_equal(pc.allpairs(d, exact=True, **kw).packed, ref), kw
+    nd = pc.normalize(d)
+    geom = pc.TileGeometry(n=700, t=4)
+    asm = pc.ResultAssembler(geom, nd.zero_variance)
+    pc.run_pipeline(nd, geom, pc.plan_passes(0, geom.total_tiles, 5000), asm, exact=True)
+    assert np.array_equal(asm.result.packed, ref)
