@@ -7,12 +7,12 @@
 // tensor path), so it is the bit-exact mode, not the fast one.
 //
 // Work unit = one 32 x 64 sub-block of a 128 x 128 GPU tile (8 per tile,
-// persistent grid-stride over [tile_begin, tile_end) x 8).  256 threads:
-// thread t is reference lane j = t & 7 for an 8 x 8 cell block, so each
-// thread carries 64 independent lane accumulators (the dependent add chains
-// overlap one another) and the 8 lanes of a cell sit in 8 consecutive
-// threads.  U's rows stream through a 4-stage cp.async ring of 32-column
-// K chunks (pitch 40 doubles; rows of odd 8-row blocks shifted by 8 doubles,
+// persistent grid-stride over [tile_begin, tile_end) x 8).  512 threads (16
+// warps: the multiply -> add dependency needs them to fill the FP64 pipe):
+// thread t is reference lane j = t & 7 for a 4 x 8 cell block, so each
+// thread carries 32 independent lane accumulators and the 8 lanes of a cell
+// sit in 8 consecutive threads.  U's rows stream through a 3-stage cp.async ring of 64-column
+// K chunks (pitch 72 doubles; rows of odd 8-row blocks shifted by 8 doubles,
 // so the four 8-lane groups of a warp reading four different row blocks
 // pair up on opposite bank halves: the minimum two wavefronts per 64-bit
 // load).  Zero K padding only adds +0.0 to lane sums
@@ -25,12 +25,13 @@
 namespace pcc {
 
 struct ExactCfg {
-  static constexpr int kThreads = 256;
+  static constexpr int RT = 4;        // cell rows per thread (x 8 columns)
+  static constexpr int kThreads = 256 * 8 / RT;
   static constexpr int BM = 32;      // sub-block rows (y)
   static constexpr int BN = 64;      // sub-block columns (x)
-  static constexpr int BK = 32;      // K chunk (4 steps of each lane)
-  static constexpr int kPitch = 40;  // doubles per staged row
-  static constexpr int STAGES = 4;
+  static constexpr int BK = 64;           // K chunk (8 steps of each lane)
+  static constexpr int kPitch = BK + 8;   // doubles per staged row
+  static constexpr int STAGES = 3;
   static constexpr int kStageDoubles = (BM + BN) * kPitch;
   static constexpr int kSmemBytes = STAGES * kStageDoubles * (int)sizeof(double);
   static constexpr int kSubPerTile = (kTile / BM) * (kTile / BN);  // 8
@@ -47,9 +48,9 @@ syrk_exact_kernel(const double *__restrict__ u, int64_t n, int64_t ldu, int k_ch
   extern __shared__ __align__(128) double smem[];
   const int tid = threadIdx.x;
   const int lane8 = tid & 7;
-  const int grp = tid >> 3;         // 0..31: which 8 x 8 cell block
-  const int bi = grp >> 3;          // 0..3  -> rows bi*8 .. +8 of the sub-block
-  const int bj = grp & 7;           // 0..7  -> cols bj*8 .. +8
+  const int grp = tid >> 3;         // which RT x 8 cell block
+  const int bi = grp >> 3;          // rows bi*RT .. +RT of the sub-block
+  const int bj = grp & 7;           // cols bj*8 .. +8
   const uint64_t un = (uint64_t)n;
   const uint64_t units = (tile_end - tile_begin) * C::kSubPerTile;
 
@@ -68,15 +69,20 @@ syrk_exact_kernel(const double *__restrict__ u, int64_t n, int64_t ldu, int k_ch
       const int64_t k0 = (int64_t)kc * C::BK;
       // (BM + BN) rows x 32 doubles = 8 x 16-byte pieces per row
       for (int i = tid; i < (C::BM + C::BN) * (C::BK / 2); i += C::kThreads) {
-        const int r = i >> 4, piece = i & 15;
+        const int r = i / (C::BK / 2), piece = i % (C::BK / 2);
         const uint64_t grow = r < C::BM ? row0 + r : col0 + (r - C::BM);
-        cp_async_16(smem_u32(sa + row_off(r) + piece * 2), u + grow * (uint64_t)ldu + k0 + piece * 2);
+        double *dst = sa + row_off(r) + piece * 2;
+        if (k0 + piece * 2 < ldu) {
+          cp_async_16(smem_u32(dst), u + grow * (uint64_t)ldu + k0 + piece * 2);
+        } else {  // past the row's padded width (ldu is a multiple of 32, BK of 64): zeros
+          *reinterpret_cast<double2 *>(dst) = make_double2(0.0, 0.0);
+        }
       }
     };
 
-    double acc[8][8];
+    double acc[C::RT][8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
+    for (int i = 0; i < C::RT; ++i)
 #pragma unroll
       for (int c = 0; c < 8; ++c) acc[i][c] = 0.0;
 
@@ -93,17 +99,17 @@ syrk_exact_kernel(const double *__restrict__ u, int64_t n, int64_t ldu, int k_ch
         if (nxt < k_chunks) load_chunk(nxt % C::STAGES, nxt);
         cp_async_commit();
       }
-      const double *sa = smem + (kc % C::STAGES) * C::kStageDoubles + row_off(bi * 8) + lane8;
+      const double *sa = smem + (kc % C::STAGES) * C::kStageDoubles + row_off(bi * C::RT) + lane8;
       const double *sb = smem + (kc % C::STAGES) * C::kStageDoubles + row_off(C::BM + bj * 8) + lane8;
 #pragma unroll
-      for (int m = 0; m < C::BK / 8; ++m) {  // this lane's k = kc*32 + m*8 + lane8, increasing
-        double a[8], b[8];
+      for (int m = 0; m < C::BK / 8; ++m) {  // this lane's k = kc*BK + m*8 + lane8, increasing
+        double a[C::RT], b[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) a[i] = sa[i * C::kPitch + m * 8];
+        for (int i = 0; i < C::RT; ++i) a[i] = sa[i * C::kPitch + m * 8];
 #pragma unroll
         for (int c = 0; c < 8; ++c) b[c] = sb[c * C::kPitch + m * 8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
+        for (int i = 0; i < C::RT; ++i) {
           // all eight products of the row first: each add waits on a
           // multiply issued eight FP64 instructions earlier
           double p[8];
@@ -120,7 +126,7 @@ syrk_exact_kernel(const double *__restrict__ u, int64_t n, int64_t ldu, int k_ch
     // the fixed tree across the 8 lanes of each cell, then lane j stores
     // column j of the thread group's 8 x 8 block (8 consecutive cells per row)
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < C::RT; ++i) {
       double mine = 0.0;
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
@@ -130,7 +136,7 @@ syrk_exact_kernel(const double *__restrict__ u, int64_t n, int64_t ldu, int k_ch
         v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, 4));
         if (c == lane8) mine = v;
       }
-      const uint64_t y = row0 + bi * 8 + i;
+      const uint64_t y = row0 + bi * C::RT + i;
       const uint64_t x = col0 + bj * 8 + lane8;
       if (y < un && x >= y && x < un) {
         const uint64_t prb = (LAYOUT == kLayoutPacked) ? row_prefix(un, y) - y - ep.out_base : 0;
