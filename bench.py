@@ -57,6 +57,7 @@ def parse_args(argv=None):
     p.add_argument("--config", default=DEFAULT_CONFIG, choices=("c1", "c2", "c3", "c4", "c5"))
     p.add_argument("--e2e-steps", type=int, default=None, help="timed end-to-end API calls (default: max(steps, 5)), median reported")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-exact", action="store_true", help="skip the bit-exact (dot8) mode measurement")
     p.add_argument("--cpu-fraction", type=float, default=None,
                    help="fraction of the reference t=4 tile range in the CPU sample")
     return p.parse_args(argv)
@@ -333,6 +334,48 @@ def run_b200(args, rank: int, world: int, local_rank: int) -> None:
         "algorithmic_flops_per_launch": flops_launch,
     }
 
+    # ---- bit-exact mode (allpairs(exact=True)): K1 + the dot8 contraction on the
+    # FP64 CUDA cores, same shard, device-timed like the step above
+    exact_mode = None
+    if not args.no_exact and te > tb:
+        shard_x = torch.empty_like(shard)
+
+        def step_exact(ev=None):
+            u, _ = normalize_device(x)
+            if ev is not None:
+                ev[0].record(stream)
+            _lib.check(L.pcc_syrk_exact_f64(ptr(u), n, l, u.shape[1], tb, te, _lib.LAYOUT_PACKED, ptr(shard_x), 0,
+                                            span_lo, 0, 0, 0, s), "syrk_exact")
+            if ev is not None:
+                ev[1].record(stream)
+
+        ex_steps = max(2, min(args.steps, 3))
+        step_exact()
+        torch.cuda.synchronize()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(ex_steps)]
+        barrier()
+        torch.cuda.synchronize()
+        t0.record(stream)
+        for i in range(ex_steps):
+            step_exact(evs[i])
+        t1.record(stream)
+        torch.cuda.synchronize()
+        ex_ms = max_over_ranks(t0.elapsed_time(t1) / ex_steps)
+        ex_syrk_ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in evs) / ex_steps)
+        ex_ach = flops_launch / (ex_syrk_ms * 1e-3) / 1e12
+        exact_mode = {
+            "what": "allpairs(exact=True): every coefficient bit-identical to the reference's dot8 "
+                    "(tests/test_gpu_parity.py::test_exact_*; full c1/c3 results hash to the reference's)",
+            "value": total_pairs / (ex_ms * 1e-3), "unit": "pairs/s", "ms_per_step": ex_ms, "steps": ex_steps,
+            "roofline": {"bound": "fp64_alu", "achieved": ex_ach, "peak": peak / 2, "unit": "TFLOP/s",
+                         "frac": ex_ach / (peak / 2),
+                         "kernel": "syrk_exact_kernel<packed> (DMUL + DADD per term, FP64 CUDA cores)",
+                         "peak_source": "DMUL/DADD issue at the DFMA rate = half the DMMA probe in FLOP/s "
+                                        "(tools/fp64_alu.cu)"},
+        }
+        torch.cuda.synchronize()
+        del shard_x
+
     # ---- end to end through the public API (pinned X upload + packed download inside)
     e2e_steps = args.e2e_steps if args.e2e_steps is not None else max(args.steps, 5)
     host_out = torch.empty(total_pairs if world == 1 else max(1, span_hi - span_lo), dtype=torch.float64,
@@ -415,6 +458,7 @@ def run_b200(args, rank: int, world: int, local_rank: int) -> None:
             "e2e": {"value": total_pairs / e2e_s, "unit": "pairs/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3, "steps": e2e_steps},
             "gpu_launches": launches,
+            "exact_mode": exact_mode,
             "clocks": clock,
         }
         print(json.dumps(line), flush=True)

@@ -250,16 +250,19 @@ def run_stream(x, n: int, l: int, device: torch.device, tile_begin: int, tile_en
                 mark(f"download {8 * (b - a) / 1e6:.0f} MB{label}", copy_out)
             downloaded.append((r_lo, r_hi))
 
+        dl_next = [0]  # next pass_done entry to download (a list, not a function
+        #               attribute: a self-referencing closure would keep this call's
+        #               device buffers alive until the cyclic GC runs)
+
         def download(upto: int) -> None:
             # in-order waits: a copy runs only after its pass and every earlier pass
-            while download.k < upto:
-                ev, r_lo, r_hi = pass_done[download.k]
-                download.k += 1
+            while dl_next[0] < upto:
+                ev, r_lo, r_hi = pass_done[dl_next[0]]
+                dl_next[0] += 1
                 copy_out.wait_event(ev)
                 if r_hi > r_lo:
                     copy_rows(r_lo, r_hi, "")
 
-        download.k = 0
         k = 0
         for c, (lo, hi) in enumerate(plan.chunks):
             # upload (pageable sources block here while the GPU runs earlier passes)
