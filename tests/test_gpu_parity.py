@@ -664,3 +664,14 @@ def test_exact_schedule_invariance(rng):
     asm = pc.ResultAssembler(geom, nd.zero_variance)
     pc.run_pipeline(nd, geom, pc.plan_passes(0, geom.total_tiles, 5000), asm, exact=True)
     assert np.array_equal(asm.result.packed, ref)
+
+
+def test_exact_subprocess_workers_and_device_output(rng, monkeypatch):
+    """PCC_EXACT workers over the reference protocol and keep_on_device: still
+    the reference's bits."""
+    x = random_values(rng, 260, 21, special_rows=True)
+    ref, _ = oracle.allpairs(x, t=4)
+    r = pc.run_workers(pc.Dataset(values=x), pc.TileGeometry(n=260, t=4), 2, backend="subprocess", exact=True)
+    assert np.array_equal(r.packed, ref)
+    rd = pc.allpairs(pc.Dataset(values=x), exact=True, keep_on_device=True)
+    assert np.array_equal(rd.packed.cpu().numpy(), ref)
