@@ -7,7 +7,7 @@
 // tensor path), so it is the bit-exact mode, not the fast one.
 //
 // Work unit = one 32 x 64 sub-block of a 128 x 128 GPU tile (8 per tile,
-// persistent grid-stride over [tile_begin, tile_end) x 8).  512 threads (16
+// persistent grid-stride over the range's tiles in the grouped order x 8).  512 threads (16
 // warps: the multiply -> add dependency needs them to fill the FP64 pipe):
 // thread t is reference lane j = t & 7 for a 4 x 8 cell block, so each
 // thread carries 32 independent lane accumulators and the 8 lanes of a cell
@@ -43,7 +43,7 @@ __device__ __forceinline__ int row_off(int r) { return r * ExactCfg::kPitch + ((
 template <int LAYOUT>
 __global__ void __launch_bounds__(ExactCfg::kThreads, 1)
 syrk_exact_kernel(const double *__restrict__ u, int64_t n, int64_t ldu, int k_chunks, uint64_t m_g,
-                  uint64_t tile_begin, uint64_t tile_end, Epilogue ep) {
+                  TileOrder order, Epilogue ep) {
   using C = ExactCfg;
   extern __shared__ __align__(128) double smem[];
   const int tid = threadIdx.x;
@@ -52,13 +52,14 @@ syrk_exact_kernel(const double *__restrict__ u, int64_t n, int64_t ldu, int k_ch
   const int bi = grp >> 3;          // rows bi*RT .. +RT of the sub-block
   const int bj = grp & 7;           // cols bj*8 .. +8
   const uint64_t un = (uint64_t)n;
-  const uint64_t units = (tile_end - tile_begin) * C::kSubPerTile;
+  const uint64_t units = order.total * C::kSubPerTile;
 
   for (uint64_t w = blockIdx.x; w < units; w += gridDim.x) {
-    const uint64_t J = tile_begin + w / C::kSubPerTile;
+    // tiles in the grouped L2-locality order (as the tensor path), the 8
+    // sub-blocks of a tile on consecutive units
     const int sub = (int)(w % C::kSubPerTile);
-    const uint64_t Y = tile_row(m_g, J);
-    const uint64_t X = J + Y - row_prefix(m_g, Y);
+    uint64_t Y, X;
+    tile_at(order, m_g, w / C::kSubPerTile, Y, X);
     const uint64_t row0 = Y * kTile + (uint64_t)(sub >> 1) * C::BM;
     const uint64_t col0 = X * kTile + (uint64_t)(sub & 1) * C::BN;
     // nothing of the triangle / of [0, n) in this sub-block: skip it

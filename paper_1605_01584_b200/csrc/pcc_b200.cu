@@ -324,7 +324,10 @@ int launch_exact(const double *u, int64_t n, int64_t l, int64_t ldu, uint64_t tb
   const uint64_t resident = (uint64_t)dc->sm_count * (uint64_t)dc->exact_ctas;
   const unsigned grid = (unsigned)(units < resident ? units : resident);
   const int k_chunks = (int)ceil_div((uint64_t)l, (uint64_t)C::BK);
-  pcc::syrk_exact_kernel<LAYOUT><<<grid, C::kThreads, C::kSmemBytes, stream>>>(u, n, ldu, k_chunks, m_g, tb, te, ep);
+  uint32_t group = 1;  // ~sqrt(tiles in flight): a wave of units covers grid / 8 tiles
+  while ((uint64_t)(group + 1) * (group + 1) * C::kSubPerTile <= grid) ++group;
+  const pcc::TileOrder order = pcc::make_tile_order(m_g, tb, te, group);
+  pcc::syrk_exact_kernel<LAYOUT><<<grid, C::kThreads, C::kSmemBytes, stream>>>(u, n, ldu, k_chunks, m_g, order, ep);
   PCC_CUDA(cudaGetLastError(), "syrk_exact_kernel launch");
   return PCC_OK;
 }
