@@ -74,7 +74,9 @@ syrk_exact_kernel(const double *__restrict__ u, int64_t n, int64_t ldu, int k_ch
         const uint64_t grow = r < C::BM ? row0 + r : col0 + (r - C::BM);
         double *dst = sa + row_off(r) + piece * 2;
         if (k0 + piece * 2 < ldu) {
+#ifndef PCC_EXACT_NOLOAD  // tools/exact_bench.cu: math-only timing (stale operands)
           cp_async_16(smem_u32(dst), u + grow * (uint64_t)ldu + k0 + piece * 2);
+#endif
         } else {  // past the row's padded width (ldu is a multiple of 32, BK of 64): zeros
           *reinterpret_cast<double2 *>(dst) = make_double2(0.0, 0.0);
         }
