@@ -675,3 +675,22 @@ def test_exact_subprocess_workers_and_device_output(rng, monkeypatch):
     assert np.array_equal(r.packed, ref)
     rd = pc.allpairs(pc.Dataset(values=x), exact=True, keep_on_device=True)
     assert np.array_equal(rd.packed.cpu().numpy(), ref)
+
+
+@given(st.integers(1, 400), st.integers(2, 160), st.integers(0, 2**32 - 1), st.sampled_from(["normal", "lognormal", "ints"]))
+@settings(max_examples=40, deadline=None)
+def test_allpairs_property_vs_oracle(n, l, seed, dist):
+    """Random shapes and value distributions (incl. small integers: ties,
+    constant rows, exact cancellations): the tensor path within 1e-12 of the
+    reference order, the exact mode bit-identical, the same zero-variance set."""
+    r = np.random.default_rng(seed)
+    x = {"normal": lambda: r.standard_normal((n, l)),
+         "lognormal": lambda: r.lognormal(0.0, 2.0, (n, l)),
+         "ints": lambda: r.integers(-2, 3, (n, l)).astype(np.float64)}[dist]()
+    ref, zv = oracle.allpairs(x, t=4)
+    d = pc.Dataset(values=x)
+    fast = pc.allpairs(d)
+    assert np.max(np.abs(fast.packed - ref)) <= 1e-12
+    assert fast.zero_variance == frozenset(np.flatnonzero(zv).tolist())
+    exact = pc.allpairs(d, exact=True)
+    assert np.array_equal(exact.packed.view(np.uint64), ref.view(np.uint64))
