@@ -370,3 +370,16 @@ def test_load_dataset_tsv_like_reference(tmp_path):
     b = tmp_path / "d.lpcc"
     pc.save_dataset(b, pc.Dataset(values=np.arange(6.0).reshape(2, 3)))
     assert pc.load_dataset(b).values.tolist() == [[0, 1, 2], [3, 4, 5]]
+
+
+def test_stream_plan_ends_with_half_wave_passes():
+    """The top-down phase ends ..., 1 wave, 1/2, 1/2 (the halves run as one
+    round of 64 x 64 quadrants each): a short download after the last pass."""
+    n = 16384
+    mg = n // 128
+    T = mg * (mg + 1) // 2
+    sp = plan_stream(n, 0, T, 148, 8)
+    sizes = [hi - lo for lo, hi, *_ in sp.passes if _[-1] == 2]
+    assert sizes[-2:] == [74, 74] and sizes[-3] == 148
+    sp = plan_stream(n, 0, T, 148, 8, half_tail=False)
+    assert [hi - lo for lo, hi, *_ in sp.passes][-2:] == [148, 148]
