@@ -156,7 +156,7 @@ def _config_dict(cfg: str, world: int) -> dict:
         "global_batch": spec.n,
         "parallelism": (f"tile-range partition over {world} GPU(s); device step: every rank normalises the "
                         "rows it needs from its resident X, no collective"
-                        + ("; e2e: row-block upload + NCCL all-gather of U" if world > 1 else "")),
+                        + ("; e2e: row-block upload + K1 broadcast of U over peer memory" if world > 1 else "")),
         "l2_policy": "inputs larger than L2 (X and U >= 537 MB vs 126 MB L2); no flush",
         "output": "packed upper triangle n(n+1)/2 f64, sharded per GPU range, kept on device",
     }
@@ -224,6 +224,14 @@ class ClockSampler:
             "reasons": reasons,
             "samples": len(rows),
         }
+
+
+def _exchange_label(ndev: int, world: int) -> str:
+    ex = os.environ.get("PCC_EXCHANGE", "p2p")
+    if ex == "p2p":
+        return ("p2p: K1 broadcasts each rank's rows into every rank's U over peer memory (CUDA IPC"
+                + (", NVLink)" if ndev >= world else "; ranks share one GPU: functional run)"))
+    return "nccl all_gather_into_tensor" if ndev >= world else "gloo via host (ranks share one GPU: functional run)"
 
 
 def _load_traffic(cfg: str):
@@ -385,12 +393,18 @@ def run_b200(args, rank: int, world: int, local_rank: int) -> None:
         def api_call():
             return pc.allpairs(ds, out=host_out)
     else:
-        # U exchange for the e2e leg: NCCL between distinct GPUs; ranks sharing
-        # one GPU (functional runs only) exchange through host memory (gloo)
-        exch_group = dist.new_group(backend="nccl") if ndev >= world else dist.group.WORLD
+        # U exchange for the e2e leg: by default one broadcast K1 kernel writes
+        # each rank's rows into every rank's U over peer memory (CUDA IPC, NVLink
+        # between GPUs); PCC_EXCHANGE=collective uses K1 + NCCL all_gather
+        # instead (host-staged gloo when ranks share a GPU)
+        exchange = os.environ.get("PCC_EXCHANGE", "p2p")
+        if exchange == "collective" and ndev >= world:
+            exch_group = dist.new_group(backend="nccl")
+        else:
+            exch_group = dist.group.WORLD
 
         def api_call():
-            return compute_worker(ds, world, rank, dev, out=host_out, group=exch_group)
+            return compute_worker(ds, world, rank, dev, out=host_out, group=exch_group, exchange=exchange)
     api_call()  # warm-up
     barrier()
     wall = []
@@ -448,8 +462,7 @@ def run_b200(args, rank: int, world: int, local_rank: int) -> None:
             "dtype": "f64",
             "data": "synthetic",
             "config": dict(_config_dict(args.config, world),
-                           **({"u_exchange": "nccl all_gather_into_tensor" if ndev >= world
-                               else "gloo via host (ranks share one GPU: functional run)"} if world > 1 else {})),
+                           **({"u_exchange": _exchange_label(ndev, world)} if world > 1 else {})),
             "gflops": float(n) * n * l / (ms_step * 1e-3) / 1e9,
             "roofline_fp64_frac_of_step": (float(n) * n * l / world / (ms_step * 1e-3) / 1e12) / peak,
             "syrk_ms": syrk_avg_ms,

@@ -92,6 +92,25 @@ int pcc_normalize_rows_f64(const double *x, int64_t ldx, double *u, int64_t ldu,
                            uint8_t *zero_variance, int64_t l, int64_t row_lo, int64_t row_hi,
                            void *stream);
 
+/* pcc_normalize_rows_f64 writing every U row and zero-variance flag to
+ * n_dest (<= 16) buffers at once: u[d] / zero_variance[d] are device
+ * pointers (host array), typically peer GPUs' U over NVLink opened with
+ * pcc_ipc_open_handle -- normalisation fused with the all-gather of U in
+ * the multi-GPU exchange (distributed.exchange_normalize, mode "p2p").
+ * Replaces normalize_rows (_kernels.py:226-252) + the worker model's
+ * per-worker normalisation (worker.py:68-80).  Rows up to 110 KB. */
+int pcc_normalize_rows_bcast_f64(const double *x, int64_t ldx, double *const *u, uint8_t *const *zero_variance,
+                                 int32_t n_dest, int64_t ldu, int64_t l, int64_t row_lo, int64_t row_hi,
+                                 void *stream);
+
+/* Plain device allocation (cudaMalloc) so an IPC handle covers exactly the
+ * buffer; CUDA IPC of such buffers between the ranks of one node. */
+int pcc_device_alloc(size_t bytes, void **ptr);
+int pcc_device_free(void *ptr);
+int pcc_ipc_get_handle(const void *ptr, unsigned char *handle /* 64 bytes */);
+int pcc_ipc_open_handle(const unsigned char *handle /* 64 bytes */, void **ptr);
+int pcc_ipc_close_handle(void *ptr);
+
 /* Zero rows [row_lo, row_hi) of U (the pad rows up to pcc_rows_padded(n)). */
 int pcc_zero_rows_f64(double *u, int64_t ldu, int64_t row_lo, int64_t row_hi, void *stream);
 

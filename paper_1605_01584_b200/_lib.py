@@ -47,6 +47,12 @@ EXPORTED_SYMBOLS = (
     "pcc_ldu",
     "pcc_gpu_tile_count",
     "pcc_normalize_rows_f64",
+    "pcc_normalize_rows_bcast_f64",
+    "pcc_device_alloc",
+    "pcc_device_free",
+    "pcc_ipc_get_handle",
+    "pcc_ipc_open_handle",
+    "pcc_ipc_close_handle",
     "pcc_zero_rows_f64",
     "pcc_syrk_f64",
     "pcc_syrk_f64_variant",
@@ -94,6 +100,13 @@ def _bind(l: ctypes.CDLL) -> None:
         "pcc_gpu_tile_count": (_u64, [_i64]),
         "pcc_normalize_rows_f64": (ctypes.c_int, [_vp, _i64, _vp, _i64, _vp, _i64, _i64, _i64, _vp]),
         "pcc_zero_rows_f64": (ctypes.c_int, [_vp, _i64, _i64, _i64, _vp]),
+        "pcc_normalize_rows_bcast_f64": (ctypes.c_int, [_vp, _i64, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _i32,
+                                                        _i64, _i64, _i64, _i64, _vp]),
+        "pcc_device_alloc": (ctypes.c_int, [ctypes.c_size_t, ctypes.POINTER(_vp)]),
+        "pcc_device_free": (ctypes.c_int, [_vp]),
+        "pcc_ipc_get_handle": (ctypes.c_int, [_vp, ctypes.c_char_p]),
+        "pcc_ipc_open_handle": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(_vp)]),
+        "pcc_ipc_close_handle": (ctypes.c_int, [_vp]),
         "pcc_syrk_f64": (ctypes.c_int, [_vp, _i64, _i64, _i64, _u64, _u64, _i32, _vp, _i64, _u64, _i32, _u64, _u64, _vp]),
         "pcc_syrk_f64_variant": (ctypes.c_int, [_i32, _vp, _i64, _i64, _i64, _u64, _u64, _i32, _vp, _i64, _u64, _i32, _u64, _u64, _vp]),
         "pcc_syrk_exact_f64": (ctypes.c_int, [_vp, _i64, _i64, _i64, _u64, _u64, _i32, _vp, _i64, _u64, _i32, _u64, _u64, _vp]),
@@ -166,3 +179,56 @@ def syrk_fn(exact: bool = False):
     """The contraction entry point: the tensor-core path (``pcc_syrk_f64``) or
     the bit-exact dot8 path (``pcc_syrk_exact_f64``); same arguments."""
     return lib().pcc_syrk_exact_f64 if exact else lib().pcc_syrk_f64
+
+
+IPC_HANDLE_BYTES = 64
+
+
+class DeviceBuffer:
+    """Raw ``cudaMalloc`` buffer (``pcc_device_alloc``), or a peer buffer opened
+    from a CUDA IPC handle; ``tensor()`` views it as a torch tensor through
+    ``__cuda_array_interface__`` (the view keeps the buffer alive)."""
+
+    def __init__(self, nbytes: int = 0, handle: bytes | None = None):
+        self.ptr = ctypes.c_void_p()
+        self.nbytes = nbytes
+        self.opened = handle is not None
+        if handle is None:
+            check(lib().pcc_device_alloc(nbytes, ctypes.byref(self.ptr)), "pcc_device_alloc")
+        else:
+            check(lib().pcc_ipc_open_handle(handle, ctypes.byref(self.ptr)), "pcc_ipc_open_handle")
+        self._shape = None
+
+    @property
+    def address(self) -> int:
+        return int(self.ptr.value or 0)
+
+    def ipc_handle(self) -> bytes:
+        buf = ctypes.create_string_buffer(IPC_HANDLE_BYTES)
+        check(lib().pcc_ipc_get_handle(self.ptr, buf), "pcc_ipc_get_handle")
+        return buf.raw
+
+    def tensor(self, shape, typestr: str):
+        import torch
+
+        self._shape = (tuple(shape), typestr)
+        return torch.as_tensor(self, device="cuda")
+
+    @property
+    def __cuda_array_interface__(self):
+        shape, typestr = self._shape
+        return {"shape": shape, "typestr": typestr, "data": (self.address, False), "version": 3}
+
+    def close(self) -> None:
+        if self.ptr.value:
+            if self.opened:
+                lib().pcc_ipc_close_handle(self.ptr)
+            else:
+                lib().pcc_device_free(self.ptr)
+            self.ptr = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 - interpreter shutdown
+            pass

@@ -193,11 +193,22 @@ __device__ unsigned long long g_k1_phase[8];
   } while (0)
 #endif
 
-template <int kNormSmemThreads>
+// Extra destinations of the broadcast variant: each U row (and flag) is
+// stored to every listed buffer -- peer GPUs' U over NVLink (CUDA IPC
+// mappings) in the multi-GPU exchange, so normalisation and the all-gather
+// of U are one kernel.
+constexpr int kMaxNormDests = 16;
+struct NormDests {
+  double *u[kMaxNormDests];
+  uint8_t *flags[kMaxNormDests];
+  int n;
+};
+
+template <int kNormSmemThreads, bool BCAST = false>
 __global__ void __launch_bounds__(kNormSmemThreads)
 normalize_rows_smem_kernel(const double *__restrict__ x, int64_t ldx, double *__restrict__ u, int64_t ldu,
                            uint8_t *__restrict__ zero_variance, int64_t l, int64_t row_lo, int64_t row_hi,
-                           int rows_per_cta) {
+                           int rows_per_cta, NormDests dests) {
   extern __shared__ __align__(16) double srow[];  // [rows_per_cta][l]
   __shared__ double s_mean[kNormSmemMaxRows], s_scale[kNormSmemMaxRows];
   __shared__ int s_zero[kNormSmemMaxRows];
@@ -259,7 +270,11 @@ normalize_rows_smem_kernel(const double *__restrict__ x, int64_t ldx, double *__
     s_zero[row] = zero;
     s_mean[row] = mean;
     s_scale[row] = zero ? 0.0 : __dsqrt_rn(q);
-    zero_variance[r0 + row] = zero ? 1 : 0;
+    if (BCAST) {
+      for (int d = 0; d < dests.n; ++d) dests.flags[d][r0 + row] = zero ? 1 : 0;
+    } else {
+      zero_variance[r0 + row] = zero ? 1 : 0;
+    }
   }
   __syncthreads();
   K1_MARK(1);
@@ -267,10 +282,17 @@ normalize_rows_smem_kernel(const double *__restrict__ x, int64_t ldx, double *__
   // 3. write U rows (coalesced): u = (x - mean) / scale, zero rows for zero
   //    variance, zero K padding
   for (int r = 0; r < rows; ++r) {
-    double *ur = u + (r0 + r) * ldu;
+    const int64_t off = (r0 + r) * ldu;
+    auto put = [&](int64_t k, double v) {  // one store, or one per destination
+      if (BCAST) {
+        for (int d = 0; d < dests.n; ++d) dests.u[d][off + k] = v;
+      } else {
+        u[off + k] = v;
+      }
+    };
     const double *ds = srow + (int64_t)r * l;
     if (s_zero[r]) {
-      for (int64_t k = tid; k < ldu; k += kNormSmemThreads) ur[k] = 0.0;
+      for (int64_t k = tid; k < ldu; k += kNormSmemThreads) put(k, 0.0);
     } else {
       const double sc = s_scale[r], m = s_mean[r];
       // u = (x - mean) / scale; four independent divisions per iteration keep
@@ -280,13 +302,13 @@ normalize_rows_smem_kernel(const double *__restrict__ x, int64_t ldx, double *__
       for (; k + 3 * T < l; k += 4 * T) {
         const double q0 = __ddiv_rn(__dsub_rn(ds[k], m), sc), q1 = __ddiv_rn(__dsub_rn(ds[k + T], m), sc);
         const double q2 = __ddiv_rn(__dsub_rn(ds[k + 2 * T], m), sc), q3 = __ddiv_rn(__dsub_rn(ds[k + 3 * T], m), sc);
-        ur[k] = q0;
-        ur[k + T] = q1;
-        ur[k + 2 * T] = q2;
-        ur[k + 3 * T] = q3;
+        put(k, q0);
+        put(k + T, q1);
+        put(k + 2 * T, q2);
+        put(k + 3 * T, q3);
       }
-      for (; k < l; k += T) ur[k] = __ddiv_rn(__dsub_rn(ds[k], m), sc);
-      for (k = l + tid; k < ldu; k += kNormSmemThreads) ur[k] = 0.0;
+      for (; k < l; k += T) put(k, __ddiv_rn(__dsub_rn(ds[k], m), sc));
+      for (k = l + tid; k < ldu; k += kNormSmemThreads) put(k, 0.0);
     }
   }
   K1_MARK(2);

@@ -375,6 +375,75 @@ int launch_syrk(const double *u, int64_t n, int64_t l, int64_t ldu, uint64_t tb,
   }
 }
 
+// Shared-memory-staged K1 launch (the default whenever a row fits), single
+// destination or broadcast to dests; kNotStaged if the row is too long.
+constexpr int kNotStaged = -1;
+template <bool BCAST>
+int launch_normalize_staged(const double *x, int64_t ldx, double *u, int64_t ldu, uint8_t *zero_variance, int64_t l,
+                            int64_t row_lo, int64_t row_hi, const pcc::NormDests &dests, cudaStream_t stream) {
+  const uint64_t rows = (uint64_t)(row_hi - row_lo);
+  const int64_t row_bytes = l * (int64_t)sizeof(double);
+  constexpr int64_t kSmPerSmem = 224 * 1024;
+  static std::once_flag attr_once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(attr_once, [] {
+    const void *fns[] = {(const void *)pcc::normalize_rows_smem_kernel<64, BCAST>,
+                         (const void *)pcc::normalize_rows_smem_kernel<128, BCAST>,
+                         (const void *)pcc::normalize_rows_smem_kernel<256, BCAST>};
+    for (const void *f : fns)
+      if (attr_err == cudaSuccess)
+        attr_err = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmPerSmem);
+  });
+  if (attr_err != cudaSuccess) return cuda_fail(attr_err, "cudaFuncSetAttribute(normalize smem)");
+  // Shared-memory staging in natural order: as many CTAs per SM as rows allow
+  // (4, 3, 2, then 1 CTA/SM), up to 8 rows per CTA.
+  int per_cta = 0;
+  size_t smem = 0;
+  // Measured (round 1, profiles/r01_normalize.log): staging beats the
+  // 3-pass kernel at every BASELINE row size (c4, 64 KB rows: 1.41 vs 1.82 ms).
+  constexpr int64_t kMaxStagedRow = 110 * 1024;
+  for (int ctas = 4; ctas >= 1 && per_cta == 0 && row_bytes <= kMaxStagedRow; --ctas) {
+    const int64_t budget = kSmPerSmem / ctas - 1024;
+    if (row_bytes <= budget) {
+      per_cta = (int)(budget / row_bytes < pcc::kNormSmemMaxRows ? budget / row_bytes : pcc::kNormSmemMaxRows);
+      smem = (size_t)per_cta * (size_t)row_bytes;
+    }
+  }
+  if (per_cta < 1) return kNotStaged;
+  static const int width = [] {  // tuning knob: PCC_NORMALIZE_THREADS = 64 | 128 | 256
+    const char *e = getenv("PCC_NORMALIZE_THREADS");
+    return e ? atoi(e) : 0;
+  }();
+  // Widest CTA whose register footprint still lets every smem-resident CTA
+  // run (measured, profiles/r01_normalize.log: c2 -> 128, c4 -> 256).
+  static int regs = 0;
+  if (regs == 0) {
+    cudaFuncAttributes fa;
+    regs = cudaFuncGetAttributes(&fa, pcc::normalize_rows_smem_kernel<256, BCAST>) == cudaSuccess ? fa.numRegs : 72;
+  }
+  const int64_t occ_smem = (228 * 1024) / ((int64_t)smem + 1024);
+  int threads = 64;
+  for (int t : {256, 128})
+    if (occ_smem * t * regs <= 65536) {
+      threads = t;
+      break;
+    }
+  if (width) threads = width;
+  const uint64_t grid = ceil_div(rows, (uint64_t)per_cta);
+  if (grid > 0x7FFFFFFFull) return fail(PCC_EINVAL, "too many rows");
+  if (threads == 256)
+    pcc::normalize_rows_smem_kernel<256, BCAST><<<(unsigned)grid, 256, smem, stream>>>(
+        x, ldx, u, ldu, zero_variance, l, row_lo, row_hi, per_cta, dests);
+  else if (threads == 128)
+    pcc::normalize_rows_smem_kernel<128, BCAST><<<(unsigned)grid, 128, smem, stream>>>(
+        x, ldx, u, ldu, zero_variance, l, row_lo, row_hi, per_cta, dests);
+  else
+    pcc::normalize_rows_smem_kernel<64, BCAST><<<(unsigned)grid, 64, smem, stream>>>(
+        x, ldx, u, ldu, zero_variance, l, row_lo, row_hi, per_cta, dests);
+  PCC_CUDA(cudaGetLastError(), "normalize_rows_smem_kernel launch");
+  return PCC_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -424,71 +493,16 @@ int pcc_normalize_rows_f64(const double *x, int64_t ldx, double *u, int64_t ldu,
   if (row_hi == row_lo) return PCC_OK;
   if (!x || !u || !zero_variance) return fail(PCC_EINVAL, "null pointer");
   const uint64_t rows = (uint64_t)(row_hi - row_lo);
-  const int64_t row_bytes = l * (int64_t)sizeof(double);
-  constexpr int64_t kSmPerSmem = 224 * 1024;
   static const int mode = [] {
     // tuning knob: PCC_NORMALIZE_KERNEL = global forces the 3-pass kernel
     const char *e = getenv("PCC_NORMALIZE_KERNEL");
     return (e && strcmp(e, "global") == 0) ? 0 : 1;
   }();
-  static std::once_flag attr_once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(attr_once, [] {
-    const void *fns[] = {(const void *)pcc::normalize_rows_smem_kernel<64>,
-                         (const void *)pcc::normalize_rows_smem_kernel<128>,
-                         (const void *)pcc::normalize_rows_smem_kernel<256>};
-    for (const void *f : fns)
-      if (attr_err == cudaSuccess)
-        attr_err = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmPerSmem);
-  });
-  if (attr_err != cudaSuccess) return cuda_fail(attr_err, "cudaFuncSetAttribute(normalize smem)");
-  // Shared-memory staging in natural order: as many CTAs per SM as rows allow
-  // (4, 3, 2, then 1 CTA/SM), up to 8 rows per CTA.
-  int per_cta = 0;
-  size_t smem = 0;
-  // Measured (round 1, profiles/r01_normalize.log): staging beats the
-  // 3-pass kernel at every BASELINE row size (c4, 64 KB rows: 1.41 vs 1.82 ms).
-  constexpr int64_t kMaxStagedRow = 110 * 1024;
-  for (int ctas = 4; ctas >= 1 && per_cta == 0 && row_bytes <= kMaxStagedRow; --ctas) {
-    const int64_t budget = kSmPerSmem / ctas - 1024;
-    if (row_bytes <= budget) {
-      per_cta = (int)(budget / row_bytes < pcc::kNormSmemMaxRows ? budget / row_bytes : pcc::kNormSmemMaxRows);
-      smem = (size_t)per_cta * (size_t)row_bytes;
-    }
-  }
-  if (per_cta >= 1 && mode == 1) {
-    static const int width = [] {  // tuning knob: PCC_NORMALIZE_THREADS = 64 | 128 | 256
-      const char *e = getenv("PCC_NORMALIZE_THREADS");
-      return e ? atoi(e) : 0;
-    }();
-    // Widest CTA whose register footprint still lets every smem-resident CTA
-    // run (measured, profiles/r01_normalize.log: c2 -> 128, c4 -> 256).
-    static int regs = 0;
-    if (regs == 0) {
-      cudaFuncAttributes fa;
-      regs = cudaFuncGetAttributes(&fa, pcc::normalize_rows_smem_kernel<256>) == cudaSuccess ? fa.numRegs : 72;
-    }
-    const int64_t occ_smem = (228 * 1024) / ((int64_t)smem + 1024);
-    int threads = 64;
-    for (int t : {256, 128})
-      if (occ_smem * t * regs <= 65536) {
-        threads = t;
-        break;
-      }
-    if (width) threads = width;
-    const uint64_t grid = ceil_div(rows, (uint64_t)per_cta);
-    if (grid > 0x7FFFFFFFull) return fail(PCC_EINVAL, "too many rows");
-    if (threads == 256)
-      pcc::normalize_rows_smem_kernel<256><<<(unsigned)grid, 256, smem, (cudaStream_t)stream>>>(
-          x, ldx, u, ldu, zero_variance, l, row_lo, row_hi, per_cta);
-    else if (threads == 128)
-      pcc::normalize_rows_smem_kernel<128><<<(unsigned)grid, 128, smem, (cudaStream_t)stream>>>(
-          x, ldx, u, ldu, zero_variance, l, row_lo, row_hi, per_cta);
-    else
-      pcc::normalize_rows_smem_kernel<64><<<(unsigned)grid, 64, smem, (cudaStream_t)stream>>>(
-          x, ldx, u, ldu, zero_variance, l, row_lo, row_hi, per_cta);
-    PCC_CUDA(cudaGetLastError(), "normalize_rows_smem_kernel launch");
-    return PCC_OK;
+  if (mode == 1) {
+    const pcc::NormDests none{};
+    const int rc = launch_normalize_staged<false>(x, ldx, u, ldu, zero_variance, l, row_lo, row_hi, none,
+                                                  (cudaStream_t)stream);
+    if (rc != kNotStaged) return rc;
   }
   // rows longer than the shared-memory budget: three streaming passes from global memory
   const uint64_t grid = ceil_div(rows, pcc::kNormRowsPerCta);
@@ -496,6 +510,66 @@ int pcc_normalize_rows_f64(const double *x, int64_t ldx, double *u, int64_t ldu,
   pcc::normalize_rows_kernel<<<(unsigned)grid, pcc::kNormThreads, 0, (cudaStream_t)stream>>>(
       x, ldx, u, ldu, zero_variance, l, row_lo, row_hi);
   PCC_CUDA(cudaGetLastError(), "normalize_rows_kernel launch");
+  return PCC_OK;
+}
+
+int pcc_normalize_rows_bcast_f64(const double *x, int64_t ldx, double *const *u, uint8_t *const *zero_variance,
+                                 int32_t n_dest, int64_t ldu, int64_t l, int64_t row_lo, int64_t row_hi,
+                                 void *stream) {
+  if (l < 2) return fail(PCC_EINVAL, "need at least 2 samples per variable, got %lld", (long long)l);
+  if (ldx < l || ldu < l) return fail(PCC_EINVAL, "ldx (%lld) and ldu (%lld) must be >= l (%lld)", (long long)ldx,
+                                      (long long)ldu, (long long)l);
+  if (row_lo < 0 || row_hi < row_lo)
+    return fail(PCC_EINVAL, "bad row range [%lld, %lld)", (long long)row_lo, (long long)row_hi);
+  if (n_dest < 1 || n_dest > pcc::kMaxNormDests)
+    return fail(PCC_EINVAL, "destination count %d outside [1, %d]", n_dest, pcc::kMaxNormDests);
+  if (!x || !u || !zero_variance) return fail(PCC_EINVAL, "null pointer");
+  pcc::NormDests d{};
+  d.n = n_dest;
+  for (int i = 0; i < n_dest; ++i) {
+    if (!u[i] || !zero_variance[i]) return fail(PCC_EINVAL, "null destination %d", i);
+    d.u[i] = u[i];
+    d.flags[i] = zero_variance[i];
+  }
+  if (row_hi == row_lo) return PCC_OK;
+  const int rc = launch_normalize_staged<true>(x, ldx, nullptr, ldu, nullptr, l, row_lo, row_hi, d,
+                                               (cudaStream_t)stream);
+  if (rc == kNotStaged)
+    return fail(PCC_EINVAL, "rows of %lld samples are too long for the broadcast normaliser", (long long)l);
+  return rc;
+}
+
+int pcc_device_alloc(size_t bytes, void **ptr) {
+  if (!ptr) return fail(PCC_EINVAL, "ptr is NULL");
+  *ptr = nullptr;
+  PCC_CUDA(cudaMalloc(ptr, bytes ? bytes : 1), "cudaMalloc");
+  return PCC_OK;
+}
+
+int pcc_device_free(void *ptr) {
+  if (ptr) PCC_CUDA(cudaFree(ptr), "cudaFree");
+  return PCC_OK;
+}
+
+int pcc_ipc_get_handle(const void *ptr, unsigned char *handle) {
+  if (!ptr || !handle) return fail(PCC_EINVAL, "null pointer");
+  cudaIpcMemHandle_t h;
+  PCC_CUDA(cudaIpcGetMemHandle(&h, const_cast<void *>(ptr)), "cudaIpcGetMemHandle");
+  memcpy(handle, &h, sizeof(h));
+  return PCC_OK;
+}
+
+int pcc_ipc_open_handle(const unsigned char *handle, void **ptr) {
+  if (!ptr || !handle) return fail(PCC_EINVAL, "null pointer");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  *ptr = nullptr;
+  PCC_CUDA(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+  return PCC_OK;
+}
+
+int pcc_ipc_close_handle(void *ptr) {
+  if (ptr) PCC_CUDA(cudaIpcCloseMemHandle(ptr), "cudaIpcCloseMemHandle");
   return PCC_OK;
 }
 

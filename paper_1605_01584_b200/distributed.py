@@ -16,6 +16,7 @@ identical for any worker count.
 
 from __future__ import annotations
 
+import ctypes
 import os
 import subprocess
 import sys
@@ -412,13 +413,75 @@ def exchange_rows(u: torch.Tensor, flags: torch.Tensor, S: int, rank: int, world
             t.copy_(host)
 
 
-def exchange_normalize(x_host, n: int, l: int, rank: int, world: int, device: torch.device, group=None):
+EXCHANGES = ("p2p", "collective")
+
+
+def _exchange_normalize_p2p(x_host, n: int, l: int, rank: int, world: int, device: torch.device, group):
+    """K1 fused with the all-gather of U over peer memory: every rank maps
+    every other rank's U (CUDA IPC handles swapped over ``group``) and one
+    broadcast K1 kernel (``pcc_normalize_rows_bcast_f64``) stores each
+    normalised row of this rank's block into all ``p`` buffers -- over NVLink
+    when the ranks sit on different GPUs of one node.  Two ``group``
+    barriers bracket the writes (buffers mapped and pad rows zeroed before,
+    every rank's rows landed after); no kernel ever waits on another rank."""
+    import torch.distributed as dist
+
+    L = _lib.lib()
+    slices, S = row_slices(n, world)
+    r0, r1 = slices[rank]
+    ldu = int(L.pcc_ldu(l))
+    with torch.cuda.device(device):
+        s = stream_handle()
+        ubuf = _lib.DeviceBuffer(world * S * ldu * 8)
+        fbuf = _lib.DeviceBuffer(world * S)
+        u = ubuf.tensor((world * S, ldu), "<f8")
+        flags = fbuf.tensor((world * S,), "|u1")
+        # rows past n are written by nobody: each rank zeroes its own buffer's
+        _lib.check(L.pcc_zero_rows_f64(ptr(u), ldu, n, world * S, s), "pad rows")
+        flags[n:].zero_()
+        mine = (ubuf.ipc_handle(), fbuf.ipc_handle())
+        handles = [None] * world
+        dist.all_gather_object(handles, mine, group=group)
+        peers = {}
+        for q, (hu, hf) in enumerate(handles):
+            if q != rank:
+                peers[q] = (_lib.DeviceBuffer(handle=hu), _lib.DeviceBuffer(handle=hf))
+        torch.cuda.current_stream().synchronize()
+        dist.barrier(group=group)  # every buffer mapped and zero-padded
+        if r1 > r0:
+            xh = x_host if isinstance(x_host, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x_host))
+            xd = torch.empty((r1 - r0, l), dtype=torch.float64, device=device)
+            xd.copy_(xh[r0:r1], non_blocking=xh.is_pinned())
+            us = [ubuf.address if q == rank else peers[q][0].address for q in range(world)]
+            fs = [fbuf.address if q == rank else peers[q][1].address for q in range(world)]
+            uarr = (ctypes.c_void_p * world)(*[a + 8 * r0 * ldu for a in us])
+            farr = (ctypes.c_void_p * world)(*[a + r0 for a in fs])
+            _lib.check(L.pcc_normalize_rows_bcast_f64(ptr(xd), l, uarr, farr, world, ldu, l, 0, r1 - r0, s),
+                       f"rank {rank} normalize+broadcast")
+        torch.cuda.current_stream().synchronize()
+        dist.barrier(group=group)  # every rank's rows have landed everywhere
+        for pu, pf in peers.values():
+            pu.close()
+            pf.close()
+    return u, flags
+
+
+def exchange_normalize(x_host, n: int, l: int, rank: int, world: int, device: torch.device, group=None,
+                       exchange: str = "collective"):
     """Exchange-mode K1: this rank uploads and normalises only its row block
     (``row_slices``), then the blocks are all-gathered so every rank holds
     all of U -- 1/p of X over each GPU's own PCIe link instead of (almost)
     all of it, and the rest over NVLink.  Returns ``(u, flags)`` with
     ``u`` of ``p S`` rows (pad rows zero) and ``flags`` of ``p S`` entries.
+    ``exchange``: ``"collective"`` -- K1, then ``all_gather_into_tensor``
+    (NCCL; host-staged over gloo); ``"p2p"`` -- one K1 kernel that stores
+    the rows straight into every rank's U over peer memory
+    (``_exchange_normalize_p2p``).
     """
+    if exchange not in EXCHANGES:
+        raise ValueError(f"unknown exchange {exchange!r}, expected one of {EXCHANGES}")
+    if exchange == "p2p" and world > 1:
+        return _exchange_normalize_p2p(x_host, n, l, rank, world, device, group)
     L = _lib.lib()
     slices, S = row_slices(n, world)
     r0, r1 = slices[rank]
@@ -440,7 +503,7 @@ def exchange_normalize(x_host, n: int, l: int, rank: int, world: int, device: to
 
 
 def compute_worker(dataset: Dataset, p: int, worker_index: int, device=None, out=None, group=None,
-                   exact: bool = False):
+                   exact: bool = False, exchange: str = "collective"):
     """Run worker ``worker_index`` of a ``p``-way split as a standalone call.
 
     The one-process-per-GPU form of ``run_workers`` (torchrun ranks): upload,
@@ -466,7 +529,7 @@ def compute_worker(dataset: Dataset, p: int, worker_index: int, device=None, out
         if host.numel() < hi_span - lo_span:
             raise ValueError(f"out holds {host.numel()} values, shard needs {hi_span - lo_span}")
     if group is not None and p > 1:
-        u, flags = exchange_normalize(dataset.values, n, l, worker_index, p, dev, group)
+        u, flags = exchange_normalize(dataset.values, n, l, worker_index, p, dev, group, exchange=exchange)
         lo, hi = shard_span(n, a.start, a.stop)
         with torch.cuda.device(dev):
             vals = torch.empty(max(hi - lo, 1), dtype=torch.float64, device=dev)

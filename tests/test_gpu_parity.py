@@ -17,6 +17,7 @@ import torch
 import oracle
 import paper_1605_01584_b200 as pc
 from paper_1605_01584_b200 import _lib
+from paper_1605_01584_b200._device import ptr, stream_handle
 from paper_1605_01584_b200.workloads import make_config
 
 from conftest import random_values
@@ -299,7 +300,7 @@ def test_compute_worker_streamed_shards_match_single(rng):
                 assert sh.zero_variance == frozenset({1})
 
 
-def _exchange_rank(rank, world, port, x, q):
+def _exchange_rank(rank, world, port, x, q, exchange="collective"):
     import os
 
     import torch.distributed as dist
@@ -315,15 +316,16 @@ def _exchange_rank(rank, world, port, x, q):
         lo, hi = shard_span(n, lo_t, hi_t)
         host = torch.full((max(1, hi - lo),), float("nan"), dtype=torch.float64).pin_memory()
         sh = compute_worker(pc.Dataset(values=torch.from_numpy(x).pin_memory()), world, rank, 0, out=host,
-                            group=dist.group.WORLD)
+                            group=dist.group.WORLD, exchange=exchange)
         q.put((rank, [(a, b, host[a - lo:b - lo].numpy().copy()) for a, b in owned_runs(n, lo_t, hi_t)],
                sorted(sh.zero_variance)))
     finally:
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("exchange", ["collective", "p2p"])
 @pytest.mark.parametrize("world,n,l", [(2, 1100, 23), (3, 700, 40), (3, 200, 9)])
-def test_exchange_mode_workers_match_single(world, n, l):
+def test_exchange_mode_workers_match_single(world, n, l, exchange):
     """compute_worker(group=...): row-block upload + K1 per rank, U all-gathered
     (here over gloo: the ranks share this box's one GPU, each rank's kernels
     independent), then each rank's contraction -- reassembled bit for bit
@@ -341,7 +343,7 @@ def test_exchange_mode_workers_match_single(world, n, l):
     sock.close()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_exchange_rank, args=(r, world, port, x, q)) for r in range(world)]
+    procs = [ctx.Process(target=_exchange_rank, args=(r, world, port, x, q, exchange)) for r in range(world)]
     for p_ in procs:
         p_.start()
     got = [q.get(timeout=300) for _ in range(world)]
@@ -694,3 +696,43 @@ def test_allpairs_property_vs_oracle(n, l, seed, dist):
     assert fast.zero_variance == frozenset(np.flatnonzero(zv).tolist())
     exact = pc.allpairs(d, exact=True)
     assert np.array_equal(exact.packed.view(np.uint64), ref.view(np.uint64))
+
+
+def test_normalize_broadcast_writes_every_destination(rng):
+    """pcc_normalize_rows_bcast_f64: one K1 launch stores each row into all
+    destinations (the fused normalise + all-gather of the p2p exchange),
+    bit-identical to the single-destination K1."""
+    import ctypes
+
+    x = torch.from_numpy(random_values(rng, 300, 77, special_rows=True)).cuda()
+    n, l = x.shape
+    L = _lib.lib()
+    ldu = int(L.pcc_ldu(l))
+    ref_u = torch.zeros((n, ldu), dtype=torch.float64, device="cuda")
+    ref_f = torch.zeros(n, dtype=torch.uint8, device="cuda")
+    _lib.check(L.pcc_normalize_rows_f64(ptr(x), l, ptr(ref_u), ldu, ptr(ref_f), l, 0, n, stream_handle()))
+    us = [torch.full((n, ldu), float("nan"), dtype=torch.float64, device="cuda") for _ in range(3)]
+    fs = [torch.full((n,), 7, dtype=torch.uint8, device="cuda") for _ in range(3)]
+    uarr = (ctypes.c_void_p * 3)(*[ptr(t) for t in us])
+    farr = (ctypes.c_void_p * 3)(*[ptr(t) for t in fs])
+    _lib.check(L.pcc_normalize_rows_bcast_f64(ptr(x), l, uarr, farr, 3, ldu, l, 0, n, stream_handle()))
+    torch.cuda.synchronize()
+    for u_, f_ in zip(us, fs):
+        assert torch.equal(u_, ref_u) and torch.equal(f_, ref_f)
+    with pytest.raises(ValueError):
+        _lib.check(L.pcc_normalize_rows_bcast_f64(ptr(x), l, uarr, farr, 0, ldu, l, 0, n, stream_handle()))
+
+
+def test_device_buffer_ipc_roundtrip_and_lifetime():
+    """DeviceBuffer: a cudaMalloc'd buffer viewed as a tensor stays alive as
+    long as the view does; its IPC handle is 64 bytes."""
+    import gc
+
+    b = _lib.DeviceBuffer(1024 * 8)
+    t = b.tensor((1024,), "<f8")
+    assert len(b.ipc_handle()) == _lib.IPC_HANDLE_BYTES
+    t.fill_(3.0)
+    del b
+    gc.collect()
+    t.add_(1.0)
+    assert float(t.sum()) == 4.0 * 1024
