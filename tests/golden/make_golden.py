@@ -125,7 +125,19 @@ def extras() -> None:
         pairs.append({"a": [float(v).hex() for v in a], "b": [float(v).hex() for v in b],
                       "naive": float(pc.pcc_naive(a, b)).hex(),
                       "normalized": float(pc.pcc_normalized(ua[0], ua[1])).hex()})
-    (HERE / "helpers.json").write_text(json.dumps({"gen_synthetic": gens, "pairs": pairs}, indent=1))
+    # file formats byte for byte (fileio.py:58-63 LPCC, :155-274 LPCR)
+    import tempfile
+
+    xs = np.array([[1.0, 2.0, 4.0, 8.0], [3.0, 3.0, 3.0, 3.0], [0.5, -1.5, 2.25, 7.0]])
+    d = pc.Dataset(values=xs)
+    res = pc.allpairs(d, threads=1)
+    with tempfile.TemporaryDirectory() as td:
+        pc.save_dataset(f"{td}/d.lpcc", d)
+        pc.save_result(f"{td}/r.lpcr", res)
+        files = {"x": xs.tolist(), "lpcc_hex": open(f"{td}/d.lpcc", "rb").read().hex(),
+                 "lpcr_hex": open(f"{td}/r.lpcr", "rb").read().hex()}
+    (HERE / "helpers.json").write_text(json.dumps({"gen_synthetic": gens, "pairs": pairs, "files": files},
+                                                  indent=1))
 
 
 def main() -> None:

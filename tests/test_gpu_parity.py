@@ -736,3 +736,56 @@ def test_device_buffer_ipc_roundtrip_and_lifetime():
     gc.collect()
     t.add_(1.0)
     assert float(t.sum()) == 4.0 * 1024
+
+
+def test_pipeline_semantics_match_reference(rng):
+    """run_pipeline behaves as the reference's (pipeline.py:109-187,
+    tests/test_pipeline.py): one call per pass in plan order, capacity 1
+    delivers every tile in order, an empty plan makes no sink call, overlap
+    on / off gives identical bits, a failing sink raises PipelineError with
+    its pass range, and two pipelines on one device do not interfere."""
+    x = random_values(rng, 70, 11, special_rows=True)
+    nd = pc.normalize(pc.Dataset(values=x))
+    geom = pc.TileGeometry(n=70, t=4)
+    T = geom.total_tiles
+    ref = pc.allpairs(pc.Dataset(values=x)).packed
+
+    class Recorder(pc.ResultSink):
+        def __init__(self):
+            self.calls, self.tiles, self.flat = [], [], []
+
+        def consume(self, pass_range, blocks):
+            self.calls.append(tuple(pass_range))
+            self.tiles += [b.tile_id for b in blocks]
+            self.flat.append(np.concatenate([b.values for b in blocks]).copy())
+
+    r = Recorder()
+    pc.run_pipeline(nd, geom, pc.plan_passes(0, T, 1), r)
+    assert r.calls == [(j, j + 1) for j in range(T)] and r.tiles == list(range(T))
+    r = Recorder()
+    pc.run_pipeline(nd, geom, pc.plan_passes(5, 5, 3), r)
+    assert r.calls == []
+    on, off = Recorder(), Recorder()
+    pc.run_pipeline(nd, geom, pc.plan_passes(0, T, 37), on, overlap=True)
+    pc.run_pipeline(nd, geom, pc.plan_passes(0, T, 37), off, overlap=False)
+    assert on.calls == off.calls and all(np.array_equal(a, b) for a, b in zip(on.flat, off.flat))
+
+    class Failing(pc.ResultSink):
+        def __init__(self, at):
+            self.at, self.n = at, 0
+
+        def consume(self, pass_range, blocks):
+            if self.n == self.at:
+                raise RuntimeError("disk full")
+            self.n += 1
+
+    for overlap in (True, False):
+        with pytest.raises(pc.PipelineError) as ei:
+            pc.run_pipeline(nd, geom, pc.plan_passes(0, T, 40), Failing(2), overlap=overlap)
+        assert tuple(ei.value.pass_range) == (80, 120)
+    with pytest.raises(ValueError):
+        pc.run_pipeline(nd, geom, pc.plan_passes(0, T + 1, 40), Recorder())
+    a1, a2 = pc.ResultAssembler(geom, nd.zero_variance), pc.ResultAssembler(geom, nd.zero_variance)
+    pc.run_pipeline(nd, geom, pc.plan_passes(0, T, 29), a1)
+    pc.run_pipeline(nd, geom, pc.plan_passes(0, T, 31), a2)
+    assert np.array_equal(a1.result.packed, ref) and np.array_equal(a2.result.packed, ref)

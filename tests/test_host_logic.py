@@ -383,3 +383,39 @@ def test_stream_plan_ends_with_half_wave_passes():
     assert sizes[-2:] == [74, 74] and sizes[-3] == 148
     sp = plan_stream(n, 0, T, 148, 8, half_tail=False)
     assert [hi - lo for lo, hi, *_ in sp.passes][-2:] == [148, 148]
+
+
+def test_file_formats_byte_identical_to_reference(tmp_path):
+    """LPCC dataset and LPCR result files written here equal the reference's
+    own files byte for byte (tests/golden/helpers.json, made with
+    paircorr.save_dataset / save_result); both load back."""
+    g = json.loads((GOLDEN / "helpers.json").read_text())["files"]
+    x = np.array(g["x"])
+    pc.save_dataset(tmp_path / "d.lpcc", pc.Dataset(values=x))
+    assert (tmp_path / "d.lpcc").read_bytes().hex() == g["lpcc_hex"]
+    packed, zv = oracle.allpairs(x)
+    r = pc.CorrelationResult(n=x.shape[0], packed=packed, zero_variance=frozenset(np.flatnonzero(zv).tolist()))
+    pc.save_result(tmp_path / "r.lpcr", r)
+    assert (tmp_path / "r.lpcr").read_bytes().hex() == g["lpcr_hex"]
+    (tmp_path / "ref.lpcr").write_bytes(bytes.fromhex(g["lpcr_hex"]))
+    back = pc.load_result(tmp_path / "ref.lpcr")
+    assert np.array_equal(back.packed, packed) and back.zero_variance == r.zero_variance
+
+
+def test_file_corruption_detected(tmp_path):
+    x = np.arange(12.0).reshape(3, 4)
+    p = tmp_path / "d.lpcc"
+    pc.save_dataset(p, pc.Dataset(values=x))
+    raw = p.read_bytes()
+    for bad in (raw[:-8], raw + b"\0" * 8, raw[:4] + (2).to_bytes(4, "little") + raw[8:], raw[:10]):
+        p.write_bytes(bad)
+        with pytest.raises(pc.DataError):
+            pc.load_dataset(p, format="binary")
+    r = tmp_path / "r.lpcr"
+    packed, _ = oracle.allpairs(x)
+    pc.save_result(r, pc.CorrelationResult(n=3, packed=packed))
+    raw = r.read_bytes()
+    for bad in (b"NOPE" + raw[4:], raw[:-8], raw[:6]):
+        r.write_bytes(bad)
+        with pytest.raises(pc.DataError):
+            pc.load_result(r)
