@@ -789,3 +789,38 @@ def test_pipeline_semantics_match_reference(rng):
     pc.run_pipeline(nd, geom, pc.plan_passes(0, T, 29), a1)
     pc.run_pipeline(nd, geom, pc.plan_passes(0, T, 31), a2)
     assert np.array_equal(a1.result.packed, ref) and np.array_equal(a2.result.packed, ref)
+
+
+@pytest.mark.parametrize("exact", [True, False])
+def test_compute_pass_tile_layout_kats(rng, exact):
+    """The reference's tile-layout KATs (tests/test_tiles.py): n=2, t=2 gives
+    [r00, r01, 0.0, r11]; n=3, t=2 boundary tiles hold r(y, x) for y <= x < n
+    and exactly 0.0 elsewhere; an empty range gives no blocks.  Exact mode
+    equals pcc_normalized bit for bit, the tensor path within 1e-12."""
+    def check(v, want):
+        if exact:
+            assert v == want
+        else:
+            assert abs(v - want) <= 1e-12
+
+    nd = pc.normalize(pc.Dataset(values=random_values(rng, 2, 6)))
+    blocks = pc.compute_pass(nd, pc.TileGeometry(n=2, t=2), 0, 1, exact=exact)
+    assert len(blocks) == 1
+    r = lambda i, j: pc.pcc_normalized(nd.u[i], nd.u[j])  # noqa: E731
+    v = blocks[0].values
+    check(v[0], r(0, 0)), check(v[1], r(0, 1)), check(v[3], r(1, 1))
+    assert v[2] == 0.0
+    nd = pc.normalize(pc.Dataset(values=random_values(rng, 3, 7)))
+    geom = pc.TileGeometry(n=3, t=2)
+    blocks = pc.compute_pass(nd, geom, 0, 3, exact=exact)
+    assert [b.tile_id for b in blocks] == [0, 1, 2]
+    for b in blocks:
+        Y, X = pc.tile_coord(geom.m, b.tile_id)
+        for off in range(4):
+            y, x = Y * 2 + off // 2, X * 2 + off % 2
+            if y <= x < 3:
+                check(b.values[off], pc.pcc_normalized(nd.u[y], nd.u[x]))
+            else:
+                assert b.values[off] == 0.0
+    nd = pc.normalize(pc.Dataset(values=random_values(rng, 4, 5)))
+    assert len(pc.compute_pass(nd, pc.TileGeometry(n=4, t=2), 2, 2, exact=exact)) == 0
