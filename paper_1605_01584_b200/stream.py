@@ -79,11 +79,16 @@ def lead_fraction(n: int, resident: bool = False) -> float:
 
     Upload time / contraction time ~= 8 B * FP64 rate / (n * PCIe rate)
     (~35 TFLOP/s vs ~50 GB/s on a B200 box); the bottom-up phase should just
-    outlast the upload so the top-down phase never waits for data.
+    outlast the upload so the top-down phase never waits for data.  The
+    1.15 margin is a measured choice (c2 e2e within noise for 0.9-2.0,
+    PCC_STREAM_LEAD_SCALE overrides it for experiments).
     """
     if resident:
         return 0.05
-    return min(0.95, max(0.05, 1.15 * 8 * 35e12 / (n * 50e9)))
+    import os
+
+    scale = float(os.environ.get("PCC_STREAM_LEAD_SCALE", "1.15"))  # tuning experiments
+    return min(0.95, max(0.05, scale * 8 * 35e12 / (n * 50e9)))
 
 
 def plan_stream(n: int, tile_begin: int, tile_end: int, wave: int, chunk_rows: int = 8, mid: int = 8,

@@ -8,6 +8,7 @@ import paper_1605_01584_b200 as pc
 from paper_1605_01584_b200.workloads import make_config
 
 p = argparse.ArgumentParser(); p.add_argument("--config", default="c2"); p.add_argument("--calls", type=int, default=20)
+p.add_argument("--chunk-rows", type=int, default=8); p.add_argument("--quiet", action="store_true")
 a = p.parse_args()
 x = torch.from_numpy(make_config(a.config)).pin_memory()
 n = x.shape[0]
@@ -17,10 +18,10 @@ ts = []
 for i in range(a.calls):
     torch.cuda.synchronize()
     t = time.perf_counter()
-    pc.allpairs(ds, out=out)
+    pc.allpairs(ds, out=out, chunk_rows=a.chunk_rows)
     ts.append((time.perf_counter() - t) * 1e3)
     st = torch.cuda.memory_stats()
-    print(f"call {i}: {ts[-1]:.1f} ms reserved {torch.cuda.memory_reserved() / 2**30:.2f} GiB "
+    if not a.quiet: print(f"call {i}: {ts[-1]:.1f} ms reserved {torch.cuda.memory_reserved() / 2**30:.2f} GiB "
           f"retries {st.get('num_alloc_retries', 0)} cudaMalloc {st.get('num_device_alloc', 0)} "
           f"cudaFree {st.get('num_device_free', 0)}", flush=True)
 print(" ".join(f"{v:.1f}" for v in ts))
