@@ -58,6 +58,18 @@ def test_invalid_arguments_rejected_before_any_device_work():
         _lib.check(L.pcc_syrk_f64(None, 0, 17, 32, 0, 1, 0, None, 0, 0, 0, 0, 0, None))
     with pytest.raises(ValueError, match="tile size"):
         _lib.check(L.pcc_compute_pass_f64(ctypes.c_void_p(16), 10, 5, 32, 0, 0, 1, None, None))
+    with pytest.raises(ValueError, match="ldu"):
+        _lib.check(L.pcc_syrk_exact_f64(None, 10, 17, 16, 0, 1, 0, None, 0, 0, 0, 0, 0, None))
+    with pytest.raises(ValueError, match="tile size"):
+        _lib.check(L.pcc_compute_pass_exact_f64(ctypes.c_void_p(16), 10, 5, 32, 0, 0, 1, None, None))
+    with pytest.raises(ValueError, match="destination count"):
+        _lib.check(L.pcc_normalize_rows_bcast_f64(ctypes.c_void_p(16), 4, None, None, 0, 32, 4, 0, 1, None))
+    with pytest.raises(ValueError, match="tile range"):
+        _lib.check(L.pcc_syrk_launches(100, 0, 10**6, ctypes.byref(ctypes.c_int32())))
+    with pytest.raises(ValueError, match="null"):
+        _lib.check(L.pcc_ipc_get_handle(None, ctypes.create_string_buffer(64)))
+    with pytest.raises(ValueError, match="null"):
+        _lib.check(L.pcc_ipc_open_handle(None, None))
     assert L.pcc_last_error()
 
 
@@ -75,7 +87,10 @@ def test_sass_is_sm100a_and_uses_dmma():
     sass = subprocess.run([exe, "-sass", str(_lib.LIB_PATH)], capture_output=True, text=True).stdout
     assert "sm_100a" in sass
     assert "DMMA.8x8x4" in sass          # FP64 tensor pipe in the contraction
-    assert "LDGSTS" in sass              # cp.async operand staging
+    assert "UTMALDG.2D" in sass          # TMA operand staging (production contraction)
+    assert "SYNCS" in sass               # mbarrier ring
+    assert "LDGSTS" in sass              # cp.async staging (K1, exact mode)
+    assert "DMUL" in sass and "DADD" in sass  # exact mode / K1 chains (no FMA contraction)
 
 
 @pytest.mark.parametrize("n", [1, 129, 300, 2000, 10007, 16384])
