@@ -824,3 +824,25 @@ def test_compute_pass_tile_layout_kats(rng, exact):
                 assert b.values[off] == 0.0
     nd = pc.normalize(pc.Dataset(values=random_values(rng, 4, 5)))
     assert len(pc.compute_pass(nd, pc.TileGeometry(n=4, t=2), 2, 2, exact=exact)) == 0
+
+
+@pytest.mark.parametrize("name", ["c2", "c5"])
+def test_exact_full_size_sampled_rows_bit_identical(name):
+    """Exact mode at full BASELINE size (c2, and c5 with 2.1e9 packed entries
+    = 64-bit offsets): sampled packed rows equal the reference's dot8 bit for
+    bit, diagonals of non-constant rows included."""
+    x = make_config(name)
+    n, l = x.shape
+    d = pc.Dataset(values=torch.from_numpy(x).pin_memory())
+    res = pc.allpairs(d, keep_on_device=True, exact=True)
+    packed = res.packed
+    u_ref, _ = oracle.normalize(x)
+    rng = np.random.default_rng(5)
+    rows = sorted({0, 129, n // 2 + 3, n - 130, n - 1, *rng.integers(0, n, 3).tolist()})
+    ref_rows = oracle.packed_rows(u_ref, rows)
+    for y in rows:
+        lo = (y * (2 * n + 1 - y)) // 2
+        got = packed[lo:lo + n - y].cpu().numpy()
+        assert np.array_equal(got.view(np.uint64), ref_rows[y].view(np.uint64)), (name, y)
+    del packed, res
+    torch.cuda.empty_cache()
