@@ -233,6 +233,14 @@ def run_stream(x, n: int, l: int, device: torch.device, tile_begin: int, tile_en
             xd = torch.empty((n, l), dtype=torch.float64, device=device)
             copy_in = torch.cuda.Stream(device)
             copy_in.wait_stream(compute)  # xd's memory is free from the compute stream's view
+            if not pinned_in:
+                # pageable source: two pinned staging slots (torch's caching host
+                # allocator keeps them across calls); the host copies chunk c+1
+                # (multi-threaded) while chunk c uploads
+                max_rows = max((hi_ - lo_ for lo_, hi_ in plan.chunks), default=0)
+                stage_in = [torch.empty(max(1, max_rows * l), dtype=torch.float64, pin_memory=True)
+                            for _ in range(2)]
+                stage_in_ev = [None, None]
         pinned_out = host_out is not None and host_out.is_pinned()
         if host_out is not None:
             copy_out = torch.cuda.Stream(device)
@@ -245,13 +253,40 @@ def run_stream(x, n: int, l: int, device: torch.device, tile_begin: int, tile_en
         pass_done = []  # (event, dl_row_lo, dl_row_hi) per launched pass, in plan order
         downloaded = []  # job-row intervals already copied
 
+        if host_out is not None and not pinned_out:
+            # pageable destination: D2H into two pinned staging slots, the host
+            # copies each piece out (multi-threaded; first touch of the pages
+            # included) while the next piece transfers
+            piece = int(min(max(1, span_hi - span_lo), 1 << 24))  # <= 128 MB per piece
+            stage_out = [torch.empty(piece, dtype=torch.float64, pin_memory=True) for _ in range(2)]
+            out_pending = []  # (event, slot, a, b) in issue order
+            out_next = [0]
+
+        def drain_one() -> None:
+            ev, sl, a, b = out_pending.pop(0)
+            ev.synchronize()
+            host_out[a - host_base:b - host_base].copy_(stage_out[sl][:b - a])
+
         def copy_rows(r_lo: int, r_hi: int, label: str) -> None:
             a = max(span_lo, _F(n, r_lo))
             b = min(span_hi, _F(n, r_hi))
             if b > a:
-                with torch.cuda.stream(copy_out):
-                    host_out[a - host_base:b - host_base].copy_(out_dev[a - out_base:b - out_base],
-                                                                non_blocking=pinned_out)
+                if pinned_out:
+                    with torch.cuda.stream(copy_out):
+                        host_out[a - host_base:b - host_base].copy_(out_dev[a - out_base:b - out_base],
+                                                                    non_blocking=True)
+                else:
+                    for pa in range(a, b, piece):
+                        pb = min(b, pa + piece)
+                        if len(out_pending) == 2:
+                            drain_one()  # frees the slot used two pieces ago
+                        sl = out_next[0] % 2
+                        out_next[0] += 1
+                        with torch.cuda.stream(copy_out):
+                            stage_out[sl][:pb - pa].copy_(out_dev[pa - out_base:pb - out_base], non_blocking=True)
+                            ev = torch.cuda.Event()
+                            ev.record(copy_out)
+                        out_pending.append((ev, sl, pa, pb))
                 mark(f"download {8 * (b - a) / 1e6:.0f} MB{label}", copy_out)
             downloaded.append((r_lo, r_hi))
 
@@ -272,11 +307,21 @@ def run_stream(x, n: int, l: int, device: torch.device, tile_begin: int, tile_en
         for c, (lo, hi) in enumerate(plan.chunks):
             # upload (pageable sources block here while the GPU runs earlier passes)
             if not on_device:
+                if pinned_in:
+                    src = xh[lo:hi]
+                else:
+                    sl = c % 2
+                    if stage_in_ev[sl] is not None:
+                        stage_in_ev[sl].synchronize()  # the slot's previous upload has finished
+                    src = stage_in[sl][:(hi - lo) * l].view(hi - lo, l)
+                    src.copy_(xh[lo:hi])
                 with torch.cuda.stream(copy_in):
-                    xd[lo:hi].copy_(xh[lo:hi], non_blocking=pinned_in)
+                    xd[lo:hi].copy_(src, non_blocking=True)
                     up = torch.cuda.Event()
                     up.record(copy_in)
                     mark(f"upload rows [{lo},{hi})", copy_in)
+                if not pinned_in:
+                    stage_in_ev[c % 2] = up
                 compute.wait_event(up)
             if resident is None:
                 _lib.check(L.pcc_normalize_rows_f64(ptr(xd), xd.stride(0), ptr(u), ldu, ptr(flags), l, lo, hi, s),
@@ -305,7 +350,7 @@ def run_stream(x, n: int, l: int, device: torch.device, tile_begin: int, tile_en
         for w in workers:
             compute.wait_stream(w)
         if host_out is not None:
-            download(len(pass_done))  # pageable destinations: blocking copies once all work is queued
+            download(len(pass_done))  # pageable destinations: staged copies once all work is queued
             copy_out.wait_stream(compute)
             # rows no pass completed on its own (a row split between the two phases)
             cur = plan.row_lo
@@ -313,6 +358,9 @@ def run_stream(x, n: int, l: int, device: torch.device, tile_begin: int, tile_en
                 if a > cur:
                     copy_rows(cur, a, " (final)")
                 cur = max(cur, b)
+            if not pinned_out:
+                while out_pending:
+                    drain_one()
             copy_out.synchronize()
         compute.synchronize()
         return u, flags, xd
