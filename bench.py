@@ -58,6 +58,7 @@ def parse_args(argv=None):
     p.add_argument("--e2e-steps", type=int, default=None, help="timed end-to-end API calls (default: max(steps, 5)), median reported")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-exact", action="store_true", help="skip the bit-exact (dot8) mode measurement")
+    p.add_argument("--no-pageable", action="store_true", help="skip the numpy-in / numpy-out e2e measurement")
     p.add_argument("--cpu-fraction", type=float, default=None,
                    help="fraction of the reference t=4 tile range in the CPU sample")
     return p.parse_args(argv)
@@ -421,6 +422,23 @@ def run_b200(args, rank: int, world: int, local_rank: int) -> None:
         # sanity: the API result matches the device-timed shard bit for bit
         assert np.array_equal(r.packed.numpy()[:1000], shard[:1000].cpu().numpy())
 
+    # ---- the reference's calling convention: plain numpy in, numpy result
+    # allocated by the call (pageable memory, staged through pinned slots)
+    e2e_pageable = None
+    if world == 1 and not args.no_pageable:
+        ds_np = pc.Dataset(values=x_host)
+        pc.allpairs(ds_np)  # warm-up
+        walls = []
+        for _ in range(3):
+            torch.cuda.synchronize()
+            a = time.perf_counter()
+            r_np = pc.allpairs(ds_np)
+            walls.append(time.perf_counter() - a)
+            del r_np
+        t_np = statistics.median(walls)
+        e2e_pageable = {"value": total_pairs / t_np, "unit": "pairs/s", "ms_per_step": t_np * 1e3, "steps": 3,
+                        "what": "allpairs(Dataset(numpy X)) returning a freshly allocated numpy result"}
+
     # ---- CPU baseline (rank 0, N=1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -472,6 +490,7 @@ def run_b200(args, rank: int, world: int, local_rank: int) -> None:
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3, "steps": e2e_steps},
             "gpu_launches": launches,
             "exact_mode": exact_mode,
+            "e2e_pageable": e2e_pageable,
             "clocks": clock,
         }
         print(json.dumps(line), flush=True)
