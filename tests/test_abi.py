@@ -7,6 +7,7 @@ import ctypes
 import re
 import shutil
 import subprocess
+from pathlib import Path
 
 import pytest
 import torch
@@ -116,3 +117,27 @@ def test_tile_schedule_is_a_permutation_of_the_range(n, group):
                 continue
             ids = np.sort(sym_job_ids(mg, ys[:k], xs[:k]))
             assert np.array_equal(ids, np.arange(tb, te, dtype=np.uint64))
+
+
+def _build_capi_example(tmp_path):
+    root = Path(__file__).resolve().parent.parent
+    exe = tmp_path / "capi_allpairs"
+    cmd = ["gcc", "-O2", "-Wall", "-Werror", f"-I{root / 'include'}", "-I/usr/local/cuda/include",
+           str(root / "examples" / "capi_allpairs.c"), "-o", str(exe), f"-L{root / 'paper_1605_01584_b200' / 'lib'}",
+           "-lpcc_b200", "-L/usr/local/cuda/lib64", "-lcudart",
+           f"-Wl,-rpath,{root / 'paper_1605_01584_b200' / 'lib'}", "-Wl,-rpath,/usr/local/cuda/lib64", "-lm"]
+    subprocess.run(cmd, check=True, capture_output=True, text=True)
+    return exe
+
+
+@pytest.mark.skipif(shutil.which("gcc") is None, reason="no gcc")
+def test_capi_example_compiles_against_the_header(tmp_path):
+    """examples/capi_allpairs.c: the ABI used from plain C (no Python) builds
+    against include/pcc_b200.h and links libpcc_b200.so."""
+    assert _build_capi_example(tmp_path).exists()
+
+
+@pytest.mark.gpu
+def test_capi_example_runs_on_the_gpu(tmp_path):
+    out = subprocess.run([str(_build_capi_example(tmp_path)), "300", "77"], capture_output=True, text=True)
+    assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stdout + out.stderr
