@@ -826,11 +826,11 @@ def test_compute_pass_tile_layout_kats(rng, exact):
     assert len(pc.compute_pass(nd, pc.TileGeometry(n=4, t=2), 2, 2, exact=exact)) == 0
 
 
-@pytest.mark.parametrize("name", ["c2", "c5"])
+@pytest.mark.parametrize("name", ["c2", "c4", "c5"])
 def test_exact_full_size_sampled_rows_bit_identical(name):
-    """Exact mode at full BASELINE size (c2, and c5 with 2.1e9 packed entries
-    = 64-bit offsets): sampled packed rows equal the reference's dot8 bit for
-    bit, diagonals of non-constant rows included."""
+    """Exact mode at full BASELINE size (c2, c4 with l = 8,192, and c5 with
+    2.1e9 packed entries = 64-bit offsets): sampled packed rows equal the
+    reference's dot8 bit for bit, diagonals of non-constant rows included."""
     x = make_config(name)
     n, l = x.shape
     d = pc.Dataset(values=torch.from_numpy(x).pin_memory())
