@@ -55,6 +55,77 @@ def _host_out(out, total: int) -> torch.Tensor:
     return t
 
 
+def _device_result_budget(device: torch.device, n: int, l: int) -> int:
+    """Bytes the packed result may take on ``device``: free memory minus X, U
+    and a margin (``PCC_DEVICE_RESULT_BUDGET`` overrides, for tests)."""
+    import os
+
+    env = os.environ.get("PCC_DEVICE_RESULT_BUDGET")
+    if env:
+        return int(env)
+    free, _ = torch.cuda.mem_get_info(device)
+    L = _lib.lib()
+    xu = n * l * 8 + int(L.pcc_rows_padded(n)) * int(L.pcc_ldu(l)) * 8
+    return max(0, int(0.9 * free) - xu - (1 << 30))
+
+
+def _allpairs_windowed(x_host, n: int, l: int, device: torch.device, host: torch.Tensor, window: int,
+                       exact: bool) -> torch.Tensor:
+    """Packed result larger than the device budget: GPU tile passes whose
+    packed span fits ``window`` doubles, each contracted into one of two
+    device windows (``out_base`` = the pass's span start) and its owned
+    cells (``owned_runs``) copied to ``host`` while the next pass computes --
+    the reference's bounded-memory pass model (pipeline.py:109-170) at GPU
+    tile granularity.  Returns the device zero-variance flags."""
+    from .distributed import owned_runs, shard_span
+
+    L = _lib.lib()
+    x = as_device_f64(x_host, device)
+    u, flags = normalize_device(x)
+    del x
+    T = int(L.pcc_gpu_tile_count(n))
+    mg = -(-n // _lib.GPU_TILE)
+    row_tiles = mg  # a pass always holds at least one tile row's worth of cells
+    window = max(window, shard_span(n, 0, min(T, row_tiles))[1])
+    passes = []
+    tb = 0
+    while tb < T:  # largest te with span(tb, te) <= window (binary search)
+        lo_te, hi_te = tb + 1, T
+        while lo_te < hi_te:
+            mid = (lo_te + hi_te + 1) // 2
+            a, b = shard_span(n, tb, mid)
+            if b - a <= window:
+                lo_te = mid
+            else:
+                hi_te = mid - 1
+        passes.append((tb, lo_te))
+        tb = lo_te
+    compute = torch.cuda.current_stream(device)
+    copy = torch.cuda.Stream(device)
+    bufs = [torch.empty(window, dtype=torch.float64, device=device) for _ in range(min(2, len(passes)))]
+    freed = [None] * len(bufs)
+    pinned = host.is_pinned()
+    syrk = _lib.syrk_fn(exact)
+    for k, (tb, te) in enumerate(passes):
+        b = k % len(bufs)
+        if freed[b] is not None:
+            compute.wait_event(freed[b])  # the window's previous downloads are done
+        span_lo, _ = shard_span(n, tb, te)
+        _lib.check(syrk(ptr(u), n, l, u.shape[1], tb, te, _lib.LAYOUT_PACKED, ptr(bufs[b]), 0, span_lo, 0, 0, 0,
+                        stream_handle(compute)), "allpairs(windowed)")
+        done = torch.cuda.Event()
+        done.record(compute)
+        copy.wait_event(done)
+        with torch.cuda.stream(copy):
+            for ra, rb in owned_runs(n, tb, te):
+                host[ra:rb].copy_(bufs[b][ra - span_lo:rb - span_lo], non_blocking=pinned)
+            freed[b] = torch.cuda.Event()
+            freed[b].record(copy)
+    copy.synchronize()
+    compute.synchronize()
+    return flags
+
+
 def _allpairs_one_device(dataset: Dataset, device: torch.device, keep_on_device: bool, out, chunk_rows: int,
                          output: str, exact: bool = False):
     n, l = dataset.n, dataset.l
@@ -73,6 +144,14 @@ def _allpairs_one_device(dataset: Dataset, device: torch.device, keep_on_device:
 
         total = sym_job_count(n)
         T = int(L.pcc_gpu_tile_count(n))
+        budget = _device_result_budget(device, n, l)
+        if not keep_on_device and total * 8 > budget:
+            # the packed result does not fit the device next to X and U: bounded
+            # device windows, each pass downloaded into the host result
+            host = _host_out(out, total)
+            flags = _allpairs_windowed(dataset.values, n, l, device, host, budget // 8, exact)
+            zv = frozenset(np.flatnonzero(flags.cpu().numpy()).tolist())
+            return (out if out is not None else host.numpy()), zv
         packed = torch.empty(total, dtype=torch.float64, device=device)
         host = None if keep_on_device else _host_out(out, total)
         _, flags, _ = run_stream(dataset.values, n, l, device, 0, T, packed, 0, host, 0, chunk_rows=chunk_rows,

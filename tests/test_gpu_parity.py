@@ -846,3 +846,16 @@ def test_exact_full_size_sampled_rows_bit_identical(name):
         assert np.array_equal(got.view(np.uint64), ref_rows[y].view(np.uint64)), (name, y)
     del packed, res
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("exact", [False, True])
+def test_windowed_allpairs_when_result_exceeds_device_budget(rng, monkeypatch, exact):
+    """A packed result larger than the device budget goes through bounded
+    device windows (one GPU tile pass each) -- same bits as the one-shot path."""
+    x = random_values(rng, 900, 41, special_rows=True)
+    ref = pc.allpairs(pc.Dataset(values=x), exact=exact)
+    monkeypatch.setenv("PCC_DEVICE_RESULT_BUDGET", str(8 * 60_000))  # ~15 windows for 405,450 cells
+    for out in (None, torch.empty(ref.packed.size, dtype=torch.float64).pin_memory()):
+        r = pc.allpairs(pc.Dataset(values=x), exact=exact, out=out)
+        got = r.packed.numpy() if isinstance(r.packed, torch.Tensor) else r.packed
+        assert np.array_equal(got, ref.packed) and r.zero_variance == ref.zero_variance
