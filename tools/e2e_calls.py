@@ -17,11 +17,16 @@ out = torch.empty(n * (n + 1) // 2, dtype=torch.float64).pin_memory()
 ts = []
 for i in range(a.calls):
     torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
     t = time.perf_counter()
     pc.allpairs(ds, out=out, chunk_rows=a.chunk_rows)
     ts.append((time.perf_counter() - t) * 1e3)
+    e1.record()
+    torch.cuda.synchronize()
+    gpu_ms = e0.elapsed_time(e1)
     st = torch.cuda.memory_stats()
-    if not a.quiet: print(f"call {i}: {ts[-1]:.1f} ms reserved {torch.cuda.memory_reserved() / 2**30:.2f} GiB "
+    if not a.quiet: print(f"call {i}: {ts[-1]:.1f} ms (device stream span {gpu_ms:.1f} ms) reserved {torch.cuda.memory_reserved() / 2**30:.2f} GiB "
           f"retries {st.get('num_alloc_retries', 0)} cudaMalloc {st.get('num_device_alloc', 0)} "
           f"cudaFree {st.get('num_device_free', 0)}", flush=True)
 print(" ".join(f"{v:.1f}" for v in ts))
