@@ -410,6 +410,14 @@ int launch_normalize_staged(const double *x, int64_t ldx, double *u, int64_t ldu
     }
   }
   if (per_cta < 1) return kNotStaged;
+  static const int rows_knob = [] {  // tuning knob: PCC_NORMALIZE_ROWS = rows staged per CTA
+    const char *e = getenv("PCC_NORMALIZE_ROWS");
+    return e ? atoi(e) : 0;
+  }();
+  if (rows_knob > 0 && rows_knob <= pcc::kNormSmemMaxRows && rows_knob * row_bytes <= kSmPerSmem - 1024) {
+    per_cta = rows_knob;
+    smem = (size_t)per_cta * (size_t)row_bytes;
+  }
   static const int width = [] {  // tuning knob: PCC_NORMALIZE_THREADS = 64 | 128 | 256
     const char *e = getenv("PCC_NORMALIZE_THREADS");
     return e ? atoi(e) : 0;
