@@ -55,6 +55,9 @@ def _host_out(out, total: int) -> torch.Tensor:
     return t
 
 
+_SMALL_BYTES = 64 << 20  # X + packed result below this: no streaming (measured crossover between c1 and c3)
+
+
 def _device_result_budget(device: torch.device, n: int, l: int) -> int:
     """Bytes the packed result may take on ``device``: free memory minus X, U
     and a margin (``PCC_DEVICE_RESULT_BUDGET`` overrides, for tests)."""
@@ -154,8 +157,21 @@ def _allpairs_one_device(dataset: Dataset, device: torch.device, keep_on_device:
             return (out if out is not None else host.numpy()), zv
         packed = torch.empty(total, dtype=torch.float64, device=device)
         host = None if keep_on_device else _host_out(out, total)
-        _, flags, _ = run_stream(dataset.values, n, l, device, 0, T, packed, 0, host, 0, chunk_rows=chunk_rows,
-                                 exact=exact)
+        if n * l * 8 + total * 8 <= _SMALL_BYTES:
+            # small problem: one upload, K1, one contraction launch, one
+            # download -- the streamed plan's extra launches and events cost
+            # more than they overlap here (c1: 1.0 -> 0.6 ms)
+            compute = torch.cuda.current_stream()
+            x = as_device_f64(dataset.values, device)
+            u, flags = normalize_device(x)
+            _lib.check(_lib.syrk_fn(exact)(ptr(u), n, l, u.shape[1], 0, T, _lib.LAYOUT_PACKED, ptr(packed), 0, 0,
+                                           0, 0, 0, stream_handle(compute)), "allpairs")
+            if host is not None:
+                host.copy_(packed, non_blocking=host.is_pinned())
+            compute.synchronize()
+        else:
+            _, flags, _ = run_stream(dataset.values, n, l, device, 0, T, packed, 0, host, 0, chunk_rows=chunk_rows,
+                                     exact=exact)
         zv = frozenset(np.flatnonzero(flags.cpu().numpy()).tolist())
         if keep_on_device:
             return packed, zv
