@@ -11,8 +11,8 @@
 // warps: the multiply -> add dependency needs them to fill the FP64 pipe):
 // thread t is reference lane j = t & 7 for a 4 x 8 cell block, so each
 // thread carries 32 independent lane accumulators and the 8 lanes of a cell
-// sit in 8 consecutive threads.  U's rows stream through a 3-stage cp.async ring of 64-column
-// K chunks (pitch 72 doubles; rows of odd 8-row blocks shifted by 8 doubles,
+// sit in 8 consecutive threads.  U's rows stream through a 2-stage cp.async ring of 128-column
+// K chunks (pitch 136 doubles; rows of odd 8-row blocks shifted by 8 doubles,
 // so the four 8-lane groups of a warp reading four different row blocks
 // pair up on opposite bank halves: the minimum two wavefronts per 64-bit
 // load).  Zero K padding only adds +0.0 to lane sums
@@ -29,9 +29,9 @@ struct ExactCfg {
   static constexpr int kThreads = 256 * 8 / RT;
   static constexpr int BM = 32;      // sub-block rows (y)
   static constexpr int BN = 64;      // sub-block columns (x)
-  static constexpr int BK = 64;           // K chunk (8 steps of each lane)
+  static constexpr int BK = 128;          // K chunk (16 steps of each lane)
   static constexpr int kPitch = BK + 8;   // doubles per staged row
-  static constexpr int STAGES = 3;
+  static constexpr int STAGES = 2;
   static constexpr int kStageDoubles = (BM + BN) * kPitch;
   static constexpr int kSmemBytes = STAGES * kStageDoubles * (int)sizeof(double);
   static constexpr int kSubPerTile = (kTile / BM) * (kTile / BN);  // 8
