@@ -33,14 +33,26 @@ struct ExactCfg {
   static constexpr int kPitch = BK + 8;   // doubles per staged row
   static constexpr int STAGES = 2;
   static constexpr int kStageDoubles = (BM + BN) * kPitch;
-  static constexpr int kSmemBytes = STAGES * kStageDoubles * (int)sizeof(double);
+  static constexpr int kRingBytes = STAGES * kStageDoubles * (int)sizeof(double);
+  static constexpr int kSmemBytes = kRingBytes + 8 * STAGES;  // + one mbarrier per stage (bulk copies)
   static constexpr int kSubPerTile = (kTile / BM) * (kTile / BN);  // 8
 };
 
 // Staged row r of a chunk (0..BM-1: A rows, BM..: B rows) starts here.
 __device__ __forceinline__ int row_off(int r) { return r * ExactCfg::kPitch + ((r >> 3) & 1) * 8; }
 
-template <int LAYOUT>
+__device__ __forceinline__ void bulk_copy_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+
+// BULK (production): each staged row arrives by one 1-D bulk copy
+// (cp.async.bulk, issued by one thread per row, completion counted in bytes
+// on the stage's mbarrier, thread 0 waits and one CTA barrier per chunk
+// publishes it) instead of 16-byte cp.async pieces issued by every thread:
+// c2 82.4 -> 74.3 ms (80 % of the FP64 ALU peak).
+template <int LAYOUT, bool BULK = true>
 __global__ void __launch_bounds__(ExactCfg::kThreads, 1)
 syrk_exact_kernel(const double *__restrict__ u, int64_t n, int64_t ldu, int k_chunks, uint64_t m_g,
                   TileOrder order, Epilogue ep) {
@@ -53,6 +65,15 @@ syrk_exact_kernel(const double *__restrict__ u, int64_t n, int64_t ldu, int k_ch
   const int bj = grp & 7;           // cols bj*8 .. +8
   const uint64_t un = (uint64_t)n;
   const uint64_t units = order.total * C::kSubPerTile;
+  const uint32_t full0 = smem_u32(smem) + C::kRingBytes;  // BULK: one mbarrier per stage after the ring
+  uint32_t chunk_seq = 0;                                  // chunks consumed by this CTA (barrier phases)
+  if (BULK) {
+    if (tid == 0) {
+      for (int st = 0; st < C::STAGES; ++st) mbar_init(full0 + 8 * st, 1);
+      mbar_fence_init();
+    }
+    __syncthreads();
+  }
 
   for (uint64_t w = blockIdx.x; w < units; w += gridDim.x) {
     // tiles in the grouped L2-locality order (as the tensor path), the 8
@@ -68,6 +89,16 @@ syrk_exact_kernel(const double *__restrict__ u, int64_t n, int64_t ldu, int k_ch
     auto load_chunk = [&](int stage, int kc) {
       double *sa = smem + stage * C::kStageDoubles;
       const int64_t k0 = (int64_t)kc * C::BK;
+      if (BULK) {
+        const int cols = (int)((ldu - k0) < C::BK ? (ldu - k0) : C::BK);  // multiple of 32
+        if (tid == 0) mbar_arrive_expect_tx(full0 + 8 * stage, (uint32_t)((C::BM + C::BN) * cols * 8));
+        if (tid < C::BM + C::BN) {
+          const uint64_t grow = tid < C::BM ? row0 + tid : col0 + (tid - C::BM);
+          bulk_copy_g2s(smem_u32(sa + row_off(tid)), u + grow * (uint64_t)ldu + k0, (uint32_t)(cols * 8),
+                        full0 + 8 * stage);
+        }
+        return;
+      }
       // (BM + BN) rows x 32 doubles = 8 x 16-byte pieces per row
       for (int i = tid; i < (C::BM + C::BN) * (C::BK / 2); i += C::kThreads) {
         const int r = i / (C::BK / 2), piece = i % (C::BK / 2);
@@ -89,23 +120,32 @@ syrk_exact_kernel(const double *__restrict__ u, int64_t n, int64_t ldu, int k_ch
 #pragma unroll
       for (int c = 0; c < 8; ++c) acc[i][c] = 0.0;
 
+    const uint32_t seq0 = chunk_seq;  // BULK: stage of chunk kc = (seq0 + kc) % STAGES
 #pragma unroll
     for (int s = 0; s < C::STAGES - 1; ++s) {
-      if (s < k_chunks) load_chunk(s, s);
-      cp_async_commit();
+      if (s < k_chunks) load_chunk(BULK ? (seq0 + s) % C::STAGES : s, s);
+      if (!BULK) cp_async_commit();
     }
     for (int kc = 0; kc < k_chunks; ++kc) {
-      cp_async_wait<C::STAGES - 2>();
+      const int cur = BULK ? (int)((seq0 + kc) % C::STAGES) : kc % C::STAGES;
+      if (BULK) {
+        if (tid == 0) mbar_wait(full0 + 8 * cur, ((seq0 + kc) / C::STAGES) & 1);
+      } else {
+        cp_async_wait<C::STAGES - 2>();
+      }
       __syncthreads();
       {
         const int nxt = kc + C::STAGES - 1;
-        if (nxt < k_chunks) load_chunk(nxt % C::STAGES, nxt);
-        cp_async_commit();
+        if (nxt < k_chunks) load_chunk(BULK ? (int)((seq0 + nxt) % C::STAGES) : nxt % C::STAGES, nxt);
+        if (!BULK) cp_async_commit();
       }
-      const double *sa = smem + (kc % C::STAGES) * C::kStageDoubles + row_off(bi * C::RT) + lane8;
-      const double *sb = smem + (kc % C::STAGES) * C::kStageDoubles + row_off(C::BM + bj * 8) + lane8;
+      const int msteps = BULK ? (int)((ldu - (int64_t)kc * C::BK) < C::BK ? (ldu - (int64_t)kc * C::BK) : C::BK) / 8
+                              : C::BK / 8;
+      const double *sa = smem + cur * C::kStageDoubles + row_off(bi * C::RT) + lane8;
+      const double *sb = smem + cur * C::kStageDoubles + row_off(C::BM + bj * 8) + lane8;
 #pragma unroll
       for (int m = 0; m < C::BK / 8; ++m) {  // this lane's k = kc*BK + m*8 + lane8, increasing
+        if (BULK && m >= msteps) break;       // (a short chunk only at the padded end of the row)
         double a[C::RT], b[8];
 #pragma unroll
         for (int i = 0; i < C::RT; ++i) a[i] = sa[i * C::kPitch + m * 8];
@@ -123,7 +163,8 @@ syrk_exact_kernel(const double *__restrict__ u, int64_t n, int64_t ldu, int k_ch
         }
       }
     }
-    cp_async_wait<0>();
+    if (!BULK) cp_async_wait<0>();
+    chunk_seq += (uint32_t)k_chunks;
     __syncthreads();  // the ring is reloaded by the next unit
 
     // the fixed tree across the 8 lanes of each cell, then lane j stores

@@ -19,8 +19,11 @@ int main(int argc, char **argv) {
   cudaMalloc(&out, (size_t)n * (n + 1) / 2 * 8);
   cudaMemcpy(u, h.data(), rows * ldu * 8, cudaMemcpyHostToDevice);
   using C = pcc::ExactCfg;
-  cudaFuncSetAttribute(pcc::syrk_exact_kernel<pcc::kLayoutPacked>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(pcc::syrk_exact_kernel<pcc::kLayoutPacked, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        C::kSmemBytes);
+  cudaFuncSetAttribute(pcc::syrk_exact_kernel<pcc::kLayoutPacked, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       C::kSmemBytes);
+  const bool bulk = !(argc > 3 && argv[3][0] == 'c');  // 'c': the cp.async variant
 
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const uint64_t m = (n + 127) / 128, T = m * (m + 1) / 2;
@@ -33,7 +36,12 @@ int main(int argc, char **argv) {
   float best = 1e30f;
   for (int r = 0; r < 3; ++r) {
     cudaEventRecord(e0);
-    pcc::syrk_exact_kernel<pcc::kLayoutPacked><<<sms, C::kThreads, C::kSmemBytes>>>(u, n, ldu, k_chunks, m, order, ep);
+    if (bulk)
+      pcc::syrk_exact_kernel<pcc::kLayoutPacked, true><<<sms, C::kThreads, C::kSmemBytes>>>(u, n, ldu, k_chunks, m,
+                                                                                            order, ep);
+    else
+      pcc::syrk_exact_kernel<pcc::kLayoutPacked, false><<<sms, C::kThreads, C::kSmemBytes>>>(u, n, ldu, k_chunks, m,
+                                                                                             order, ep);
     cudaEventRecord(e1); cudaEventSynchronize(e1);
     float ms; cudaEventElapsedTime(&ms, e0, e1); if (r && ms < best) best = ms;
   }
@@ -42,7 +50,7 @@ int main(int argc, char **argv) {
   cudaMemcpy(res.data(), out, res.size() * 8, cudaMemcpyDeviceToHost);
   double cs = 0;
   for (size_t i = 0; i < res.size(); i += 997) cs += res[i];
-  printf("checksum %.17g\n", cs);
+  printf("%s checksum %.17g\n", bulk ? "bulk" : "cp.async", cs);
   printf("n=%ld l=%ld: %.3f ms  %.2f Tops/s  %.1f%% of 18.52 (%s)\n", n, l, best, ops / (best * 1e-3) / 1e12,
          ops / (best * 1e-3) / 1e12 / 18.52 * 100, cudaGetErrorString(cudaGetLastError()));
   return 0;
