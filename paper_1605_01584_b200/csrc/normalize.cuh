@@ -204,6 +204,12 @@ struct NormDests {
   int n;
 };
 
+__device__ __forceinline__ void bulk_copy_row(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+
 template <int kNormSmemThreads, bool BCAST = false>
 __global__ void __launch_bounds__(kNormSmemThreads)
 normalize_rows_smem_kernel(const double *__restrict__ x, int64_t ldx, double *__restrict__ u, int64_t ldu,
@@ -220,9 +226,24 @@ normalize_rows_smem_kernel(const double *__restrict__ x, int64_t ldx, double *__
   long long k1_t_ = clock64();
 #endif
 
-  // 1. stage the rows (16-byte copies when source and destination rows are
-  //    16-byte aligned, 8-byte copies otherwise)
-  for (int r = 0; r < rows; ++r) {
+  // 1. stage the rows: one 1-D bulk copy per row (cp.async.bulk, thread 0,
+  //    byte-counted mbarrier) when every row start is 16-byte aligned and l
+  //    is even; else 16-byte (or 8-byte) cp.async pieces by all threads
+  __shared__ __align__(8) uint64_t s_bar;
+  const bool bulk = (((reinterpret_cast<uintptr_t>(x) | (uintptr_t)(ldx * 8)) & 15) == 0) && (l % 2 == 0);
+  if (bulk) {
+    if (tid == 0) {
+      const uint32_t bar = smem_u32(&s_bar);
+      mbar_init(bar, 1);
+      mbar_fence_init();
+      mbar_arrive_expect_tx(bar, (uint32_t)(rows * l * sizeof(double)));
+      for (int r = 0; r < rows; ++r)
+        bulk_copy_row(sbase + (uint32_t)(r * l * sizeof(double)), x + (r0 + r) * ldx, (uint32_t)(l * sizeof(double)),
+                      bar);
+      mbar_wait(bar, 0);
+    }
+  }
+  for (int r = 0; r < rows && !bulk; ++r) {
     const double *xr = x + (r0 + r) * ldx;
     const uint32_t sr = sbase + (uint32_t)(r * l * sizeof(double));
     if (((reinterpret_cast<uintptr_t>(xr) | sr) & 15) == 0) {
