@@ -147,6 +147,25 @@ int pcc_syrk_exact_f64(const double *u, int64_t n, int64_t l, int64_t ldu, uint6
                        uint64_t tile_end, int32_t layout, double *out, int64_t ld_out, uint64_t out_base,
                        int32_t ref_t, uint64_t ref_begin, uint64_t ref_end, void *stream);
 
+/* Split mode: the contraction on the int8 tensor cores (tcgen05.mma
+ * kind::i8, s32 accumulators in tensor memory) to FP64 accuracy -- the
+ * Ozaki splitting scheme.  pcc_split_rows_f64 writes, for U rows
+ * [row_lo, row_hi) (up to pcc_rows_padded(n), so pad rows become zero), 7
+ * signed radix-128 digit planes (int8, pcc_split_slice_bytes(n, l) bytes,
+ * 16-byte aligned) and one power-of-two scale per row (double[rows]); every
+ * step is exact.  pcc_syrk_split_f64 then contracts GPU tiles
+ * [tile_begin, tile_end) from those digits with the arguments, layouts and
+ * errors of pcc_syrk_f64: 34 int8 products per K step (digit pairs
+ * i + j <= 9), exact in s32, combined in FP64.  |result - U·Uᵀ| <= 9e-13 per
+ * coefficient for l <= 8192; l > 8192 is PCC_EINVAL. */
+uint64_t pcc_split_slice_bytes(int64_t n, int64_t l);
+int pcc_split_rows_f64(const double *u, int64_t n, int64_t l, int64_t ldu, int64_t row_lo,
+                       int64_t row_hi, int8_t *slices, double *scale, void *stream);
+int pcc_syrk_split_f64(const int8_t *slices, const double *scale, int64_t n, int64_t l,
+                       uint64_t tile_begin, uint64_t tile_end, int32_t layout, double *out,
+                       int64_t ld_out, uint64_t out_base, int32_t ref_t, uint64_t ref_begin,
+                       uint64_t ref_end, void *stream);
+
 /* Same as pcc_syrk_f64 with an explicit contraction kernel shape (0 = the
  * production default; 1..4 = the alternatives measured in DESIGN.md).  Every
  * shape computes each cell with the same K order, so all variants produce

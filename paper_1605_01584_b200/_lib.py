@@ -57,6 +57,9 @@ EXPORTED_SYMBOLS = (
     "pcc_syrk_f64",
     "pcc_syrk_f64_variant",
     "pcc_syrk_exact_f64",
+    "pcc_split_slice_bytes",
+    "pcc_split_rows_f64",
+    "pcc_syrk_split_f64",
     "pcc_compute_pass_f64",
     "pcc_compute_pass_exact_f64",
     "pcc_scatter_range_f64",
@@ -110,6 +113,9 @@ def _bind(l: ctypes.CDLL) -> None:
         "pcc_syrk_f64": (ctypes.c_int, [_vp, _i64, _i64, _i64, _u64, _u64, _i32, _vp, _i64, _u64, _i32, _u64, _u64, _vp]),
         "pcc_syrk_f64_variant": (ctypes.c_int, [_i32, _vp, _i64, _i64, _i64, _u64, _u64, _i32, _vp, _i64, _u64, _i32, _u64, _u64, _vp]),
         "pcc_syrk_exact_f64": (ctypes.c_int, [_vp, _i64, _i64, _i64, _u64, _u64, _i32, _vp, _i64, _u64, _i32, _u64, _u64, _vp]),
+        "pcc_split_slice_bytes": (_u64, [_i64, _i64]),
+        "pcc_split_rows_f64": (ctypes.c_int, [_vp, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _vp]),
+        "pcc_syrk_split_f64": (ctypes.c_int, [_vp, _vp, _i64, _i64, _u64, _u64, _i32, _vp, _i64, _u64, _i32, _u64, _u64, _vp]),
         "pcc_compute_pass_f64": (ctypes.c_int, [_vp, _i64, _i64, _i64, _i64, _u64, _u64, _vp, _vp]),
         "pcc_compute_pass_exact_f64": (ctypes.c_int, [_vp, _i64, _i64, _i64, _i64, _u64, _u64, _vp, _vp]),
         "pcc_scatter_range_f64": (ctypes.c_int, [_vp, _vp, _u64, _u64, _i64, _i64, _vp]),

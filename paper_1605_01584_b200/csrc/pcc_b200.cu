@@ -13,6 +13,7 @@
 #include "../../include/pcc_b200.h"
 #include "normalize.cuh"
 #include "exact.cuh"
+#include "split.cuh"
 #include "syrk.cuh"
 #include "verify.cuh"
 
@@ -47,6 +48,7 @@ struct DeviceConfig {
   int variant_ctas[16] = {0};
   int quad_ctas = 0;
   int exact_ctas = 0;
+  int split_ctas = 0;
   size_t total_mem = 0;
 };
 
@@ -128,7 +130,7 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t
                                   const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-int encode_umap(const double *u, int64_t ldu, int64_t rows, CUtensorMap *map, int box_rows = pcc::kTile) {
+EncodeTiledFn encode_fn() {
   static EncodeTiledFn fn = nullptr;
   static std::once_flag once;
   static cudaError_t once_err = cudaSuccess;
@@ -138,7 +140,13 @@ int encode_umap(const double *u, int64_t ldu, int64_t rows, CUtensorMap *map, in
     once_err = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q);
     if (once_err == cudaSuccess && q == cudaDriverEntryPointSuccess) fn = reinterpret_cast<EncodeTiledFn>(p);
   });
-  if (fn == nullptr) return fail(PCC_ECUDA, "cuTensorMapEncodeTiled unavailable (%s)", cudaGetErrorString(once_err));
+  if (fn == nullptr) fail(PCC_ECUDA, "cuTensorMapEncodeTiled unavailable (%s)", cudaGetErrorString(once_err));
+  return fn;
+}
+
+int encode_umap(const double *u, int64_t ldu, int64_t rows, CUtensorMap *map, int box_rows = pcc::kTile) {
+  EncodeTiledFn fn = encode_fn();
+  if (fn == nullptr) return PCC_ECUDA;
   const cuuint64_t dims[2] = {(cuuint64_t)ldu, (cuuint64_t)rows};
   const cuuint64_t strides[1] = {(cuuint64_t)ldu * sizeof(double)};
   const cuuint32_t box[2] = {(cuuint32_t)pcc::kSlab, (cuuint32_t)box_rows};
@@ -148,6 +156,44 @@ int encode_umap(const double *u, int64_t ldu, int64_t rows, CUtensorMap *map, in
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(PCC_ECUDA, "cuTensorMapEncodeTiled failed (CUresult %d)", (int)r);
   return PCC_OK;
+}
+
+// Split-mode digit planes int8 [KB][7][rows][32] as a 3-D tensor {32 B, rows,
+// 7 KB}; a box {32, 128, box_slices} is `box_slices` K-major operand tiles
+// of one K step, written with the 32-byte swizzle the UMMA descriptors use.
+int encode_slice_map(const int8_t *slices, int64_t rows, int64_t k_blocks, int box_slices, CUtensorMap *map) {
+  EncodeTiledFn fn = encode_fn();
+  if (fn == nullptr) return PCC_ECUDA;
+  const cuuint64_t dims[3] = {32, (cuuint64_t)rows, (cuuint64_t)(pcc::SplitCfg::kSlices * k_blocks)};
+  const cuuint64_t strides[2] = {32, (cuuint64_t)rows * 32};
+  const cuuint32_t box[3] = {32, (cuuint32_t)pcc::kTile, (cuuint32_t)box_slices};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t *>(slices), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(PCC_ECUDA, "cuTensorMapEncodeTiled(slices) failed (CUresult %d)", (int)r);
+  return PCC_OK;
+}
+
+template <int LAYOUT>
+int configure_split_one(int *ctas) {
+  using C = pcc::SplitCfg;
+  PCC_CUDA(cudaFuncSetAttribute(pcc::syrk_split_kernel<LAYOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                C::kSmemBytes),
+           "cudaFuncSetAttribute(split smem)");
+  PCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas, pcc::syrk_split_kernel<LAYOUT>, C::kThreads,
+                                                         C::kSmemBytes),
+           "cudaOccupancyMaxActiveBlocksPerMultiprocessor(split)");
+  return PCC_OK;
+}
+
+int configure_split(int *ctas) {
+  int c0 = 0, c1 = 0, c2 = 0;
+  int rc = configure_split_one<pcc::kLayoutPacked>(&c0);
+  if (rc == PCC_OK) rc = configure_split_one<pcc::kLayoutDense>(&c1);
+  if (rc == PCC_OK) rc = configure_split_one<pcc::kLayoutTiles>(&c2);
+  *ctas = c0 < c1 ? (c0 < c2 ? c0 : c2) : (c1 < c2 ? c1 : c2);
+  return rc;
 }
 
 template <class C, int LAYOUT>
@@ -198,6 +244,7 @@ int device_config(const DeviceConfig **out, int device = -1) {
     if (rc == PCC_OK) rc = configure_tma_variant<V0, false>(&c.variant_ctas[12]);
     if (rc == PCC_OK) rc = configure_tma_variant<VQ>(&c.quad_ctas);
     if (rc == PCC_OK) rc = configure_exact(&c.exact_ctas);
+    if (rc == PCC_OK) rc = configure_split(&c.split_ctas);
     if (rc == PCC_OK) rc = configure_one<V1, pcc::kLayoutPacked>(&c.variant_ctas[1]);
     if (rc == PCC_OK) rc = configure_one<V2, pcc::kLayoutPacked>(&c.variant_ctas[2]);
     if (rc == PCC_OK) rc = configure_one<V3, pcc::kLayoutPacked>(&c.variant_ctas[3]);
@@ -329,6 +376,32 @@ int launch_exact(const double *u, int64_t n, int64_t l, int64_t ldu, uint64_t tb
   const pcc::TileOrder order = pcc::make_tile_order(m_g, tb, te, group);
   pcc::syrk_exact_kernel<LAYOUT><<<grid, C::kThreads, C::kSmemBytes, stream>>>(u, n, ldu, k_chunks, m_g, order, ep);
   PCC_CUDA(cudaGetLastError(), "syrk_exact_kernel launch");
+  return PCC_OK;
+}
+
+template <int LAYOUT>
+int launch_split(const int8_t *slices, const double *scale, int64_t n, int64_t l, uint64_t tb, uint64_t te,
+                 const pcc::Epilogue &ep, cudaStream_t stream) {
+  using C = pcc::SplitCfg;
+  if (te <= tb) return PCC_OK;
+  const DeviceConfig *dc = nullptr;
+  int rc = device_config(&dc);
+  if (rc) return rc;
+  const int64_t rows = pcc_rows_padded(n), k_blocks = (int64_t)ceil_div((uint64_t)l, (uint64_t)C::kKStep);
+  CUtensorMap map7, map4;
+  rc = encode_slice_map(slices, rows, k_blocks, 7, &map7);
+  if (rc == PCC_OK) rc = encode_slice_map(slices, rows, k_blocks, 4, &map4);
+  if (rc) return rc;
+  const uint64_t m_g = ceil_div((uint64_t)n, pcc::kTile);
+  const uint64_t resident = (uint64_t)dc->sm_count * (uint64_t)(dc->split_ctas > 0 ? dc->split_ctas : 1);
+  const uint64_t tiles = te - tb;
+  const unsigned grid = (unsigned)(tiles < resident ? tiles : resident);
+  uint32_t group = 1;
+  while ((uint64_t)(group + 1) * (group + 1) <= grid) ++group;
+  const pcc::TileOrder order = pcc::make_tile_order(m_g, tb, te, group);
+  pcc::syrk_split_kernel<LAYOUT><<<grid, C::kThreads, C::kSmemBytes, stream>>>(map7, map4, scale, n, (int)k_blocks,
+                                                                               m_g, order, ep);
+  PCC_CUDA(cudaGetLastError(), "syrk_split_kernel launch");
   return PCC_OK;
 }
 
@@ -634,6 +707,66 @@ int pcc_syrk_exact_f64(const double *u, int64_t n, int64_t l, int64_t ldu, uint6
                        uint64_t ref_begin, uint64_t ref_end, void *stream) {
   return pcc_syrk_f64_variant(PCC_VARIANT_EXACT, u, n, l, ldu, tile_begin, tile_end, layout, out, ld_out, out_base,
                               ref_t, ref_begin, ref_end, stream);
+}
+
+uint64_t pcc_split_slice_bytes(int64_t n, int64_t l) {
+  if (n < 1 || l < 1) return 0;
+  return (uint64_t)pcc::SplitCfg::kSlices * (uint64_t)pcc_rows_padded(n) * ceil_div((uint64_t)l, 32) * 32;
+}
+
+int pcc_split_rows_f64(const double *u, int64_t n, int64_t l, int64_t ldu, int64_t row_lo, int64_t row_hi,
+                       int8_t *slices, double *scale, void *stream) {
+  int rc = check_u(u, n, l, ldu);
+  if (rc) return rc;
+  const int64_t rows = pcc_rows_padded(n);
+  if (row_lo < 0 || row_lo > row_hi || row_hi > rows)
+    return fail(PCC_EINVAL, "row range [%lld, %lld) invalid for %lld padded rows", (long long)row_lo,
+                (long long)row_hi, (long long)rows);
+  if (slices == nullptr || scale == nullptr) return fail(PCC_EINVAL, "slices / scale is NULL");
+  if (reinterpret_cast<uintptr_t>(slices) % 16 != 0) return fail(PCC_EINVAL, "slices must be 16-byte aligned");
+  if (row_hi == row_lo) return PCC_OK;
+  const int64_t rows_per_block = 8;
+  const unsigned grid = (unsigned)ceil_div((uint64_t)(row_hi - row_lo), (uint64_t)rows_per_block);
+  pcc::split_rows_kernel<<<grid, 32 * rows_per_block, 0, (cudaStream_t)stream>>>(u, ldu, l, row_lo, row_hi, rows,
+                                                                                 slices, scale);
+  PCC_CUDA(cudaGetLastError(), "split_rows_kernel launch");
+  return PCC_OK;
+}
+
+int pcc_syrk_split_f64(const int8_t *slices, const double *scale, int64_t n, int64_t l, uint64_t tile_begin,
+                       uint64_t tile_end, int32_t layout, double *out, int64_t ld_out, uint64_t out_base,
+                       int32_t ref_t, uint64_t ref_begin, uint64_t ref_end, void *stream) {
+  if (n < 1 || l < 2) return fail(PCC_EINVAL, "need n >= 1 and l >= 2 (got n=%lld, l=%lld)", (long long)n, (long long)l);
+  if (l > pcc::SplitCfg::kMaxL)
+    return fail(PCC_EINVAL, "split mode is bounded to l <= %lld (got %lld); use pcc_syrk_f64",
+                (long long)pcc::SplitCfg::kMaxL, (long long)l);
+  if (slices == nullptr || scale == nullptr) return fail(PCC_EINVAL, "slices / scale is NULL");
+  if (reinterpret_cast<uintptr_t>(slices) % 16 != 0) return fail(PCC_EINVAL, "slices must be 16-byte aligned");
+  const uint64_t total = pcc_gpu_tile_count(n);
+  if (tile_begin > tile_end || tile_end > total)
+    return fail(PCC_EINVAL, "tile range [%llu, %llu) invalid for %llu tiles", (unsigned long long)tile_begin,
+                (unsigned long long)tile_end, (unsigned long long)total);
+  if (out == nullptr) return fail(PCC_EINVAL, "out is NULL");
+  pcc::Epilogue ep{out, ld_out, out_base, ref_t, 0, ref_begin, ref_end};
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (layout) {
+    case PCC_LAYOUT_PACKED:
+      return launch_split<pcc::kLayoutPacked>(slices, scale, n, l, tile_begin, tile_end, ep, s);
+    case PCC_LAYOUT_DENSE:
+      if (ld_out < n) return fail(PCC_EINVAL, "dense ld_out %lld < n %lld", (long long)ld_out, (long long)n);
+      return launch_split<pcc::kLayoutDense>(slices, scale, n, l, tile_begin, tile_end, ep, s);
+    case PCC_LAYOUT_TILES: {
+      if (ref_t < 1) return fail(PCC_EINVAL, "tile size must be >= 1, got %d", ref_t);
+      ep.ref_m = ceil_div((uint64_t)n, (uint64_t)ref_t);
+      const uint64_t ref_total = ep.ref_m * (ep.ref_m + 1) / 2;
+      if (ref_begin > ref_end || ref_end > ref_total)
+        return fail(PCC_EINVAL, "tile range [%llu, %llu) invalid for %llu tiles", (unsigned long long)ref_begin,
+                    (unsigned long long)ref_end, (unsigned long long)ref_total);
+      return launch_split<pcc::kLayoutTiles>(slices, scale, n, l, tile_begin, tile_end, ep, s);
+    }
+    default:
+      return fail(PCC_EINVAL, "unknown layout %d", layout);
+  }
 }
 
 static int compute_pass_impl(int32_t variant, const double *u, int64_t n, int64_t l, int64_t ldu, int64_t t,

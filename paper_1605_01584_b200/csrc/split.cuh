@@ -1,0 +1,246 @@
+// split.cuh -- the split-integer contraction ("split mode"): U·Uᵀ to FP64
+// accuracy on the 5th-generation tensor cores (tcgen05.mma kind::i8, s32
+// accumulators in TMEM), the Ozaki splitting scheme.
+//
+// Each normalised row u_r (‖u_r‖ = 1 or u_r = 0) is written exactly as
+//     u_r = 2^(e_r) · Σ_{i=1..7} s_{r,i} · 2^(-7i) + ρ_r,
+// s_{r,1} ∈ [-127, 127], s_{r,i≥2} ∈ [-64, 64] (round-to-nearest digits of
+// a radix-128 expansion; every step is an exact FP64 operation), with
+// 2^(e_r) ≤ 2·max|u_r| and |ρ_r,k| ≤ max|u_r|·2^-49.  Then
+//     u_y·u_x ≈ 2^(e_y+e_x) Σ_{d=2..9} 2^(-7d) · A_d,
+//     A_d = Σ_{i+j=d} S_i(y)·S_j(x)            (int8 dot products, exact in s32)
+// i.e. 34 int8 GEMM products (all i, j ≤ 7 with i + j ≤ 9), summed per
+// diagonal d in one s32 TMEM accumulator each (|A_d| ≤ 6·64²·l < 2³¹ for
+// l ≤ 8192... ≤ 2·10⁸ at l = 8192), combined in FP64 by Horner's rule in
+// the epilogue.  Error bound per coefficient, l ≤ 8192:
+// representation ≤ 2·√l·2^-49 ≈ 3.2e-13, dropped products (i + j ≥ 10)
+// ≤ 5.7e-13, FP64 combination ~1e-16 — inside the north star's 1e-12.
+//
+// Layouts.  Slices: int8 [KB][7][R][32] (KB = ⌈l/32⌉ K blocks of 32, R =
+// padded rows), so a TMA box {32 B, 128 rows, 7 slices} is the 7 operand
+// tiles of one K step, each 4 KB, K-major with the 32-byte swizzle the
+// UMMA descriptor names.  Scales: double[R] = 2^(e_r - 7).
+//
+// Kernel (one 128 x 128 GPU tile of the bijection per CTA at a time,
+// persistent, grouped L2-locality order like K2): warp 0 = TMA producer,
+// warp 1 = TMEM owner + MMA issuer (one thread), warps 2..9 = epilogue.
+// TMEM (512 columns) holds four 128 x 128 s32 accumulators, so each tile
+// takes two passes over K: pass 0 accumulates d = 6..9 (24 MMAs per K step,
+// slices 1..7), pass 1 d = 2..5 (10 MMAs, slices 1..4); the epilogue warps
+// fold pass 0 into FP64 registers (Horner) while pass 1 runs, then finish
+// and store through the same store_cell() as K2 (packed / dense / tiles).
+#pragma once
+
+#include "common.cuh"
+#include "syrk.cuh"
+#include "tcgen05.cuh"
+
+namespace pcc {
+
+struct SplitCfg {
+  static constexpr int kSlices = 7;
+  static constexpr int kKStep = 32;                      // int8 K per stage = one MMA
+  static constexpr int kSliceBytes = kTile * kKStep;     // 4 KB: one 128-row operand tile
+  static constexpr int kOpBytes = kSlices * kSliceBytes; // 28 KB
+  static constexpr int kStageBytes = 2 * kOpBytes;       // A + B
+  static constexpr int kStages = 3;
+  static constexpr int kEpiWarps = 8;
+  static constexpr int kThreads = 32 * (2 + kEpiWarps);
+  static constexpr uint32_t kTmemCols = 512;
+  static constexpr int kBarBytes = 8 * (2 * kStages + 2) + 16;
+  static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + kBarBytes;
+  static constexpr int64_t kMaxL = 8192;  // the error bound above holds up to here
+};
+
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap *map, int32_t c0, int32_t c1,
+                                            int32_t c2, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];\n" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+      : "memory");
+}
+
+// ---- slicing: U rows -> int8 digit planes + per-row scale ------------------
+// One warp per row; lane handles 4 consecutive K of every 128-K chunk, so 8
+// lanes fill one 32-byte (K block, slice, row) segment per store.
+__global__ void __launch_bounds__(256) split_rows_kernel(const double *__restrict__ u, int64_t ldu, int64_t l,
+                                                         int64_t row_lo, int64_t row_hi, int64_t rows_total,
+                                                         int8_t *__restrict__ slices, double *__restrict__ scale) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = row_lo + (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= row_hi) return;
+  const double *row = u + r * ldu;
+  double m = 0.0;
+  for (int64_t k = lane; k < l; k += 32) m = fmax(m, fabs(row[k]));
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  int e = 0;
+  if (m > 0.0) {
+    frexp(m, &e);                                // m = f·2^e, f in [0.5, 1)
+    if (ldexp(m, 7 - e) >= 127.5) ++e;           // keep the leading digit within [-127, 127]
+  }
+  if (lane == 0) scale[r] = ldexp(1.0, e - 7);
+  const int64_t kb_count = (l + 31) / 32;
+  const int64_t plane = rows_total * 32;         // bytes between slice planes
+  for (int64_t k0 = 0; k0 < kb_count * 32; k0 += 128) {
+    const int64_t k = k0 + 4 * lane;
+    if (k >= kb_count * 32) break;
+    uint32_t packed[SplitCfg::kSlices] = {};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      double v = (k + j < l) ? ldexp(row[k + j], 7 - e) : 0.0;
+#pragma unroll
+      for (int i = 0; i < SplitCfg::kSlices; ++i) {
+        const double d = rint(v);
+        v = (v - d) * 128.0;                     // exact: fractional part, times a power of two
+        packed[i] |= ((uint32_t)(int32_t)d & 0xFFu) << (8 * j);
+      }
+    }
+    const int64_t kb = k >> 5;
+    int8_t *dst = slices + (kb * SplitCfg::kSlices) * plane + r * 32 + (k & 31);
+#pragma unroll
+    for (int i = 0; i < SplitCfg::kSlices; ++i) *reinterpret_cast<uint32_t *>(dst + i * plane) = packed[i];
+  }
+}
+
+// ---- the contraction ----------------------------------------------------
+template <int LAYOUT>
+__global__ void __launch_bounds__(SplitCfg::kThreads, 1)
+    syrk_split_kernel(const __grid_constant__ CUtensorMap map7, const __grid_constant__ CUtensorMap map4,
+                      const double *__restrict__ scale, int64_t n, int k_blocks, uint64_t m_g, TileOrder order,
+                      Epilogue ep) {
+  using C = SplitCfg;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t ring = (raw + 1023u) & ~1023u;  // 32-byte swizzle atoms: keep 1 KB alignment
+  const uint32_t bars = ring + C::kStages * C::kStageBytes;
+  auto full_bar = [&](int s) { return bars + 8u * s; };
+  auto empty_bar = [&](int s) { return bars + 8u * (C::kStages + s); };
+  const uint32_t tfull = bars + 8u * (2 * C::kStages);
+  const uint32_t tempty = tfull + 8u;
+  const uint32_t tmem_slot = tempty + 8u;
+  uint32_t *tmem_slot_ptr =
+      reinterpret_cast<uint32_t *>(smem_raw + (tmem_slot - raw));
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::kStages; ++s) mbar_init(full_bar(s), 1), mbar_init(empty_bar(s), 1);
+    mbar_init(tfull, 1);
+    mbar_init(tempty, C::kEpiWarps);
+    mbar_fence_init();
+    tma_prefetch_desc(&map7);
+    tma_prefetch_desc(&map4);
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, C::kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot_ptr;
+  const uint64_t count = order.total;
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (uint64_t s = blockIdx.x; s < count; s += gridDim.x) {
+        uint64_t Y, X;
+        tile_at(order, m_g, s, Y, X);
+        for (int pass = 0; pass < 2; ++pass) {
+          const CUtensorMap *map = pass == 0 ? &map7 : &map4;
+          const uint32_t bytes = 2u * (pass == 0 ? 7u : 4u) * C::kSliceBytes;
+          for (int kb = 0; kb < k_blocks; ++kb) {
+            mbar_wait(empty_bar(stage), phase ^ 1);
+            mbar_arrive_expect_tx(full_bar(stage), bytes);
+            const uint32_t a = ring + stage * C::kStageBytes;
+            tma_load_3d(a, map, 0, (int32_t)(Y * kTile), kb * C::kSlices, full_bar(stage));
+            tma_load_3d(a + C::kOpBytes, map, 0, (int32_t)(X * kTile), kb * C::kSlices, full_bar(stage));
+            if (++stage == C::kStages) stage = 0, phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_i8_s32<128, 128>();
+      const uint64_t desc0 = umma_desc_k_sw32(0);
+      int stage = 0;
+      uint32_t phase = 0, use = 0;
+      for (uint64_t s = blockIdx.x; s < count; s += gridDim.x) {
+        for (int pass = 0; pass < 2; ++pass, ++use) {
+          mbar_wait(tempty, (use & 1) ^ 1);  // the epilogue has drained the accumulators
+          tc_fence_after();
+          const int s_lo = pass == 0 ? 4 : 0;  // 0-based diagonal i + j (d - 2)
+          for (int kb = 0; kb < k_blocks; ++kb) {
+            mbar_wait(full_bar(stage), phase);
+            tc_fence_after();
+            const uint32_t a = ring + stage * C::kStageBytes, b = a + C::kOpBytes;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int sd = s_lo + q;
+              const int i_lo = sd > 6 ? sd - 6 : 0, i_hi = sd < 6 ? sd : 6;
+              for (int i = i_lo; i <= i_hi; ++i) {
+                const uint64_t da = desc0 + ((a + i * C::kSliceBytes) >> 4);
+                const uint64_t db = desc0 + ((b + (sd - i) * C::kSliceBytes) >> 4);
+                umma_i8(tmem + 128u * q, da, db, idesc, (kb > 0 || i > i_lo) ? 1u : 0u);
+              }
+            }
+            umma_commit(empty_bar(stage));  // the slot is free once these MMAs have read it
+            if (++stage == C::kStages) stage = 0, phase ^= 1;
+          }
+          umma_commit(tfull);
+        }
+      }
+    }
+  } else {
+    // ---------------- epilogue ----------------
+    const int quad = warp & 3;             // TMEM lanes this warp may access
+    const int half = (warp - 2) >> 2;      // column half of the tile
+    const uint32_t lane_base = (uint32_t)(32 * quad) << 16;
+    const uint64_t un = (uint64_t)n;
+    uint32_t use = 0;
+    for (uint64_t s = blockIdx.x; s < count; s += gridDim.x) {
+      uint64_t Y, X;
+      tile_at(order, m_g, s, Y, X);
+      double t[64];
+#pragma unroll
+      for (int pass = 0; pass < 2; ++pass, ++use) {
+        mbar_wait(tfull, use & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+#pragma unroll
+          for (int q = 3; q >= 0; --q) {
+            int32_t v[16];
+            tmem_ld16(tmem + lane_base + 128u * q + (uint32_t)(64 * half + 16 * c), v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              t[16 * c + j] = (pass == 0 && q == 3) ? (double)v[j] : fma(t[16 * c + j], 0.0078125, (double)v[j]);
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tempty);
+      }
+      const uint64_t y = Y * kTile + 32 * quad + lane;
+      if (y < un) {
+        const double sy = scale[y];
+        const uint64_t prb = (LAYOUT == kLayoutPacked) ? row_prefix(un, y) - y - ep.out_base : 0;
+        const uint64_t x0 = X * kTile + 64 * half;
+#pragma unroll
+        for (int j = 0; j < 64; ++j) {
+          const uint64_t x = x0 + j;
+          if (x >= y && x < un) store_cell<LAYOUT>(ep, y, x, prb, t[j] * sy * __ldg(scale + x));
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, C::kTmemCols);
+}
+
+}  // namespace pcc

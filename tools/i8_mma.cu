@@ -1,0 +1,181 @@
+// i8_mma.cu -- tcgen05.mma kind::i8 on one B200: (1) correctness of the
+// descriptor encodings in csrc/tcgen05.cuh (K-major, 32-byte swizzle, s32
+// accumulators in TMEM) against a host integer GEMM, (2) the tensor pipe's
+// int8 throughput for M = 128 and N = 64 / 128 / 256 with random operands
+// (power draw depends on the data), one CTA per SM.
+//
+//   nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -I paper_1605_01584_b200/csrc \
+//        tools/i8_mma.cu -o tools/i8_mma && ./tools/i8_mma
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "common.cuh"
+#include "tcgen05.cuh"
+
+using namespace pcc;
+
+#define CK(x)                                                                   \
+  do {                                                                          \
+    cudaError_t e_ = (x);                                                       \
+    if (e_ != cudaSuccess) {                                                    \
+      printf("%s:%d %s: %s\n", __FILE__, __LINE__, #x, cudaGetErrorString(e_)); \
+      exit(1);                                                                  \
+    }                                                                           \
+  } while (0)
+
+// byte offset of (row r, k byte c) in a K-major 32-byte-swizzled operand
+__host__ __device__ inline uint32_t sw32(uint32_t r, uint32_t c) {
+  uint32_t off = r * 32 + c;
+  return off ^ (((off >> 7) & 1) << 4);
+}
+
+__device__ inline void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
+// D[128 x 64] = sum_s A_s[128 x 32] B_s[64 x 32]^T over `steps` K steps.
+__global__ void check_kernel(const int8_t *a, const int8_t *b, int steps, int32_t *d) {
+  __shared__ __align__(1024) int8_t sa[4][128 * 32];
+  __shared__ __align__(1024) int8_t sb[4][64 * 32];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int s = 0; s < steps; ++s) {
+    for (int i = tid; i < 128 * 32; i += blockDim.x) sa[s][sw32(i / 32, i % 32)] = a[s * 128 * 32 + i];
+    for (int i = tid; i < 64 * 32; i += blockDim.x) sb[s][sw32(i / 32, i % 32)] = b[s * 64 * 32 + i];
+  }
+  if (warp == 0) tmem_alloc(smem_u32(&tmem_base), 64);
+  if (tid == 0) mbar_init(smem_u32(&bar), 1), mbar_fence_init();
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tm = tmem_base;
+  if (tid == 0) {
+    for (int s = 0; s < steps; ++s)
+      umma_i8(tm, umma_desc_k_sw32(smem_u32(sa[s])), umma_desc_k_sw32(smem_u32(sb[s])), idesc_i8_s32<128, 64>(),
+              s > 0);
+    umma_commit(smem_u32(&bar));
+  }
+  mbar_wait(smem_u32(&bar), 0);
+  tc_fence_after();
+  for (int c = 0; c < 64; c += 16) {
+    int32_t v[16];
+    tmem_ld16(tm + ((uint32_t)(warp * 32) << 16) + c, v);
+    tmem_ld_wait();
+    for (int j = 0; j < 16; ++j) d[(warp * 32 + (tid & 31)) * 64 + c + j] = v[j];
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tm, 64);
+}
+
+template <int N>
+__global__ void peak_kernel(const int8_t *src, int iters, int32_t *sink) {
+  constexpr int kAcc = 512 / N;  // accumulators that fit in TMEM
+  extern __shared__ __align__(1024) int8_t sm[];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ uint32_t tmem_base;
+  int8_t *sa = (int8_t *)(((uintptr_t)sm + 1023) & ~(uintptr_t)1023);  // 7 x 128 x 32
+  int8_t *sb = sa + 7 * 128 * 32;                                      // 7 x N x 32
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int i = tid; i < 7 * (128 + N) * 32; i += blockDim.x) sa[i] = src[(blockIdx.x * 977 + i) & ((1 << 20) - 1)];
+  if (warp == 0) tmem_alloc(smem_u32(&tmem_base), 512);
+  if (tid == 0) mbar_init(smem_u32(&bar), 1), mbar_fence_init();
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tm = tmem_base;
+  if (tid == 0) {
+    const uint32_t a0 = smem_u32(sa), b0 = smem_u32(sb);
+    for (int it = 0; it < iters; ++it) {
+      int q = 0;
+#pragma unroll 1
+      for (int i = 0; i < 7; ++i)
+#pragma unroll 1
+        for (int j = 0; j < 7 && i + j <= 7; ++j, ++q)
+          umma_i8(tm + (uint32_t)(((i + j) % kAcc) * N), umma_desc_k_sw32(a0 + i * 128 * 32),
+                  umma_desc_k_sw32(b0 + j * N * 32), idesc_i8_s32<128, N>(), it > 0 || q >= kAcc);
+    }
+    umma_commit(smem_u32(&bar));
+  }
+  mbar_wait(smem_u32(&bar), 0);
+  tc_fence_after();
+  int32_t v[16];
+  tmem_ld16(tm + ((uint32_t)(warp * 32) << 16), v);
+  tmem_ld_wait();
+  if (v[0] == 0x7fffffff) sink[tid] = v[1];
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tm, 512);
+}
+
+template <int N>
+void run_peak(const int8_t *src, int32_t *sink, int sms) {
+  const size_t smem = 1024 + 7 * (128 + N) * 32;
+  CK(cudaFuncSetAttribute(peak_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int iters = 20000;
+  peak_kernel<N><<<sms, 128, smem>>>(src, 100, sink);
+  CK(cudaDeviceSynchronize());
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0), cudaEventCreate(&e1);
+  for (int rep = 0; rep < 3; ++rep) {
+    cudaEventRecord(e0);
+    peak_kernel<N><<<sms, 128, smem>>>(src, iters, sink);
+    cudaEventRecord(e1);
+    CK(cudaEventSynchronize(e1));
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double ops = 2.0 * 128 * N * 32 * 34.0 * iters * sms;  // 34 MMAs per iteration (i + j <= 7, i, j < 7)
+    printf("M=128 N=%3d K=32 s8*s8->s32: %.3f ms  %.1f TOPS  (%.0f clk per MMA per SM at 1.965 GHz)\n", N, ms,
+           ops / ms / 1e9, ms * 1e-3 * 1.965e9 / (34.0 * iters));
+  }
+}
+
+int main() {
+  cudaDeviceProp p;
+  CK(cudaGetDeviceProperties(&p, 0));
+  printf("%s, %d SMs\n", p.name, p.multiProcessorCount);
+  // (1) correctness, 1..4 accumulated K steps
+  srand(7);
+  std::vector<int8_t> a(4 * 128 * 32), b(4 * 64 * 32);
+  for (auto &x : a) x = (int8_t)(rand() % 255 - 127);
+  for (auto &x : b) x = (int8_t)(rand() % 255 - 127);
+  int8_t *da, *db;
+  int32_t *dd;
+  CK(cudaMalloc(&da, a.size()));
+  CK(cudaMalloc(&db, b.size()));
+  CK(cudaMalloc(&dd, 128 * 64 * 4));
+  CK(cudaMemcpy(da, a.data(), a.size(), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(db, b.data(), b.size(), cudaMemcpyHostToDevice));
+  int bad_total = 0;
+  for (int steps = 1; steps <= 4; ++steps) {
+    check_kernel<<<1, 128>>>(da, db, steps, dd);
+    CK(cudaDeviceSynchronize());
+    std::vector<int32_t> d(128 * 64);
+    CK(cudaMemcpy(d.data(), dd, d.size() * 4, cudaMemcpyDeviceToHost));
+    int bad = 0;
+    for (int r = 0; r < 128; ++r)
+      for (int c = 0; c < 64; ++c) {
+        int32_t ref = 0;
+        for (int s = 0; s < steps; ++s)
+          for (int k = 0; k < 32; ++k) ref += (int32_t)a[s * 4096 + r * 32 + k] * (int32_t)b[s * 2048 + c * 32 + k];
+        if (ref != d[r * 64 + c] && bad++ < 3) printf("  mismatch r=%d c=%d got %d want %d\n", r, c, d[r * 64 + c], ref);
+      }
+    printf("check steps=%d: %s (%d mismatches)\n", steps, bad ? "FAIL" : "ok", bad);
+    bad_total += bad;
+  }
+  // (2) throughput
+  std::vector<int8_t> r(1 << 20);
+  for (auto &x : r) x = (int8_t)(rand() % 255 - 127);
+  int8_t *src;
+  int32_t *sink;
+  CK(cudaMalloc(&src, r.size()));
+  CK(cudaMalloc(&sink, 4096));
+  CK(cudaMemcpy(src, r.data(), r.size(), cudaMemcpyHostToDevice));
+  run_peak<64>(src, sink, p.multiProcessorCount);
+  run_peak<128>(src, sink, p.multiProcessorCount);
+  run_peak<256>(src, sink, p.multiProcessorCount);
+  return bad_total ? 1 : 0;
+}
