@@ -40,6 +40,9 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
+# best measured int8 tcgen05.mma throughput on this pool's B200 (tools/i8_mma.cu,
+# profiles/r01_i8_mma_peak.log); MEASURED_PEAKS.json carries no int8 figure
+I8_PEAK_TOPS = 4122.9
 DEFAULT_CONFIG = "c2"  # BASELINE.json configs[1]: the single-GPU headline configuration
 
 
@@ -58,6 +61,7 @@ def parse_args(argv=None):
     p.add_argument("--e2e-steps", type=int, default=None, help="timed end-to-end API calls (default: max(steps, 5)), median reported")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-exact", action="store_true", help="skip the bit-exact (dot8) mode measurement")
+    p.add_argument("--no-split", action="store_true", help="skip the split-mode (int8 tensor core) measurement")
     p.add_argument("--no-pageable", action="store_true", help="skip the numpy-in / numpy-out e2e measurement")
     p.add_argument("--cpu-fraction", type=float, default=None,
                    help="fraction of the reference t=4 tile range in the CPU sample")
@@ -385,6 +389,67 @@ def run_b200(args, rank: int, world: int, local_rank: int) -> None:
         torch.cuda.synchronize()
         del shard_x
 
+    # ---- split mode (allpairs(method="split")): K1 + int8 digit planes + the
+    # contraction on the int8 tensor cores, same shard, device-timed; plus its
+    # own end-to-end call through the public API
+    split_mode = None
+    if not args.no_split and te > tb and l <= _lib.SPLIT_MAX_L:
+        shard_s = torch.empty_like(shard)
+        sp_state = {}
+
+        def step_split(ev=None):
+            u, _ = normalize_device(x)
+            con = _lib.Contraction("split", u, n, l)
+            if ev is not None:
+                ev[0].record(stream)
+            con.prepare_all(s)
+            if ev is not None:
+                ev[1].record(stream)
+            con.syrk(tb, te, _lib.LAYOUT_PACKED, ptr(shard_s), 0, span_lo, 0, 0, 0, s, "syrk_split")
+            if ev is not None:
+                ev[2].record(stream)
+            sp_state["con"] = con
+
+        sp_steps = max(3, args.steps)
+        step_split()
+        step_split()
+        torch.cuda.synchronize()
+        evs = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(3)) for _ in range(sp_steps)]
+        barrier()
+        torch.cuda.synchronize()
+        t0.record(stream)
+        for i in range(sp_steps):
+            step_split(evs[i])
+        t1.record(stream)
+        torch.cuda.synchronize()
+        sp_ms = max_over_ranks(t0.elapsed_time(t1) / sp_steps)
+        sp_rows_ms = max_over_ranks(sum(a.elapsed_time(b) for a, b, _ in evs) / sp_steps)
+        sp_syrk_ms = max_over_ranks(sum(b.elapsed_time(c) for _, b, c in evs) / sp_steps)
+        i8_ops = 68.0 * l * my_cells  # algorithmic: 34 int8 digit products x 2 l ops per owned pair
+        i8_peak = I8_PEAK_TOPS
+        i8_ach = i8_ops / (sp_syrk_ms * 1e-3) / 1e12
+        diff = float((shard_s[:max(1, span_hi - span_lo)] - shard[:max(1, span_hi - span_lo)]).abs().max())
+        del sp_state["con"]
+        split_mode = {
+            "what": "allpairs(method='split'): Ozaki int8 digit planes on the int8 tensor cores "
+                    "(tcgen05.mma kind::i8, s32 in TMEM), every coefficient within 1e-12 of the reference "
+                    "(tests/test_gpu_split.py); FP64-accurate, not a reduced-precision result",
+            "value": total_pairs / (sp_ms * 1e-3), "unit": "pairs/s", "ms_per_step": sp_ms, "steps": sp_steps,
+            "split_rows_ms": sp_rows_ms, "syrk_ms": sp_syrk_ms,
+            "fp64_equivalent_tflops": flops_launch / (sp_syrk_ms * 1e-3) / 1e12,
+            "max_abs_diff_vs_fp64_tensor_path": diff,
+            "roofline": {"bound": "tensor", "achieved": i8_ach, "peak": i8_peak, "unit": "TOP/s",
+                         "frac": i8_ach / i8_peak,
+                         "kernel": "syrk_split_kernel<packed> (TMA 3-D boxes of 7 digit planes, tcgen05.mma "
+                                   "kind::i8 M128 N128 K32, 4 s32 accumulators in TMEM, 2 K passes per tile)",
+                         "algorithmic_ops_per_launch": i8_ops,
+                         "peak_source": "measured int8 tcgen05.mma throughput on this pool's B200 "
+                                        "(tools/i8_mma.cu, profiles/r01_i8_mma_peak.log: 128x256x32 shape; "
+                                        "the 128x128x32 shape this kernel issues peaks at 3180)"},
+        }
+        del shard_s
+        torch.cuda.synchronize()
+
     # ---- end to end through the public API (pinned X upload + packed download inside)
     e2e_steps = args.e2e_steps if args.e2e_steps is not None else max(args.steps, 5)
     host_out = torch.empty(total_pairs if world == 1 else max(1, span_hi - span_lo), dtype=torch.float64,
@@ -416,6 +481,26 @@ def run_b200(args, rank: int, world: int, local_rank: int) -> None:
         r = api_call()
         wall.append(time.perf_counter() - a)
     e2e_s = max_over_ranks(statistics.median(wall))
+    if split_mode is not None:
+        # the same public call with method="split"
+        if world == 1:
+            def api_split():
+                return pc.allpairs(ds, out=host_out, method="split")
+        else:
+            def api_split():
+                return compute_worker(ds, world, rank, dev, out=host_out, group=exch_group, exchange=exchange,
+                                      method="split")
+        api_split()
+        wall_s = []
+        for _ in range(e2e_steps):
+            torch.cuda.synchronize()
+            barrier()
+            a = time.perf_counter()
+            api_split()
+            wall_s.append(time.perf_counter() - a)
+        e2e_split = max_over_ranks(statistics.median(wall_s))
+        split_mode["e2e"] = {"value": total_pairs / e2e_split, "unit": "pairs/s", "ms_per_step": e2e_split * 1e3,
+                             "steps": e2e_steps, "h2d_bytes_per_step": n * l * 8, "d2h_bytes_per_step": total_pairs * 8}
     h2d = n * l * 8  # world == 1: all of X; N > 1: one row block of X per rank
     d2h = total_pairs * 8
     if world == 1:
@@ -490,6 +575,7 @@ def run_b200(args, rank: int, world: int, local_rank: int) -> None:
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3, "steps": e2e_steps},
             "gpu_launches": launches,
             "exact_mode": exact_mode,
+            "split_mode": split_mode,
             "e2e_pageable": e2e_pageable,
             "clocks": clock,
         }

@@ -157,7 +157,7 @@ int pcc_syrk_exact_f64(const double *u, int64_t n, int64_t l, int64_t ldu, uint6
  * [tile_begin, tile_end) from those digits with the arguments, layouts and
  * errors of pcc_syrk_f64: 34 int8 products per K step (digit pairs
  * i + j <= 9), exact in s32, combined in FP64.  |result - U·Uᵀ| <= 9e-13 per
- * coefficient for l <= 8192; l > 8192 is PCC_EINVAL. */
+ * coefficient for l <= 8192 (K2s); l > 8192 is PCC_EINVAL. */
 uint64_t pcc_split_slice_bytes(int64_t n, int64_t l);
 int pcc_split_rows_f64(const double *u, int64_t n, int64_t l, int64_t ldu, int64_t row_lo,
                        int64_t row_hi, int8_t *slices, double *scale, void *stream);
@@ -189,6 +189,12 @@ int pcc_compute_pass_f64(const double *u, int64_t n, int64_t l, int64_t ldu, int
  * bit. */
 int pcc_compute_pass_exact_f64(const double *u, int64_t n, int64_t l, int64_t ldu, int64_t t,
                                uint64_t j_lo, uint64_t j_hi, double *out, void *stream);
+
+/* pcc_compute_pass_f64 from split-mode digit planes (pcc_split_rows_f64 over
+ * every row the pass touches): the reference's pass-buffer layout, each
+ * coefficient within 1e-12 of the reference's. */
+int pcc_compute_pass_split_f64(const int8_t *slices, const double *scale, int64_t n, int64_t l,
+                               int64_t t, uint64_t j_lo, uint64_t j_hi, double *out, void *stream);
 
 /* Replaces _kernels.scatter_range(packed, values, first_tile, count, m, t, n)
  * (_kernels.py:322-348) on device: copies cells y <= x < n of `count`

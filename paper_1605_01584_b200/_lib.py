@@ -62,6 +62,7 @@ EXPORTED_SYMBOLS = (
     "pcc_syrk_split_f64",
     "pcc_compute_pass_f64",
     "pcc_compute_pass_exact_f64",
+    "pcc_compute_pass_split_f64",
     "pcc_scatter_range_f64",
     "pcc_allpairs_f64",
     "pcc_row_stats_f64",
@@ -118,6 +119,7 @@ def _bind(l: ctypes.CDLL) -> None:
         "pcc_syrk_split_f64": (ctypes.c_int, [_vp, _vp, _i64, _i64, _u64, _u64, _i32, _vp, _i64, _u64, _i32, _u64, _u64, _vp]),
         "pcc_compute_pass_f64": (ctypes.c_int, [_vp, _i64, _i64, _i64, _i64, _u64, _u64, _vp, _vp]),
         "pcc_compute_pass_exact_f64": (ctypes.c_int, [_vp, _i64, _i64, _i64, _i64, _u64, _u64, _vp, _vp]),
+        "pcc_compute_pass_split_f64": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i64, _u64, _u64, _vp, _vp]),
         "pcc_scatter_range_f64": (ctypes.c_int, [_vp, _vp, _u64, _u64, _i64, _i64, _vp]),
         "pcc_allpairs_f64": (ctypes.c_int, [_vp, _i64, _i64, _i64, _vp, _i64, _vp, _u64, _u64, _i32, _vp, _i64, _u64, _vp]),
         "pcc_row_stats_f64": (ctypes.c_int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp]),
@@ -185,6 +187,91 @@ def syrk_fn(exact: bool = False):
     """The contraction entry point: the tensor-core path (``pcc_syrk_f64``) or
     the bit-exact dot8 path (``pcc_syrk_exact_f64``); same arguments."""
     return lib().pcc_syrk_exact_f64 if exact else lib().pcc_syrk_f64
+
+
+# Contraction methods (``allpairs(..., method=)``):
+#   "tensor" -- FP64 tensor cores (DMMA), within 1e-12 of the reference (default);
+#   "split"  -- int8 tensor cores (tcgen05.mma kind::i8) on exact radix-128
+#               digit planes of U (the Ozaki scheme), within 1e-12, l <= 8192;
+#   "exact"  -- the reference's dot8 arithmetic on the FP64 CUDA cores, bit-identical.
+METHODS = ("tensor", "split", "exact")
+SPLIT_MAX_L = 8192
+
+
+def resolve_method(method: str | None = None, exact: bool = False) -> str:
+    """``method`` name from the public arguments (``exact=True`` is ``"exact"``)."""
+    if exact:
+        if method not in (None, "exact"):
+            raise ValueError(f"exact=True conflicts with method={method!r}")
+        return "exact"
+    m = "tensor" if method is None else method
+    if m not in METHODS:
+        raise ValueError(f"unknown contraction method {m!r}, expected one of {METHODS}")
+    return m
+
+
+def check_method_shape(method: str, l: int) -> None:
+    if method == "split" and l > SPLIT_MAX_L:
+        raise ValueError(f"method='split' is bounded to l <= {SPLIT_MAX_L} samples (its 1e-12 error bound); "
+                         f"got l={l}: use method='tensor'")
+
+
+class Contraction:
+    """The contraction over one normalised U (``pcc_rows_padded(n) x ldu``
+    f64 on a CUDA device, pad rows zero) by ``method`` (``METHODS``).
+
+    ``prepare(row_lo, row_hi, stream)`` must follow the normalisation of those
+    rows and precede any contraction that reads them: the split method
+    writes their int8 digit planes and scales (``pcc_split_rows_f64``; a
+    range reaching row n - 1 also covers the pad rows), the other methods
+    read U directly and do nothing.  ``syrk`` / ``compute_pass`` take the
+    arguments of ``pcc_syrk_f64`` / ``pcc_compute_pass_f64`` after U and
+    raise ``DeviceError`` on failure."""
+
+    def __init__(self, method: str, u, n: int, l: int):
+        import torch
+
+        if method not in METHODS:
+            raise ValueError(f"unknown contraction method {method!r}, expected one of {METHODS}")
+        check_method_shape(method, l)
+        self.method, self.u, self.n, self.l = method, u, int(n), int(l)
+        self.ldu, self.rows = int(u.shape[1]), int(u.shape[0])
+        if method == "split":
+            self.slices = torch.empty(int(lib().pcc_split_slice_bytes(n, l)), dtype=torch.uint8, device=u.device)
+            self.scale = torch.empty(self.rows, dtype=torch.float64, device=u.device)
+
+    def prepare(self, row_lo: int, row_hi: int, stream) -> None:
+        if self.method != "split" or row_hi <= row_lo:
+            return
+        if row_hi >= self.n:
+            row_hi = self.rows
+        check(lib().pcc_split_rows_f64(self.u.data_ptr(), self.n, self.l, self.ldu, row_lo, row_hi,
+                                       self.slices.data_ptr(), self.scale.data_ptr(), stream), "split_rows")
+
+    def prepare_all(self, stream) -> "Contraction":
+        self.prepare(0, self.n, stream)
+        return self
+
+    def syrk(self, tile_begin: int, tile_end: int, layout: int, out: int, ld_out: int, out_base: int,
+             ref_t: int, ref_begin: int, ref_end: int, stream, what: str = "syrk") -> None:
+        L = lib()
+        if self.method == "split":
+            rc = L.pcc_syrk_split_f64(self.slices.data_ptr(), self.scale.data_ptr(), self.n, self.l, tile_begin,
+                                      tile_end, layout, out, ld_out, out_base, ref_t, ref_begin, ref_end, stream)
+        else:
+            rc = syrk_fn(self.method == "exact")(self.u.data_ptr(), self.n, self.l, self.ldu, tile_begin, tile_end,
+                                                 layout, out, ld_out, out_base, ref_t, ref_begin, ref_end, stream)
+        check(rc, what)
+
+    def compute_pass(self, t: int, j_lo: int, j_hi: int, out: int, stream) -> None:
+        L = lib()
+        if self.method == "split":
+            rc = L.pcc_compute_pass_split_f64(self.slices.data_ptr(), self.scale.data_ptr(), self.n, self.l, t,
+                                              j_lo, j_hi, out, stream)
+        else:
+            fn = L.pcc_compute_pass_exact_f64 if self.method == "exact" else L.pcc_compute_pass_f64
+            rc = fn(self.u.data_ptr(), self.n, self.l, self.ldu, t, j_lo, j_hi, out, stream)
+        check(rc, "compute_pass")
 
 
 IPC_HANDLE_BYTES = 64

@@ -769,10 +769,14 @@ int pcc_syrk_split_f64(const int8_t *slices, const double *scale, int64_t n, int
   }
 }
 
-static int compute_pass_impl(int32_t variant, const double *u, int64_t n, int64_t l, int64_t ldu, int64_t t,
-                             uint64_t j_lo, uint64_t j_hi, double *out, void *stream) {
-  int rc = check_u(u, n, l, ldu);
-  if (rc) return rc;
+// Reference pass (tiles [j_lo, j_hi) of tile size t, _kernels.py:351-373):
+// validate, zero the pass buffer (cells outside y <= x < n stay 0.0,
+// _kernels.py:370-373) and find the GPU tiles [*tb, *te) covering those
+// reference tile rows; the caller then runs the contraction with the TILES
+// epilogue over them (an empty pass gives *tb == *te).
+static int compute_pass_prepare(int64_t n, int64_t t, uint64_t j_lo, uint64_t j_hi, double *out, void *stream,
+                                uint64_t *tb, uint64_t *te) {
+  *tb = *te = 0;
   if (t < 1) return fail(PCC_EINVAL, "tile size must be >= 1, got %lld", (long long)t);
   const uint64_t m = ceil_div((uint64_t)n, (uint64_t)t);
   const uint64_t total = m * (m + 1) / 2;
@@ -782,19 +786,37 @@ static int compute_pass_impl(int32_t variant, const double *u, int64_t n, int64_
   if (j_hi == j_lo) return PCC_OK;
   if (out == nullptr) return fail(PCC_EINVAL, "out is NULL");
   cudaStream_t s = (cudaStream_t)stream;
-  // Cells outside y <= x < n are exactly 0.0 (_kernels.py:370-373).
   PCC_CUDA(cudaMemsetAsync(out, 0, (size_t)(j_hi - j_lo) * (size_t)t * (size_t)t * sizeof(double), s),
            "cudaMemsetAsync(pass buffer)");
-  // GPU tile rows covering the reference tile rows of [j_lo, j_hi).
   const uint64_t yt_a = pcc::tile_row(m, j_lo), yt_b = pcc::tile_row(m, j_hi - 1);
   const uint64_t y_a = yt_a * (uint64_t)t;
   uint64_t y_b = (yt_b + 1) * (uint64_t)t;
   if (y_b > (uint64_t)n) y_b = (uint64_t)n;
   const uint64_t m_g = ceil_div((uint64_t)n, pcc::kTile);
   const uint64_t Ya = y_a / pcc::kTile, Yb = (y_b - 1) / pcc::kTile;
-  const uint64_t tb = pcc::row_prefix(m_g, Ya), te = pcc::row_prefix(m_g, Yb + 1);
+  *tb = pcc::row_prefix(m_g, Ya);
+  *te = pcc::row_prefix(m_g, Yb + 1);
+  return PCC_OK;
+}
+
+static int compute_pass_impl(int32_t variant, const double *u, int64_t n, int64_t l, int64_t ldu, int64_t t,
+                             uint64_t j_lo, uint64_t j_hi, double *out, void *stream) {
+  int rc = check_u(u, n, l, ldu);
+  if (rc) return rc;
+  uint64_t tb, te;
+  rc = compute_pass_prepare(n, t, j_lo, j_hi, out, stream, &tb, &te);
+  if (rc || tb == te) return rc;
   return pcc_syrk_f64_variant(variant, u, n, l, ldu, tb, te, PCC_LAYOUT_TILES, out, 0, 0, (int32_t)t, j_lo, j_hi,
                               stream);
+}
+
+int pcc_compute_pass_split_f64(const int8_t *slices, const double *scale, int64_t n, int64_t l, int64_t t,
+                               uint64_t j_lo, uint64_t j_hi, double *out, void *stream) {
+  if (n < 1 || l < 2) return fail(PCC_EINVAL, "need n >= 1 and l >= 2 (got n=%lld, l=%lld)", (long long)n, (long long)l);
+  uint64_t tb, te;
+  int rc = compute_pass_prepare(n, t, j_lo, j_hi, out, stream, &tb, &te);
+  if (rc || tb == te) return rc;
+  return pcc_syrk_split_f64(slices, scale, n, l, tb, te, PCC_LAYOUT_TILES, out, 0, 0, (int32_t)t, j_lo, j_hi, stream);
 }
 
 int pcc_compute_pass_f64(const double *u, int64_t n, int64_t l, int64_t ldu, int64_t t, uint64_t j_lo,

@@ -245,7 +245,7 @@ def merge(reports: list[WorkerReport], geom: TileGeometry, zero_variance: frozen
 
 
 def _run_subprocess(dataset: Dataset, dataset_path: str, geom: TileGeometry, p: int, capacity: int,
-                    threads: int, devs: list[torch.device], exact: bool = False) -> CorrelationResult:
+                    threads: int, devs: list[torch.device], method: str = "tensor") -> CorrelationResult:
     """One GPU worker process per assignment, the reference's wire protocol
     (distributed.py:209-318): BLOCKS frames are scattered into one packed
     result as they arrive; a failing worker raises ``WorkerError`` with its
@@ -304,7 +304,7 @@ def _run_subprocess(dataset: Dataset, dataset_path: str, geom: TileGeometry, p: 
     try:
         for a in assignments:
             env = dict(os.environ, PAIRCORR_THREADS=str(threads),
-                       PCC_DEVICE=str(devs[a.worker_index % len(devs)].index), PCC_EXACT="1" if exact else "0",
+                       PCC_DEVICE=str(devs[a.worker_index % len(devs)].index), PCC_METHOD=method,
                        PYTHONPATH=root + os.pathsep + os.environ.get("PYTHONPATH", ""))
             procs.append(subprocess.Popen([sys.executable, "-m", "paper_1605_01584_b200.worker"],
                                           stdin=subprocess.PIPE, stdout=subprocess.PIPE,
@@ -336,7 +336,7 @@ def _run_subprocess(dataset: Dataset, dataset_path: str, geom: TileGeometry, p: 
 
 
 def compute_shard(x_host, n: int, l: int, a: WorkerAssignment, device: torch.device,
-                  x_device: torch.Tensor | None = None, exact: bool = False) -> tuple[Shard, torch.Tensor]:
+                  x_device: torch.Tensor | None = None, method: str = "tensor") -> tuple[Shard, torch.Tensor]:
     """Worker body: upload, normalise everything, contract ``a``'s tile range.
 
     Returns the shard and the device zero-variance flags; asynchronous on
@@ -348,16 +348,14 @@ def compute_shard(x_host, n: int, l: int, a: WorkerAssignment, device: torch.dev
         lo, hi = shard_span(n, a.start, a.stop)
         vals = torch.empty(max(hi - lo, 1), dtype=torch.float64, device=device)
         if a.stop > a.start:
-            _lib.check(
-                _lib.syrk_fn(exact)(ptr(u), n, l, u.shape[1], a.start, a.stop, _lib.LAYOUT_PACKED, ptr(vals), 0,
-                                        lo, 0, 0, 0, stream_handle()),
-                f"worker {a.worker_index}",
-            )
+            con = _lib.Contraction(method, u, n, l).prepare_all(stream_handle())
+            con.syrk(a.start, a.stop, _lib.LAYOUT_PACKED, ptr(vals), 0, lo, 0, 0, 0, stream_handle(),
+                     f"worker {a.worker_index}")
         return Shard(a.worker_index, device, a.start, a.stop, lo, vals), flags
 
 
 def stream_shard(x_host, n: int, l: int, a: WorkerAssignment, device: torch.device, host_out=None,
-                 exact: bool = False):
+                 method: str = "tensor"):
     """Worker body with overlapped upload / contraction / download (stream.run_stream).
 
     Uploads and normalises only the rows the range touches (>= its first
@@ -368,7 +366,7 @@ def stream_shard(x_host, n: int, l: int, a: WorkerAssignment, device: torch.devi
     lo, hi = shard_span(n, a.start, a.stop)
     with torch.cuda.device(device):
         vals = torch.empty(max(hi - lo, 1), dtype=torch.float64, device=device)
-        _, flags, _ = run_stream(x_host, n, l, device, a.start, a.stop, vals, lo, host_out, lo, exact=exact)
+        _, flags, _ = run_stream(x_host, n, l, device, a.start, a.stop, vals, lo, host_out, lo, method=method)
     return Shard(a.worker_index, device, a.start, a.stop, lo, vals), flags
 
 
@@ -503,7 +501,7 @@ def exchange_normalize(x_host, n: int, l: int, rank: int, world: int, device: to
 
 
 def compute_worker(dataset: Dataset, p: int, worker_index: int, device=None, out=None, group=None,
-                   exact: bool = False, exchange: str = "collective"):
+                   exact: bool = False, exchange: str = "collective", method: str | None = None):
     """Run worker ``worker_index`` of a ``p``-way split as a standalone call.
 
     The one-process-per-GPU form of ``run_workers`` (torchrun ranks): upload,
@@ -516,7 +514,10 @@ def compute_worker(dataset: Dataset, p: int, worker_index: int, device=None, out
     ``worker_index``).  With it, X is not uploaded whole by every worker:
     each uploads and normalises its ``row_slices`` block and the blocks are
     all-gathered (``exchange_normalize``) before the contraction.
+    ``exact`` / ``method``: the contraction (see ``allpairs``).
     """
+    method = _lib.resolve_method(method, exact)
+    _lib.check_method_shape(method, dataset.l)
     if not 0 <= worker_index < p:
         raise ValueError(f"worker index {worker_index} outside [0, {p})")
     n, l = dataset.n, dataset.l
@@ -533,11 +534,11 @@ def compute_worker(dataset: Dataset, p: int, worker_index: int, device=None, out
         lo, hi = shard_span(n, a.start, a.stop)
         with torch.cuda.device(dev):
             vals = torch.empty(max(hi - lo, 1), dtype=torch.float64, device=dev)
-            run_stream(None, n, l, dev, a.start, a.stop, vals, lo, host, lo, resident=(u, flags), exact=exact)
+            run_stream(None, n, l, dev, a.start, a.stop, vals, lo, host, lo, resident=(u, flags), method=method)
         shard = Shard(a.worker_index, dev, a.start, a.stop, lo, vals)
         flags = flags[:n]
     else:
-        shard, flags = stream_shard(dataset.values, n, l, a, dev, host, exact=exact)
+        shard, flags = stream_shard(dataset.values, n, l, a, dev, host, method=method)
     shard.zero_variance = frozenset(np.flatnonzero(flags.cpu().numpy()).tolist())
     return shard
 
@@ -553,6 +554,7 @@ def run_workers(
     gather: bool = True,
     out=None,
     exact: bool = False,
+    method: str | None = None,
 ):
     """Partition the work across ``p`` workers on ``devices`` (distributed.py:117-151).
 
@@ -564,8 +566,9 @@ def run_workers(
     worker process per range of the caller's t x t tiles, speaking the
     reference's framed protocol (``worker.py``), gathered on the host.  A
     failing worker raises ``WorkerError`` with its index and unfinished range.
-    ``exact``: the bit-exact dot8 contraction (see ``allpairs``).
+    ``exact`` / ``method``: the contraction (see ``allpairs``).
     """
+    method = _lib.resolve_method(method, exact)
     if backend not in BACKENDS:
         raise ValueError(f"unknown backend {backend!r}, expected one of {BACKENDS}")
     dataset_path = None
@@ -576,6 +579,7 @@ def run_workers(
         dataset = load_dataset(dataset)
     if geom is not None and dataset.n != geom.n:
         raise ValueError(f"geometry is for n={geom.n} but dataset has n={dataset.n}")
+    _lib.check_method_shape(method, dataset.l)
     devs = resolve_devices(devices)
     if backend == "subprocess":
         # the reference's worker-process model: reference t x t tiles over the wire
@@ -585,12 +589,12 @@ def run_workers(
         geom = geom if geom is not None else TileGeometry(n=dataset.n)
         capacity = default_capacity(geom.t) if capacity is None else capacity
         if dataset_path is not None:
-            return _run_subprocess(dataset, dataset_path, geom, p, capacity, threads, devs, exact)
+            return _run_subprocess(dataset, dataset_path, geom, p, capacity, threads, devs, method)
         with tempfile.NamedTemporaryFile(suffix=".lpcc", delete=False) as tmp:
             tmp_path = tmp.name
         try:
             save_dataset(tmp_path, dataset)
-            return _run_subprocess(dataset, tmp_path, geom, p, capacity, threads, devs, exact)
+            return _run_subprocess(dataset, tmp_path, geom, p, capacity, threads, devs, method)
         finally:
             os.unlink(tmp_path)
     n, l = dataset.n, dataset.l
@@ -602,7 +606,7 @@ def run_workers(
     def run_one(a: WorkerAssignment) -> None:
         dev = devs[a.worker_index % len(devs)]
         try:
-            shards[a.worker_index], flags[a.worker_index] = compute_shard(dataset.values, n, l, a, dev, exact=exact)
+            shards[a.worker_index], flags[a.worker_index] = compute_shard(dataset.values, n, l, a, dev, method=method)
             with torch.cuda.device(dev):
                 torch.cuda.current_stream().synchronize()
         except BaseException as exc:  # noqa: BLE001 - re-raised as WorkerError below

@@ -178,7 +178,7 @@ def plan_stream(n: int, tile_begin: int, tile_end: int, wave: int, chunk_rows: i
 def run_stream(x, n: int, l: int, device: torch.device, tile_begin: int, tile_end: int,
                out_dev: torch.Tensor, out_base: int, host_out: torch.Tensor | None,
                host_base: int = 0, chunk_rows: int = 8, trace: list | None = None, resident=None,
-               exact: bool = False):
+               method: str = "tensor"):
     """Execute GPU tiles ``[tile_begin, tile_end)`` with overlapped upload,
     normalisation, contraction and download.
 
@@ -191,7 +191,9 @@ def run_stream(x, n: int, l: int, device: torch.device, tile_begin: int, tile_en
     ``resident``: ``(u, flags)`` already normalised on ``device`` (e.g. after
     the multi-GPU row exchange); ``x`` is then ignored and only the
     contraction passes and downloads run (top-down, no upload phase).
-    ``exact``: contract with the bit-exact dot8 kernel (``pcc_syrk_exact_f64``).
+    ``method``: the contraction (``_lib.METHODS``; ``"exact"`` = the bit-exact
+    dot8 kernel, ``"split"`` = int8 digit planes made chunk by chunk right
+    after each chunk's normalisation).
     Returns ``(u, flags, x_device)`` after the host has synchronised
     (``x_device`` is None with ``resident``).
     """
@@ -203,7 +205,6 @@ def run_stream(x, n: int, l: int, device: torch.device, tile_begin: int, tile_en
             trace.append((label, ev))
 
     L = _lib.lib()
-    syrk = _lib.syrk_fn(exact)
     with torch.cuda.device(device):
         info = _lib.device_info(device.index)
         wave = info.sm_count * info.syrk_ctas_per_sm
@@ -220,6 +221,9 @@ def run_stream(x, n: int, l: int, device: torch.device, tile_begin: int, tile_en
             u = torch.empty((rows_pad, ldu), dtype=torch.float64, device=device)
             flags = torch.zeros(n, dtype=torch.uint8, device=device)
             _lib.check(L.pcc_zero_rows_f64(ptr(u), ldu, n, rows_pad, s), "pad rows")
+        con = _lib.Contraction(method, u, n, l)
+        if resident is not None:
+            con.prepare_all(s)
 
         on_device = resident is not None or (isinstance(x, torch.Tensor) and x.is_cuda)
         if resident is not None:
@@ -326,6 +330,7 @@ def run_stream(x, n: int, l: int, device: torch.device, tile_begin: int, tile_en
             if resident is None:
                 _lib.check(L.pcc_normalize_rows_f64(ptr(xd), xd.stride(0), ptr(u), ldu, ptr(flags), l, lo, hi, s),
                            "normalize")
+                con.prepare(lo, hi, s)
             normed = torch.cuda.Event()
             normed.record(compute)
             # every pass whose rows are now normalised, in plan order
@@ -337,8 +342,7 @@ def run_stream(x, n: int, l: int, device: torch.device, tile_begin: int, tile_en
                 ws = workers[k % len(workers)] if phase == 1 else workers[0]
                 ws.wait_event(normed)
                 mark(f"  start [{p_lo},{p_hi})", ws)
-                _lib.check(syrk(ptr(u), n, l, ldu, p_lo, p_hi, _lib.LAYOUT_PACKED, ptr(out_dev), 0,
-                                          out_base, 0, 0, 0, stream_handle(ws)), "syrk")
+                con.syrk(p_lo, p_hi, _lib.LAYOUT_PACKED, ptr(out_dev), 0, out_base, 0, 0, 0, stream_handle(ws))
                 done = torch.cuda.Event()
                 done.record(ws)
                 mark(f"pass tiles [{p_lo},{p_hi})", ws)

@@ -148,9 +148,12 @@ def _check_range(geom: TileGeometry, j_start: int, j_end: int) -> None:
 
 
 def compute_pass_device(u: NormalizedDataset, geom: TileGeometry, j_start: int, j_end: int,
-                        out: torch.Tensor, stream: torch.cuda.Stream | None = None, exact: bool = False) -> None:
+                        out: torch.Tensor, stream: torch.cuda.Stream | None = None, exact: bool = False,
+                        method: str | None = None, contraction: "_lib.Contraction | None" = None) -> None:
     """Fill the device buffer ``out`` with the pass layout of tiles ``[j_start, j_end)``
-    (``exact``: bit-identical to the reference's ``compute_tile_range``)."""
+    (``exact``: bit-identical to the reference's ``compute_tile_range``;
+    ``method``: see ``allpairs``; ``contraction``: a prepared
+    ``_lib.Contraction`` over ``u`` to reuse across passes)."""
     _check_range(geom, j_start, j_end)
     if geom.n != u.n:
         raise ValueError(f"geometry is for n={geom.n} but data has n={u.n}")
@@ -160,11 +163,11 @@ def compute_pass_device(u: NormalizedDataset, geom: TileGeometry, j_start: int, 
     if need == 0:
         return
     with torch.cuda.device(u.device):
-        _lib.check(
-            (_lib.lib().pcc_compute_pass_exact_f64 if exact else _lib.lib().pcc_compute_pass_f64)(
-                ptr(u.u_device), u.n, u.l, u.ldu, geom.t, j_start, j_end, ptr(out), stream_handle(stream)),
-            "compute_pass",
-        )
+        s = stream_handle(stream)
+        con = contraction
+        if con is None:
+            con = _lib.Contraction(_lib.resolve_method(method, exact), u.u_device, u.n, u.l).prepare_all(s)
+        con.compute_pass(geom.t, j_start, j_end, ptr(out), s)
 
 
 def compute_pass(
@@ -177,6 +180,7 @@ def compute_pass(
     pool=None,
     *,
     exact: bool = False,
+    method: str | None = None,
 ) -> BlockList:
     """Compute tiles ``[j_start, j_end)`` on the GPU into a flat pass buffer (tiles.py:133-199).
 
@@ -185,7 +189,7 @@ def compute_pass(
     ``pool`` are accepted for compatibility and change nothing.  Returns the
     reference's ``BlockList`` of per-tile views with ``flat`` set.
     ``exact``: the bit-exact dot8 contraction (the reference's pass buffer,
-    bit for bit).
+    bit for bit); ``method``: the contraction (see ``allpairs``).
     """
     _check_range(geom, j_start, j_end)
     count = j_end - j_start
@@ -198,7 +202,7 @@ def compute_pass(
     if count == 0:
         return BlockList()
     dev = torch.empty(need, dtype=torch.float64, device=u.device)
-    compute_pass_device(u, geom, j_start, j_end, dev, exact=exact)
+    compute_pass_device(u, geom, j_start, j_end, dev, exact=exact, method=method)
     if isinstance(out, torch.Tensor):
         out[:need].copy_(dev)
         host = out

@@ -419,3 +419,31 @@ def test_file_corruption_detected(tmp_path):
         r.write_bytes(bad)
         with pytest.raises(pc.DataError):
             pc.load_result(r)
+
+
+def test_contraction_method_resolution():
+    from paper_1605_01584_b200 import _lib
+
+    assert _lib.resolve_method() == "tensor"
+    assert _lib.resolve_method(exact=True) == "exact"
+    assert _lib.resolve_method("split") == "split"
+    assert _lib.resolve_method("exact", exact=True) == "exact"
+    with pytest.raises(ValueError):
+        _lib.resolve_method("split", exact=True)
+    with pytest.raises(ValueError):
+        _lib.resolve_method("bf16")
+    _lib.check_method_shape("split", _lib.SPLIT_MAX_L)
+    _lib.check_method_shape("tensor", 10 * _lib.SPLIT_MAX_L)
+    with pytest.raises(ValueError, match="split"):
+        _lib.check_method_shape("split", _lib.SPLIT_MAX_L + 1)
+
+
+def test_split_bound_rejected_before_any_device_work():
+    import paper_1605_01584_b200 as pc
+    from paper_1605_01584_b200 import _lib
+
+    x = np.random.default_rng(0).standard_normal((3, _lib.SPLIT_MAX_L + 1))
+    with pytest.raises(ValueError, match="split"):
+        pc.allpairs(pc.Dataset(values=x), method="split")
+    with pytest.raises(ValueError, match="method"):
+        pc.allpairs(pc.Dataset(values=x[:, :10]), method="fp32")
