@@ -425,7 +425,10 @@ def run_b200(args, rank: int, world: int, local_rank: int) -> None:
         sp_ms = max_over_ranks(t0.elapsed_time(t1) / sp_steps)
         sp_rows_ms = max_over_ranks(sum(a.elapsed_time(b) for a, b, _ in evs) / sp_steps)
         sp_syrk_ms = max_over_ranks(sum(b.elapsed_time(c) for _, b, c in evs) / sp_steps)
-        i8_ops = 68.0 * l * my_cells  # algorithmic: 34 int8 digit products x 2 l ops per owned pair
+        # algorithmic: 2 l ops per owned pair for each int8 digit product the
+        # tile pair needs (34, or 28 where its rows allow the adaptive depth)
+        products = _lib.split_products(sp_state["con"].scale, n, l, tb, te)
+        i8_ops = 2.0 * l * my_cells * products / (te - tb)
         i8_peak = I8_PEAK_TOPS
         i8_ach = i8_ops / (sp_syrk_ms * 1e-3) / 1e12
         diff = float((shard_s[:max(1, span_hi - span_lo)] - shard[:max(1, span_hi - span_lo)]).abs().max())
@@ -436,12 +439,14 @@ def run_b200(args, rank: int, world: int, local_rank: int) -> None:
                     "(tests/test_gpu_split.py); FP64-accurate, not a reduced-precision result",
             "value": total_pairs / (sp_ms * 1e-3), "unit": "pairs/s", "ms_per_step": sp_ms, "steps": sp_steps,
             "split_rows_ms": sp_rows_ms, "syrk_ms": sp_syrk_ms,
+            "products_per_tile": products / (te - tb),
             "fp64_equivalent_tflops": flops_launch / (sp_syrk_ms * 1e-3) / 1e12,
             "max_abs_diff_vs_fp64_tensor_path": diff,
             "roofline": {"bound": "tensor", "achieved": i8_ach, "peak": i8_peak, "unit": "TOP/s",
                          "frac": i8_ach / i8_peak,
                          "kernel": "syrk_split_kernel<packed> (TMA 3-D boxes of 7 digit planes, tcgen05.mma "
-                                   "kind::i8 M128 N128 K32, 4 s32 accumulators in TMEM, 2 K passes per tile)",
+                                   "kind::i8 M128 N128 K32, 4 s32 accumulators in TMEM, 2 K passes per tile, "
+                                   "adaptive depth 34/28 products)",
                          "algorithmic_ops_per_launch": i8_ops,
                          "peak_source": "measured int8 tcgen05.mma throughput on this pool's B200 "
                                         "(tools/i8_mma.cu, profiles/r01_i8_mma_peak.log: 128x256x32 shape; "
@@ -481,6 +486,9 @@ def run_b200(args, rank: int, world: int, local_rank: int) -> None:
         r = api_call()
         wall.append(time.perf_counter() - a)
     e2e_s = max_over_ranks(statistics.median(wall))
+    if world == 1:
+        # sanity: the API result matches the device-timed shard bit for bit
+        assert np.array_equal(r.packed.numpy()[:1000], shard[:1000].cpu().numpy())
     if split_mode is not None:
         # the same public call with method="split"
         if world == 1:
@@ -503,9 +511,6 @@ def run_b200(args, rank: int, world: int, local_rank: int) -> None:
                              "steps": e2e_steps, "h2d_bytes_per_step": n * l * 8, "d2h_bytes_per_step": total_pairs * 8}
     h2d = n * l * 8  # world == 1: all of X; N > 1: one row block of X per rank
     d2h = total_pairs * 8
-    if world == 1:
-        # sanity: the API result matches the device-timed shard bit for bit
-        assert np.array_equal(r.packed.numpy()[:1000], shard[:1000].cpu().numpy())
 
     # ---- the reference's calling convention: plain numpy in, numpy result
     # allocated by the call (pageable memory, staged through pinned slots)

@@ -196,6 +196,7 @@ def syrk_fn(exact: bool = False):
 #   "exact"  -- the reference's dot8 arithmetic on the FP64 CUDA cores, bit-identical.
 METHODS = ("tensor", "split", "exact")
 SPLIT_MAX_L = 8192
+SPLIT_ROW_BYTES = 64  # digit-plane layout int8 [ceil(l/64)][7][rows][64] (split.cuh)
 
 
 def resolve_method(method: str | None = None, exact: bool = False) -> str:
@@ -214,6 +215,24 @@ def check_method_shape(method: str, l: int) -> None:
     if method == "split" and l > SPLIT_MAX_L:
         raise ValueError(f"method='split' is bounded to l <= {SPLIT_MAX_L} samples (its 1e-12 error bound); "
                          f"got l={l}: use method='tensor'")
+
+
+def split_products(scale, n: int, l: int, tile_begin: int, tile_end: int) -> int:
+    """int8 products (tcgen05.mma of 128 x 128 x 32 per K step) the split
+    contraction issues per K step summed over GPU tiles [tile_begin,
+    tile_end): 34 per tile, 28 where the tile pair's rows allow dropping the
+    sd = 7 diagonal (split.cuh ``split_drop_top``, same arithmetic)."""
+    import numpy as np
+
+    s = np.asarray(scale.cpu() if hasattr(scale, "cpu") else scale, dtype=np.float64)
+    mg = -(-n // GPU_TILE)
+    tmax = s[:mg * GPU_TILE].reshape(mg, GPU_TILE).max(axis=1)
+    iy, ix = np.triu_indices(mg)  # row-major upper triangle = the bijection's id order
+    iy, ix = iy[tile_begin:tile_end], ix[tile_begin:tile_end]
+    sy, sx = tmax[iy], tmax[ix]
+    bound = sy * sx * float(l) * (6.04 * 2.0 ** -37) + (sy + sx) * 2.0 ** -43 * np.sqrt(float(l))
+    drop = bound <= 5e-13
+    return int(34 * drop.size - 6 * int(drop.sum()))
 
 
 class Contraction:

@@ -164,12 +164,13 @@ int encode_umap(const double *u, int64_t ldu, int64_t rows, CUtensorMap *map, in
 int encode_slice_map(const int8_t *slices, int64_t rows, int64_t k_blocks, int box_slices, CUtensorMap *map) {
   EncodeTiledFn fn = encode_fn();
   if (fn == nullptr) return PCC_ECUDA;
-  const cuuint64_t dims[3] = {32, (cuuint64_t)rows, (cuuint64_t)(pcc::SplitCfg::kSlices * k_blocks)};
-  const cuuint64_t strides[2] = {32, (cuuint64_t)rows * 32};
-  const cuuint32_t box[3] = {32, (cuuint32_t)pcc::kTile, (cuuint32_t)box_slices};
+  constexpr int W = pcc::SplitCfg::kRowBytes;
+  const cuuint64_t dims[3] = {W, (cuuint64_t)rows, (cuuint64_t)(pcc::SplitCfg::kSlices * k_blocks)};
+  const cuuint64_t strides[2] = {W, (cuuint64_t)rows * W};
+  const cuuint32_t box[3] = {W, (cuuint32_t)pcc::kTile, (cuuint32_t)box_slices};
   const cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t *>(slices), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(PCC_ECUDA, "cuTensorMapEncodeTiled(slices) failed (CUresult %d)", (int)r);
   return PCC_OK;
@@ -379,6 +380,11 @@ int launch_exact(const double *u, int64_t n, int64_t l, int64_t ldu, uint64_t tb
   return PCC_OK;
 }
 
+static const int split_dbg = [] {  // experiment knob: 1 = no TMA loads, 2 = no MMAs (wrong results)
+  const char *e = getenv("PCC_SPLIT_DEBUG");
+  return e ? atoi(e) : 0;
+}();
+
 template <int LAYOUT>
 int launch_split(const int8_t *slices, const double *scale, int64_t n, int64_t l, uint64_t tb, uint64_t te,
                  const pcc::Epilogue &ep, cudaStream_t stream) {
@@ -387,7 +393,7 @@ int launch_split(const int8_t *slices, const double *scale, int64_t n, int64_t l
   const DeviceConfig *dc = nullptr;
   int rc = device_config(&dc);
   if (rc) return rc;
-  const int64_t rows = pcc_rows_padded(n), k_blocks = (int64_t)ceil_div((uint64_t)l, (uint64_t)C::kKStep);
+  const int64_t rows = pcc_rows_padded(n), k_blocks = (int64_t)ceil_div((uint64_t)l, (uint64_t)C::kRowBytes);
   CUtensorMap map7, map4;
   rc = encode_slice_map(slices, rows, k_blocks, 7, &map7);
   if (rc == PCC_OK) rc = encode_slice_map(slices, rows, k_blocks, 4, &map4);
@@ -399,8 +405,8 @@ int launch_split(const int8_t *slices, const double *scale, int64_t n, int64_t l
   uint32_t group = 1;
   while ((uint64_t)(group + 1) * (group + 1) <= grid) ++group;
   const pcc::TileOrder order = pcc::make_tile_order(m_g, tb, te, group);
-  pcc::syrk_split_kernel<LAYOUT><<<grid, C::kThreads, C::kSmemBytes, stream>>>(map7, map4, scale, n, (int)k_blocks,
-                                                                               m_g, order, ep);
+  pcc::syrk_split_kernel<LAYOUT><<<grid, C::kThreads, C::kSmemBytes, stream>>>(map7, map4, scale, n, l,
+                                                                               (int)k_blocks, m_g, order, ep, split_dbg);
   PCC_CUDA(cudaGetLastError(), "syrk_split_kernel launch");
   return PCC_OK;
 }
@@ -711,7 +717,8 @@ int pcc_syrk_exact_f64(const double *u, int64_t n, int64_t l, int64_t ldu, uint6
 
 uint64_t pcc_split_slice_bytes(int64_t n, int64_t l) {
   if (n < 1 || l < 1) return 0;
-  return (uint64_t)pcc::SplitCfg::kSlices * (uint64_t)pcc_rows_padded(n) * ceil_div((uint64_t)l, 32) * 32;
+  return (uint64_t)pcc::SplitCfg::kSlices * (uint64_t)pcc_rows_padded(n) *
+         ceil_div((uint64_t)l, (uint64_t)pcc::SplitCfg::kRowBytes) * pcc::SplitCfg::kRowBytes;
 }
 
 int pcc_split_rows_f64(const double *u, int64_t n, int64_t l, int64_t ldu, int64_t row_lo, int64_t row_hi,

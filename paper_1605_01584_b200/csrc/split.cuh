@@ -39,18 +39,48 @@ namespace pcc {
 
 struct SplitCfg {
   static constexpr int kSlices = 7;
-  static constexpr int kKStep = 32;                      // int8 K per stage = one MMA
-  static constexpr int kSliceBytes = kTile * kKStep;     // 4 KB: one 128-row operand tile
-  static constexpr int kOpBytes = kSlices * kSliceBytes; // 28 KB
+  static constexpr int kKStep = 32;                      // int8 K of one MMA
+  static constexpr int kRowBytes = 64;                   // int8 K per staged row = per stage (2 MMA K steps)
+  static constexpr int kKSub = kRowBytes / kKStep;
+  static constexpr int kSliceBytes = kTile * kRowBytes;  // 8 KB: one 128-row operand tile of a stage
+  static constexpr int kOpBytes = kSlices * kSliceBytes; // 56 KB
   static constexpr int kStageBytes = 2 * kOpBytes;       // A + B
-  static constexpr int kStages = 3;
+  static constexpr int kStages = 2;
   static constexpr int kEpiWarps = 8;
   static constexpr int kThreads = 32 * (2 + kEpiWarps);
   static constexpr uint32_t kTmemCols = 512;
   static constexpr int kBarBytes = 8 * (2 * kStages + 2) + 16;
   static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + kBarBytes;
   static constexpr int64_t kMaxL = 8192;  // the error bound above holds up to here
+  // Adaptive depth: a tile pair skips diagonal d = 9 (0-based sd = 7: 6 of
+  // the 34 products) when its own rows bound the resulting error by
+  // kDropBudget (split_drop_top below).
+  static constexpr double kDropBudget = 5e-13;
 };
+
+// Whole warp, same result in every lane: may tile pair (Y, X) drop the sd = 7
+// products?  With s = the tile's largest row scale (scale_r = 2^(e_r-7),
+// |digits| <= 64 past the first), the dropped products sd >= 7 add at most
+//     s_Y s_X l 64^2 (6 + 5/128 + ...) 128^-7  <=  s_Y s_X l 6.04 2^-37
+// per coefficient, and the 7-digit representation (|rho| <= s 2^-43,
+// ||u||_1 <= sqrt(l)) at most (s_Y + s_X) 2^-43 sqrt(l); drop when their sum
+// is <= kDropBudget.  Rows that are all zero (and pad rows) have scale 0.
+__device__ __forceinline__ bool split_drop_top(const double *__restrict__ scale, uint64_t Y, uint64_t X, int lane,
+                                               double l_f, double sqrt_l) {
+  double sy = 0.0, sx = 0.0;
+#pragma unroll
+  for (int r = lane; r < kTile; r += 32) {
+    sy = fmax(sy, __ldg(scale + Y * kTile + r));
+    sx = fmax(sx, __ldg(scale + X * kTile + r));
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    sy = fmax(sy, __shfl_xor_sync(0xffffffffu, sy, o));
+    sx = fmax(sx, __shfl_xor_sync(0xffffffffu, sx, o));
+  }
+  const double bound = sy * sx * l_f * (6.04 * 0x1p-37) + (sy + sx) * 0x1p-43 * sqrt_l;
+  return bound <= SplitCfg::kDropBudget;
+}
 
 __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap *map, int32_t c0, int32_t c1,
                                             int32_t c2, uint32_t bar) {
@@ -80,12 +110,13 @@ __global__ void __launch_bounds__(256) split_rows_kernel(const double *__restric
     frexp(m, &e);                                // m = f·2^e, f in [0.5, 1)
     if (ldexp(m, 7 - e) >= 127.5) ++e;           // keep the leading digit within [-127, 127]
   }
-  if (lane == 0) scale[r] = ldexp(1.0, e - 7);
-  const int64_t kb_count = (l + 31) / 32;
-  const int64_t plane = rows_total * 32;         // bytes between slice planes
-  for (int64_t k0 = 0; k0 < kb_count * 32; k0 += 128) {
+  if (lane == 0) scale[r] = m > 0.0 ? ldexp(1.0, e - 7) : 0.0;  // all-zero rows: 0 (digits are 0 too)
+  constexpr int W = SplitCfg::kRowBytes;
+  const int64_t kb_count = (l + W - 1) / W;
+  const int64_t plane = rows_total * W;          // bytes between slice planes
+  for (int64_t k0 = 0; k0 < kb_count * W; k0 += 128) {
     const int64_t k = k0 + 4 * lane;
-    if (k >= kb_count * 32) break;
+    if (k >= kb_count * W) break;
     uint32_t packed[SplitCfg::kSlices] = {};
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -97,8 +128,8 @@ __global__ void __launch_bounds__(256) split_rows_kernel(const double *__restric
         packed[i] |= ((uint32_t)(int32_t)d & 0xFFu) << (8 * j);
       }
     }
-    const int64_t kb = k >> 5;
-    int8_t *dst = slices + (kb * SplitCfg::kSlices) * plane + r * 32 + (k & 31);
+    const int64_t kb = k / W;
+    int8_t *dst = slices + (kb * SplitCfg::kSlices) * plane + r * W + (k % W);
 #pragma unroll
     for (int i = 0; i < SplitCfg::kSlices; ++i) *reinterpret_cast<uint32_t *>(dst + i * plane) = packed[i];
   }
@@ -108,8 +139,8 @@ __global__ void __launch_bounds__(256) split_rows_kernel(const double *__restric
 template <int LAYOUT>
 __global__ void __launch_bounds__(SplitCfg::kThreads, 1)
     syrk_split_kernel(const __grid_constant__ CUtensorMap map7, const __grid_constant__ CUtensorMap map4,
-                      const double *__restrict__ scale, int64_t n, int k_blocks, uint64_t m_g, TileOrder order,
-                      Epilogue ep) {
+                      const double *__restrict__ scale, int64_t n, int64_t l, int k_blocks, uint64_t m_g,
+                      TileOrder order, Epilogue ep, int dbg) {
   using C = SplitCfg;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -138,6 +169,7 @@ __global__ void __launch_bounds__(SplitCfg::kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot_ptr;
   const uint64_t count = order.total;
+  const double l_f = (double)l, sqrt_l = sqrt((double)l);
 
   if (warp == 0) {
     // ---------------- TMA producer ----------------
@@ -152,10 +184,14 @@ __global__ void __launch_bounds__(SplitCfg::kThreads, 1)
           const uint32_t bytes = 2u * (pass == 0 ? 7u : 4u) * C::kSliceBytes;
           for (int kb = 0; kb < k_blocks; ++kb) {
             mbar_wait(empty_bar(stage), phase ^ 1);
+            if (dbg == 1) {
+              mbar_arrive(full_bar(stage));
+            } else {
             mbar_arrive_expect_tx(full_bar(stage), bytes);
             const uint32_t a = ring + stage * C::kStageBytes;
             tma_load_3d(a, map, 0, (int32_t)(Y * kTile), kb * C::kSlices, full_bar(stage));
             tma_load_3d(a + C::kOpBytes, map, 0, (int32_t)(X * kTile), kb * C::kSlices, full_bar(stage));
+            }
             if (++stage == C::kStages) stage = 0, phase ^= 1;
           }
         }
@@ -163,12 +199,15 @@ __global__ void __launch_bounds__(SplitCfg::kThreads, 1)
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
-    if (lane == 0) {
-      constexpr uint32_t idesc = idesc_i8_s32<128, 128>();
-      const uint64_t desc0 = umma_desc_k_sw32(0);
-      int stage = 0;
-      uint32_t phase = 0, use = 0;
-      for (uint64_t s = blockIdx.x; s < count; s += gridDim.x) {
+    constexpr uint32_t idesc = idesc_i8_s32<128, 128>();
+    const uint64_t desc0 = umma_desc_k_sw64(0);
+    int stage = 0;
+    uint32_t phase = 0, use = 0;
+    for (uint64_t s = blockIdx.x; s < count; s += gridDim.x) {
+      uint64_t Y, X;
+      tile_at(order, m_g, s, Y, X);
+      const int q_top = split_drop_top(scale, Y, X, lane, l_f, sqrt_l) ? 2 : 3;
+      if (lane == 0) {
         for (int pass = 0; pass < 2; ++pass, ++use) {
           mbar_wait(tempty, (use & 1) ^ 1);  // the epilogue has drained the accumulators
           tc_fence_after();
@@ -179,12 +218,17 @@ __global__ void __launch_bounds__(SplitCfg::kThreads, 1)
             const uint32_t a = ring + stage * C::kStageBytes, b = a + C::kOpBytes;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
+              if (pass == 0 && q > q_top) continue;  // adaptive depth: sd = 7 dropped
               const int sd = s_lo + q;
               const int i_lo = sd > 6 ? sd - 6 : 0, i_hi = sd < 6 ? sd : 6;
               for (int i = i_lo; i <= i_hi; ++i) {
-                const uint64_t da = desc0 + ((a + i * C::kSliceBytes) >> 4);
-                const uint64_t db = desc0 + ((b + (sd - i) * C::kSliceBytes) >> 4);
-                umma_i8(tmem + 128u * q, da, db, idesc, (kb > 0 || i > i_lo) ? 1u : 0u);
+#pragma unroll
+                for (int ks = 0; ks < C::kKSub; ++ks) {  // K step within the 64-byte swizzled rows: +32 B
+                  const uint64_t da = desc0 + ((a + i * C::kSliceBytes + ks * C::kKStep) >> 4);
+                  const uint64_t db = desc0 + ((b + (sd - i) * C::kSliceBytes + ks * C::kKStep) >> 4);
+                  if (dbg != 2)
+                    umma_i8(tmem + 128u * q, da, db, idesc, (kb > 0 || ks > 0 || i > i_lo) ? 1u : 0u);
+                }
               }
             }
             umma_commit(empty_bar(stage));  // the slot is free once these MMAs have read it
@@ -192,7 +236,10 @@ __global__ void __launch_bounds__(SplitCfg::kThreads, 1)
           }
           umma_commit(tfull);
         }
+      } else {
+        use += 2;
       }
+      __syncwarp();
     }
   } else {
     // ---------------- epilogue ----------------
@@ -204,6 +251,7 @@ __global__ void __launch_bounds__(SplitCfg::kThreads, 1)
     for (uint64_t s = blockIdx.x; s < count; s += gridDim.x) {
       uint64_t Y, X;
       tile_at(order, m_g, s, Y, X);
+      const int q_top = split_drop_top(scale, Y, X, lane, l_f, sqrt_l) ? 2 : 3;
       double t[64];
 #pragma unroll
       for (int pass = 0; pass < 2; ++pass, ++use) {
@@ -213,12 +261,13 @@ __global__ void __launch_bounds__(SplitCfg::kThreads, 1)
         for (int c = 0; c < 4; ++c) {
 #pragma unroll
           for (int q = 3; q >= 0; --q) {
+            if (pass == 0 && q > q_top) continue;
             int32_t v[16];
             tmem_ld16(tmem + lane_base + 128u * q + (uint32_t)(64 * half + 16 * c), v);
             tmem_ld_wait();
 #pragma unroll
             for (int j = 0; j < 16; ++j)
-              t[16 * c + j] = (pass == 0 && q == 3) ? (double)v[j] : fma(t[16 * c + j], 0.0078125, (double)v[j]);
+              t[16 * c + j] = (pass == 0 && q == q_top) ? (double)v[j] : fma(t[16 * c + j], 0.0078125, (double)v[j]);
           }
         }
         tc_fence_before();

@@ -30,6 +30,20 @@ __device__ __forceinline__ uint64_t umma_desc_k_sw32(uint32_t smem_addr) {
   return d;
 }
 
+// K-major, 64-byte swizzle: rows of 64 bytes (two int8 MMA K steps), 8-row
+// atoms of 512 B packed back to back (SBO = 512 B) -- what a TMA box
+// {64 B, rows} with CU_TENSOR_MAP_SWIZZLE_64B writes; the second K step of a
+// row starts 32 B further (the swizzle is a function of the address bits).
+__device__ __forceinline__ uint64_t umma_desc_k_sw64(uint32_t smem_addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;                    // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(512 >> 4) << 32;           // SBO: 8-row atom stride
+  d |= (uint64_t)1 << 46;                    // descriptor version (sm_100)
+  d |= (uint64_t)4 << 61;                    // SWIZZLE_64B
+  return d;
+}
+
 template <int M, int N>
 __host__ __device__ constexpr uint32_t idesc_i8_s32() {
   return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);

@@ -84,12 +84,15 @@ def test_digit_planes_are_an_exact_expansion(rng):
     con = _lib.Contraction("split", u, n, l).prepare_all(torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     rows = u.shape[0]
-    kb = -(-l // 32)
-    d = con.slices.cpu().numpy().view(np.int8).reshape(kb, 7, rows, 32)
-    d = d.transpose(2, 0, 3, 1).reshape(rows, kb * 32, 7).astype(np.float64)  # [row][k][digit]
+    W = _lib.SPLIT_ROW_BYTES
+    kb = -(-l // W)
+    d = con.slices.cpu().numpy().view(np.int8).reshape(kb, 7, rows, W)
+    d = d.transpose(2, 0, 3, 1).reshape(rows, kb * W, 7).astype(np.float64)  # [row][k][digit]
     assert np.abs(d[:, :, 0]).max() <= 127 and np.abs(d[:, :, 1:]).max() <= 64
     scale = con.scale.cpu().numpy()
-    m, e = np.frexp(scale)
+    zero_rows = ~np.any(d != 0, axis=(1, 2))
+    assert zero_rows[n:].all() and (scale[zero_rows] == 0.0).all(), "all-zero rows have scale 0"
+    m, e = np.frexp(scale[~zero_rows])
     assert (m == 0.5).all(), "scales are powers of two"
     w = 128.0 ** -np.arange(7)
     recon = (d @ w) * scale[:, None]

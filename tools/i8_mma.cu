@@ -71,7 +71,7 @@ __global__ void check_kernel(const int8_t *a, const int8_t *b, int steps, int32_
 }
 
 template <int N>
-__global__ void peak_kernel(const int8_t *src, int iters, int32_t *sink) {
+__global__ void peak_kernel(const int8_t *src, int iters, int32_t *sink, long long *cycles, int zero) {
   constexpr int kAcc = 512 / N;  // accumulators that fit in TMEM
   extern __shared__ __align__(1024) int8_t sm[];
   __shared__ __align__(8) uint64_t bar;
@@ -79,7 +79,8 @@ __global__ void peak_kernel(const int8_t *src, int iters, int32_t *sink) {
   int8_t *sa = (int8_t *)(((uintptr_t)sm + 1023) & ~(uintptr_t)1023);  // 7 x 128 x 32
   int8_t *sb = sa + 7 * 128 * 32;                                      // 7 x N x 32
   const int tid = threadIdx.x, warp = tid >> 5;
-  for (int i = tid; i < 7 * (128 + N) * 32; i += blockDim.x) sa[i] = src[(blockIdx.x * 977 + i) & ((1 << 20) - 1)];
+  for (int i = tid; i < 7 * (128 + N) * 32; i += blockDim.x)
+    sa[i] = zero ? (int8_t)0 : src[(blockIdx.x * 977 + i) & ((1 << 20) - 1)];
   if (warp == 0) tmem_alloc(smem_u32(&tmem_base), 512);
   if (tid == 0) mbar_init(smem_u32(&bar), 1), mbar_fence_init();
   fence_async_smem();
@@ -87,6 +88,7 @@ __global__ void peak_kernel(const int8_t *src, int iters, int32_t *sink) {
   __syncthreads();
   tc_fence_after();
   const uint32_t tm = tmem_base;
+  long long c0 = clock64();
   if (tid == 0) {
     const uint32_t a0 = smem_u32(sa), b0 = smem_u32(sb);
     for (int it = 0; it < iters; ++it) {
@@ -101,6 +103,7 @@ __global__ void peak_kernel(const int8_t *src, int iters, int32_t *sink) {
     umma_commit(smem_u32(&bar));
   }
   mbar_wait(smem_u32(&bar), 0);
+  if (tid == 0 && cycles) cycles[blockIdx.x] = clock64() - c0;
   tc_fence_after();
   int32_t v[16];
   tmem_ld16(tm + ((uint32_t)(warp * 32) << 16), v);
@@ -112,25 +115,32 @@ __global__ void peak_kernel(const int8_t *src, int iters, int32_t *sink) {
 }
 
 template <int N>
-void run_peak(const int8_t *src, int32_t *sink, int sms) {
+void run_peak(const int8_t *src, int32_t *sink, int sms, int zero) {
   const size_t smem = 1024 + 7 * (128 + N) * 32;
   CK(cudaFuncSetAttribute(peak_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int iters = 20000;
-  peak_kernel<N><<<sms, 128, smem>>>(src, 100, sink);
+  long long *cyc;
+  CK(cudaMalloc(&cyc, sms * sizeof(long long)));
+  peak_kernel<N><<<sms, 128, smem>>>(src, 100, sink, nullptr, zero);
   CK(cudaDeviceSynchronize());
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0), cudaEventCreate(&e1);
   for (int rep = 0; rep < 3; ++rep) {
     cudaEventRecord(e0);
-    peak_kernel<N><<<sms, 128, smem>>>(src, iters, sink);
+    peak_kernel<N><<<sms, 128, smem>>>(src, iters, sink, cyc, zero);
     cudaEventRecord(e1);
     CK(cudaEventSynchronize(e1));
     float ms;
     cudaEventElapsedTime(&ms, e0, e1);
+    std::vector<long long> c(sms);
+    CK(cudaMemcpy(c.data(), cyc, sms * sizeof(long long), cudaMemcpyDeviceToHost));
+    long long cmax = 0;
+    for (auto v : c) cmax = v > cmax ? v : cmax;
     const double ops = 2.0 * 128 * N * 32 * 34.0 * iters * sms;  // 34 MMAs per iteration (i + j <= 7, i, j < 7)
-    printf("M=128 N=%3d K=32 s8*s8->s32: %.3f ms  %.1f TOPS  (%.0f clk per MMA per SM at 1.965 GHz)\n", N, ms,
-           ops / ms / 1e9, ms * 1e-3 * 1.965e9 / (34.0 * iters));
+    printf("M=128 N=%3d K=32 s8*s8->s32 %s: %.3f ms  %.1f TOPS  %.1f SM clk per MMA (clock64), avg clock %.0f MHz\n",
+           N, zero ? "zeros " : "random", ms, ops / ms / 1e9, (double)cmax / (34.0 * iters), cmax / (ms * 1e3));
   }
+  CK(cudaFree(cyc));
 }
 
 int main() {
@@ -174,8 +184,10 @@ int main() {
   CK(cudaMalloc(&src, r.size()));
   CK(cudaMalloc(&sink, 4096));
   CK(cudaMemcpy(src, r.data(), r.size(), cudaMemcpyHostToDevice));
-  run_peak<64>(src, sink, p.multiProcessorCount);
-  run_peak<128>(src, sink, p.multiProcessorCount);
-  run_peak<256>(src, sink, p.multiProcessorCount);
+  for (int zero = 0; zero < 2; ++zero) {
+    run_peak<64>(src, sink, p.multiProcessorCount, zero);
+    run_peak<128>(src, sink, p.multiProcessorCount, zero);
+    run_peak<256>(src, sink, p.multiProcessorCount, zero);
+  }
   return bad_total ? 1 : 0;
 }

@@ -18,6 +18,7 @@ p = argparse.ArgumentParser()
 p.add_argument("--config", default="c1")
 p.add_argument("--reps", type=int, default=3)
 p.add_argument("--skip-dmma", action="store_true")
+p.add_argument("--sustain", type=int, default=0, help="also time N back-to-back split launches with clock sampling")
 a = p.parse_args()
 L = _lib.lib()
 x = torch.from_numpy(make_config(a.config)).cuda()
@@ -53,6 +54,8 @@ t_split = timed(lambda: _lib.check(L.pcc_syrk_split_f64(slices.data_ptr(), scale
                                                         _lib.LAYOUT_PACKED, out_s.data_ptr(), 0, 0, 0, 0, 0, s0),
                                    "syrk_split"))
 flops = float(n) * n * l
+prod = _lib.split_products(scale, n, l, 0, tiles)
+print(f"{a.config}: products per tile {prod / tiles:.2f} (34 = full depth, 28 = adaptive depth everywhere)")
 print(f"{a.config}: n={n} l={l}  split_rows {t_split_rows:.3f} ms  split syrk {t_split:.3f} ms "
       f"({flops / t_split / 1e9:.1f} TFLOP/s-equivalent n^2 l/t)", flush=True)
 if not a.skip_dmma:
@@ -62,3 +65,19 @@ if not a.skip_dmma:
     print(f"  dmma syrk {t_d:.3f} ms ({flops / t_d / 1e9:.1f} TFLOP/s)  speed-up {t_d / t_split:.2f}x", flush=True)
     print(f"  nan in split: {int(torch.isnan(out_s).sum())}  max|split - dmma| = {float(d.max()):.3e}  "
           f"mean = {float(d.mean()):.3e}", flush=True)
+
+if a.sustain:
+    from bench import ClockSampler
+
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.sustain)]
+    torch.cuda.synchronize()
+    with ClockSampler(0) as cs:
+        for e0, e1 in evs:
+            e0.record()
+            _lib.check(L.pcc_syrk_split_f64(slices.data_ptr(), scale.data_ptr(), n, l, 0, tiles, _lib.LAYOUT_PACKED,
+                                            out_s.data_ptr(), 0, 0, 0, 0, 0, s0), "syrk_split")
+            e1.record()
+        torch.cuda.synchronize()
+    ts = [e0.elapsed_time(e1) for e0, e1 in evs]
+    print(f"  sustained x{a.sustain}: first {ts[0]:.3f} ms, median {sorted(ts)[len(ts) // 2]:.3f} ms, "
+          f"last {ts[-1]:.3f} ms; clocks {cs.summary()}", flush=True)
