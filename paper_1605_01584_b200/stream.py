@@ -74,11 +74,17 @@ class StreamPlan:
     passes: tuple[tuple[int, int, int, int, int, int], ...]
 
 
-def lead_fraction(n: int, resident: bool = False) -> float:
+# FP64-equivalent contraction rate (n^2 l / t) per method on one B200, for
+# the bottom-up share of the streamed plan
+METHOD_RATE = {"tensor": 35e12, "split": 95e12, "exact": 15e12}
+
+
+def lead_fraction(n: int, resident: bool = False, rate: float = METHOD_RATE["tensor"]) -> float:
     """Share of the range's work done bottom-up while X is still uploading.
 
     Upload time / contraction time ~= 8 B * FP64 rate / (n * PCIe rate)
-    (~35 TFLOP/s vs ~50 GB/s on a B200 box); the bottom-up phase should just
+    (``rate``, the method's FP64-equivalent contraction rate, ``METHOD_RATE``:
+    ~35 TFLOP/s on the FP64 tensor path vs ~50 GB/s); the bottom-up phase should just
     outlast the upload so the top-down phase never waits for data.  The
     1.15 margin is a measured choice (c2 e2e within noise for 0.9-2.0,
     PCC_STREAM_LEAD_SCALE overrides it for experiments).
@@ -88,11 +94,12 @@ def lead_fraction(n: int, resident: bool = False) -> float:
     import os
 
     scale = float(os.environ.get("PCC_STREAM_LEAD_SCALE", "1.15"))  # tuning experiments
-    return min(0.95, max(0.05, scale * 8 * 35e12 / (n * 50e9)))
+    return min(0.95, max(0.05, scale * 8 * rate / (n * 50e9)))
 
 
 def plan_stream(n: int, tile_begin: int, tile_end: int, wave: int, chunk_rows: int = 8, mid: int = 8,
-                lead: float | None = None, half_tail: bool = True) -> StreamPlan:
+                lead: float | None = None, half_tail: bool = True,
+                rate: float = METHOD_RATE["tensor"]) -> StreamPlan:
     """Plan the streamed execution of GPU tiles ``[tile_begin, tile_end)``.
 
     X arrives bottom-up in chunks of GPU tile rows -- 2, 2, 4, 4 rows first
@@ -108,15 +115,27 @@ def plan_stream(n: int, tile_begin: int, tile_end: int, wave: int, chunk_rows: i
     mg = -(-n // T_G)
     if tile_end <= tile_begin:
         return StreamPlan(n, (), ())
-    lead = lead_fraction(n) if lead is None else lead
+    lead = lead_fraction(n, rate=rate) if lead is None else lead
     y_first = sym_job_coord(mg, tile_begin).y
     row_lo = y_first * T_G
     chunk_rows = max(1, chunk_rows)
     ramp = [r for r in (2, 2, 4, 4) if r < chunk_rows]
+    # mostly bottom-up plans (fast methods: the upload and the download are
+    # the critical path) end with small top bands (4, 2, 1 tile rows), so the
+    # work and the download released by the upload's last chunk are short
+    top_ramp = [1, 2, 4] if lead > 0.5 else []
+    top_ramp = [r for r in top_ramp if r < chunk_rows]
+    reserved = min(sum(top_ramp), max(0, mg - y_first - sum(ramp)))
     bands = []  # bottom-up tile-row bands [b, t)
     top = mg
-    while top > y_first:
+    while top > y_first + reserved:
         size = ramp[len(bands)] if len(bands) < len(ramp) else chunk_rows
+        b = max(y_first + reserved, top - size)
+        bands.append((b, top))
+        top = b
+    for size in reversed(top_ramp):
+        if top <= y_first:
+            break
         b = max(y_first, top - size)
         bands.append((b, top))
         top = b
@@ -208,7 +227,8 @@ def run_stream(x, n: int, l: int, device: torch.device, tile_begin: int, tile_en
     with torch.cuda.device(device):
         info = _lib.device_info(device.index)
         wave = info.sm_count * info.syrk_ctas_per_sm
-        plan = plan_stream(n, tile_begin, tile_end, wave, chunk_rows, lead=0.0 if resident is not None else None)
+        plan = plan_stream(n, tile_begin, tile_end, wave, chunk_rows, lead=0.0 if resident is not None else None,
+                           rate=METHOD_RATE[method])
         compute = torch.cuda.current_stream()
         s = stream_handle(compute)
         mark("start", compute)

@@ -8,6 +8,7 @@ from paper_1605_01584_b200.stream import run_stream
 from paper_1605_01584_b200.workloads import CONFIGS, make_config
 
 p = argparse.ArgumentParser(); p.add_argument("--config", default="c2"); p.add_argument("--chunk-rows", type=int, default=4)
+p.add_argument("--method", default="tensor")
 a = p.parse_args()
 spec = CONFIGS[a.config]; n, l = spec.n, spec.l
 x = torch.from_numpy(make_config(a.config)).pin_memory()
@@ -19,7 +20,7 @@ for it in range(3):
     tr = []
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    run_stream(x, n, l, dev, 0, T, out, 0, host, 0, chunk_rows=a.chunk_rows, trace=tr)
+    run_stream(x, n, l, dev, 0, T, out, 0, host, 0, chunk_rows=a.chunk_rows, trace=tr, method=a.method)
     wall = time.perf_counter() - t0
     torch.cuda.synchronize()
     if it == 2:
