@@ -1,8 +1,10 @@
 /* The C ABI from plain C -- no Python, no torch: what a non-Python caller of
  * the engine (or a cgo / JNI binding) does.  Normalises a small random
  * dataset with pcc_normalize_rows_f64, contracts it with pcc_syrk_f64 (packed
- * layout, tensor cores) and pcc_syrk_exact_f64 (the reference's dot8), and
- * checks both against a direct O(n^2 l) Pearson computation on the host.
+ * layout, FP64 tensor cores), pcc_syrk_exact_f64 (the reference's dot8) and
+ * split mode (pcc_split_rows_f64 + pcc_syrk_split_f64: int8 tensor cores on
+ * exact digit planes), and checks all three against a direct O(n^2 l)
+ * Pearson computation on the host.
  *
  *   gcc -O2 -I include -I /usr/local/cuda/include examples/capi_allpairs.c -o examples/capi_allpairs \
  *       -L paper_1605_01584_b200/lib -lpcc_b200 -L /usr/local/cuda/lib64 -lcudart \
@@ -76,10 +78,17 @@ int main(int argc, char **argv) {
   CHECK_PCC(pcc_normalize_rows_f64(dx, l, du, ldu, dzv, l, 0, n, NULL));  /* K1 */
   CHECK_PCC(pcc_zero_rows_f64(du, ldu, n, rows, NULL));                 /* pad rows */
   const uint64_t tiles = pcc_gpu_tile_count(n);
-  double worst[2] = {0, 0};
-  for (int exact = 0; exact < 2; ++exact) {
-    if (exact)
+  int8_t *dslices;
+  double *dscale;
+  CHECK_CUDA(cudaMalloc((void **)&dslices, pcc_split_slice_bytes(n, l)));
+  CHECK_CUDA(cudaMalloc((void **)&dscale, sizeof(double) * rows));
+  CHECK_PCC(pcc_split_rows_f64(du, n, l, ldu, 0, rows, dslices, dscale, NULL)); /* digit planes, pad rows too */
+  double worst[3] = {0, 0, 0};
+  for (int exact = 0; exact < 3; ++exact) {
+    if (exact == 1)
       CHECK_PCC(pcc_syrk_exact_f64(du, n, l, ldu, 0, tiles, PCC_LAYOUT_PACKED, dout, 0, 0, 0, 0, 0, NULL));
+    else if (exact == 2)
+      CHECK_PCC(pcc_syrk_split_f64(dslices, dscale, n, l, 0, tiles, PCC_LAYOUT_PACKED, dout, 0, 0, 0, 0, 0, NULL));
     else
       CHECK_PCC(pcc_syrk_f64(du, n, l, ldu, 0, tiles, PCC_LAYOUT_PACKED, dout, 0, 0, 0, 0, 0, NULL));
     CHECK_CUDA(cudaMemcpy(packed, dout, sizeof(double) * pairs, cudaMemcpyDeviceToHost));
@@ -90,10 +99,11 @@ int main(int argc, char **argv) {
       }
   }
   CHECK_CUDA(cudaMemcpy(zv, dzv, n, cudaMemcpyDeviceToHost));
-  printf("n=%lld l=%lld: max |r - definition| tensor path %.2e, exact mode %.2e; zero-variance row 1 flagged %d\n",
-         (long long)n, (long long)l, worst[0], worst[1], zv[1]);
-  const int ok = worst[0] < 1e-12 && worst[1] < 1e-12 && zv[1] == 1;
-  cudaFree(dx), cudaFree(du), cudaFree(dout), cudaFree(dzv);
+  printf("n=%lld l=%lld: max |r - definition| tensor path %.2e, exact mode %.2e, split mode %.2e; "
+         "zero-variance row 1 flagged %d\n",
+         (long long)n, (long long)l, worst[0], worst[1], worst[2], zv[1]);
+  const int ok = worst[0] < 1e-12 && worst[1] < 1e-12 && worst[2] < 1e-12 && zv[1] == 1;
+  cudaFree(dx), cudaFree(du), cudaFree(dout), cudaFree(dzv), cudaFree(dslices), cudaFree(dscale);
   free(x), free(packed), free(zv);
   printf(ok ? "ok\n" : "FAILED\n");
   return ok ? 0 : 1;

@@ -123,7 +123,10 @@ def plan_stream(n: int, tile_begin: int, tile_end: int, wave: int, chunk_rows: i
     # mostly bottom-up plans (fast methods: the upload and the download are
     # the critical path) end with small top bands (4, 2, 1 tile rows), so the
     # work and the download released by the upload's last chunk are short
-    top_ramp = [1, 2, 4] if lead > 0.5 else []
+    import os
+
+    ramp_on = os.environ.get("PCC_STREAM_TOP_RAMP")  # A/B knob: "0" / "1" force it off / on
+    top_ramp = [1, 2, 4] if (lead > 0.5 if ramp_on is None else ramp_on == "1") else []
     top_ramp = [r for r in top_ramp if r < chunk_rows]
     reserved = min(sum(top_ramp), max(0, mg - y_first - sum(ramp)))
     bands = []  # bottom-up tile-row bands [b, t)

@@ -300,7 +300,7 @@ def test_compute_worker_streamed_shards_match_single(rng):
                 assert sh.zero_variance == frozenset({1})
 
 
-def _exchange_rank(rank, world, port, x, q, exchange="collective"):
+def _exchange_rank(rank, world, port, x, q, exchange="collective", method="tensor"):
     import os
 
     import torch.distributed as dist
@@ -316,16 +316,16 @@ def _exchange_rank(rank, world, port, x, q, exchange="collective"):
         lo, hi = shard_span(n, lo_t, hi_t)
         host = torch.full((max(1, hi - lo),), float("nan"), dtype=torch.float64).pin_memory()
         sh = compute_worker(pc.Dataset(values=torch.from_numpy(x).pin_memory()), world, rank, 0, out=host,
-                            group=dist.group.WORLD, exchange=exchange)
+                            group=dist.group.WORLD, exchange=exchange, method=method)
         q.put((rank, [(a, b, host[a - lo:b - lo].numpy().copy()) for a, b in owned_runs(n, lo_t, hi_t)],
                sorted(sh.zero_variance)))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("exchange", ["collective", "p2p"])
+@pytest.mark.parametrize("exchange,method", [("collective", "tensor"), ("p2p", "tensor"), ("p2p", "split")])
 @pytest.mark.parametrize("world,n,l", [(2, 1100, 23), (3, 700, 40), (3, 200, 9)])
-def test_exchange_mode_workers_match_single(world, n, l, exchange):
+def test_exchange_mode_workers_match_single(world, n, l, exchange, method):
     """compute_worker(group=...): row-block upload + K1 per rank, U all-gathered
     (here over gloo: the ranks share this box's one GPU, each rank's kernels
     independent), then each rank's contraction -- reassembled bit for bit
@@ -343,7 +343,7 @@ def test_exchange_mode_workers_match_single(world, n, l, exchange):
     sock.close()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_exchange_rank, args=(r, world, port, x, q, exchange)) for r in range(world)]
+    procs = [ctx.Process(target=_exchange_rank, args=(r, world, port, x, q, exchange, method)) for r in range(world)]
     for p_ in procs:
         p_.start()
     got = [q.get(timeout=300) for _ in range(world)]
@@ -356,7 +356,7 @@ def test_exchange_mode_workers_match_single(world, n, l, exchange):
         for a, b, v in runs:
             packed[a:b] = v
     assert np.max(np.abs(packed - ref)) <= 1e-12
-    assert np.array_equal(packed, pc.allpairs(pc.Dataset(values=x)).packed)
+    assert np.array_equal(packed, pc.allpairs(pc.Dataset(values=x), method=method).packed)
 
 
 def test_streamed_upload_from_pageable_and_device_inputs(rng):
