@@ -58,9 +58,10 @@ def _host_out(out, total: int) -> torch.Tensor:
 _SMALL_BYTES = 64 << 20  # X + packed result below this: no streaming (measured crossover between c1 and c3)
 
 
-def _device_result_budget(device: torch.device, n: int, l: int) -> int:
+def _device_result_budget(device: torch.device, n: int, l: int, method: str = "tensor") -> int:
     """Bytes the packed result may take on ``device``: free memory minus X, U
-    and a margin (``PCC_DEVICE_RESULT_BUDGET`` overrides, for tests)."""
+    (plus the split method's digit planes) and a margin
+    (``PCC_DEVICE_RESULT_BUDGET`` overrides, for tests)."""
     import os
 
     env = os.environ.get("PCC_DEVICE_RESULT_BUDGET")
@@ -69,6 +70,8 @@ def _device_result_budget(device: torch.device, n: int, l: int) -> int:
     free, _ = torch.cuda.mem_get_info(device)
     L = _lib.lib()
     xu = n * l * 8 + int(L.pcc_rows_padded(n)) * int(L.pcc_ldu(l)) * 8
+    if method == "split":
+        xu += int(L.pcc_split_slice_bytes(n, l)) + 8 * int(L.pcc_rows_padded(n))
     return max(0, int(0.9 * free) - xu - (1 << 30))
 
 
@@ -147,7 +150,7 @@ def _allpairs_one_device(dataset: Dataset, device: torch.device, keep_on_device:
 
         total = sym_job_count(n)
         T = int(L.pcc_gpu_tile_count(n))
-        budget = _device_result_budget(device, n, l)
+        budget = _device_result_budget(device, n, l, method)
         if not keep_on_device and total * 8 > budget:
             # the packed result does not fit the device next to X and U: bounded
             # device windows, each pass downloaded into the host result

@@ -114,6 +114,76 @@ __global__ void peak_kernel(const int8_t *src, int iters, int32_t *sink, long lo
   if (warp == 0) tmem_dealloc(tm, 512);
 }
 
+// A operand from tensor memory (".kind::i8 [d], [a_tmem], b_desc"): 3
+// accumulators of N columns + 7 A slices of 8 columns (128 rows x 32 int8).
+template <int N>
+__global__ void peak_ts_kernel(const int8_t *src, int iters, int32_t *sink, long long *cycles) {
+  extern __shared__ __align__(1024) int8_t sm[];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ uint32_t tmem_base;
+  int8_t *sb = (int8_t *)(((uintptr_t)sm + 1023) & ~(uintptr_t)1023);  // 7 x N x 32
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int i = tid; i < 7 * N * 32; i += blockDim.x) sb[i] = src[(blockIdx.x * 977 + i) & ((1 << 20) - 1)];
+  if (warp == 0) tmem_alloc(smem_u32(&tmem_base), 512);
+  if (tid == 0) mbar_init(smem_u32(&bar), 1), mbar_fence_init();
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tm = tmem_base;
+  long long c0 = clock64();
+  if (tid == 0) {
+    const uint32_t b0 = smem_u32(sb);
+    for (int it = 0; it < iters; ++it) {
+      int q = 0;
+#pragma unroll 1
+      for (int i = 0; i < 7; ++i)
+#pragma unroll 1
+        for (int j = 0; j < 7 && i + j <= 7; ++j, ++q) {
+          const uint32_t d = tm + (uint32_t)(((i + j) % 3) * N), a = tm + 384u + 8u * i;
+          const uint64_t bd = umma_desc_k_sw32(b0 + j * N * 32);
+          const uint32_t acc = (it > 0 || q >= 3) ? 1u : 0u;
+          asm volatile(
+              "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+              " tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
+              "r"(a), "l"(bd), "r"(idesc_i8_s32<128, N>()), "r"(acc));
+        }
+    }
+    umma_commit(smem_u32(&bar));
+  }
+  mbar_wait(smem_u32(&bar), 0);
+  if (tid == 0 && cycles) cycles[blockIdx.x] = clock64() - c0;
+  tc_fence_after();
+  int32_t v[16];
+  tmem_ld16(tm + ((uint32_t)(warp * 32) << 16), v);
+  tmem_ld_wait();
+  if (v[0] == 0x7fffffff) sink[tid] = v[1];
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tm, 512);
+}
+
+template <int N>
+void run_peak_ts(const int8_t *src, int32_t *sink, int sms) {
+  const size_t smem = 1024 + 7 * N * 32;
+  CK(cudaFuncSetAttribute(peak_ts_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int iters = 20000;
+  long long *cyc;
+  CK(cudaMalloc(&cyc, sms * sizeof(long long)));
+  peak_ts_kernel<N><<<sms, 128, smem>>>(src, 100, sink, nullptr);
+  CK(cudaDeviceSynchronize());
+  for (int rep = 0; rep < 3; ++rep) {
+    peak_ts_kernel<N><<<sms, 128, smem>>>(src, iters, sink, cyc);
+    CK(cudaDeviceSynchronize());
+    std::vector<long long> c(sms);
+    CK(cudaMemcpy(c.data(), cyc, sms * sizeof(long long), cudaMemcpyDeviceToHost));
+    long long cmax = 0;
+    for (auto v : c) cmax = v > cmax ? v : cmax;
+    printf("TS (A in TMEM) M=128 N=%3d K=32: %.1f SM clk per MMA (clock64)\n", N, (double)cmax / (34.0 * iters));
+  }
+  CK(cudaFree(cyc));
+}
+
 template <int N>
 void run_peak(const int8_t *src, int32_t *sink, int sms, int zero) {
   const size_t smem = 1024 + 7 * (128 + N) * 32;
@@ -184,6 +254,8 @@ int main() {
   CK(cudaMalloc(&src, r.size()));
   CK(cudaMalloc(&sink, 4096));
   CK(cudaMemcpy(src, r.data(), r.size(), cudaMemcpyHostToDevice));
+  run_peak_ts<64>(src, sink, p.multiProcessorCount);
+  run_peak_ts<128>(src, sink, p.multiProcessorCount);
   for (int zero = 0; zero < 2; ++zero) {
     run_peak<64>(src, sink, p.multiProcessorCount, zero);
     run_peak<128>(src, sink, p.multiProcessorCount, zero);
