@@ -184,6 +184,80 @@ void run_peak_ts(const int8_t *src, int32_t *sink, int sms) {
   CK(cudaFree(cyc));
 }
 
+// CTA pair (cta_group::2): M = 256 (128 rows per CTA), N columns; the leader
+// CTA issues, completion multicast to both CTAs' barriers.  Throughput only.
+template <int N>
+__global__ void __cluster_dims__(2, 1, 1) peak_pair_kernel(const int8_t *src, int iters, long long *cycles) {
+  constexpr int kAcc = 512 / N;
+  extern __shared__ __align__(1024) int8_t sm[];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ uint32_t tmem_base;
+  int8_t *sa = (int8_t *)(((uintptr_t)sm + 1023) & ~(uintptr_t)1023);  // 7 x 128 x 32
+  int8_t *sb = sa + 7 * 128 * 32;                                      // 7 x N x 32
+  const int tid = threadIdx.x, warp = tid >> 5;
+  uint32_t rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  for (int i = tid; i < 7 * (128 + N) * 32; i += blockDim.x) sa[i] = src[(blockIdx.x * 977 + i) & ((1 << 20) - 1)];
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(&tmem_base)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+  }
+  if (tid == 0) mbar_init(smem_u32(&bar), 1), mbar_fence_init();
+  fence_async_smem();
+  tc_fence_before();
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+  tc_fence_after();
+  const uint32_t tm = tmem_base;
+  long long c0 = clock64();
+  if (tid == 0 && rank == 0) {
+    const uint32_t a0 = smem_u32(sa), b0 = smem_u32(sb);
+    constexpr uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+    for (int it = 0; it < iters; ++it) {
+      int q = 0;
+#pragma unroll 1
+      for (int i = 0; i < 7; ++i)
+#pragma unroll 1
+        for (int j = 0; j < 7 && i + j <= 7; ++j, ++q) {
+          const uint32_t acc = (it > 0 || q >= kAcc) ? 1u : 0u;
+          asm volatile(
+              "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+              " tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tm + (uint32_t)(((i + j) % kAcc) * N)),
+              "l"(umma_desc_k_sw32(a0 + i * 128 * 32)), "l"(umma_desc_k_sw32(b0 + j * N * 32)), "r"(idesc), "r"(acc));
+        }
+    }
+    asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n"
+                 ::"r"(smem_u32(&bar)), "h"((uint16_t)3) : "memory");
+  }
+  mbar_wait(smem_u32(&bar), 0);
+  if (tid == 0 && cycles) cycles[blockIdx.x] = clock64() - c0;
+  tc_fence_before();
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;\n" ::"r"(tm));
+}
+
+template <int N>
+void run_peak_pair(const int8_t *src, int sms) {
+  const size_t smem = 1024 + 7 * (128 + N) * 32;
+  CK(cudaFuncSetAttribute(peak_pair_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int iters = 20000;
+  long long *cyc;
+  CK(cudaMalloc(&cyc, sms * sizeof(long long)));
+  const int grid = sms & ~1;
+  peak_pair_kernel<N><<<grid, 128, smem>>>(src, 100, nullptr);
+  CK(cudaDeviceSynchronize());
+  for (int rep = 0; rep < 3; ++rep) {
+    peak_pair_kernel<N><<<grid, 128, smem>>>(src, iters, cyc);
+    CK(cudaDeviceSynchronize());
+    std::vector<long long> c(grid);
+    CK(cudaMemcpy(c.data(), cyc, grid * sizeof(long long), cudaMemcpyDeviceToHost));
+    long long cmax = 0;
+    for (auto v : c) cmax = v > cmax ? v : cmax;
+    printf("PAIR cta_group::2 M=256 N=%3d K=32: %.1f SM clk per MMA (clock64) = %.1f clk per 128x%d per SM\n", N,
+           (double)cmax / (34.0 * iters), (double)cmax / (34.0 * iters), N);
+  }
+  CK(cudaFree(cyc));
+}
+
 template <int N>
 void run_peak(const int8_t *src, int32_t *sink, int sms, int zero) {
   const size_t smem = 1024 + 7 * (128 + N) * 32;
@@ -254,6 +328,8 @@ int main() {
   CK(cudaMalloc(&src, r.size()));
   CK(cudaMalloc(&sink, 4096));
   CK(cudaMemcpy(src, r.data(), r.size(), cudaMemcpyHostToDevice));
+  run_peak_pair<128>(src, p.multiProcessorCount);
+  run_peak_pair<256>(src, p.multiProcessorCount);
   run_peak_ts<64>(src, sink, p.multiProcessorCount);
   run_peak_ts<128>(src, sink, p.multiProcessorCount);
   for (int zero = 0; zero < 2; ++zero) {
