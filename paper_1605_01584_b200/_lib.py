@@ -254,7 +254,9 @@ class Contraction:
             raise ValueError(f"unknown contraction method {method!r}, expected one of {METHODS}")
         check_method_shape(method, l)
         self.method, self.u, self.n, self.l = method, u, int(n), int(l)
-        self.ldu, self.rows = int(u.shape[1]), int(u.shape[0])
+        # U may carry extra zero rows (the multi-GPU exchange pads to p blocks);
+        # the digit planes cover pcc_rows_padded(n) rows
+        self.ldu, self.rows = int(u.shape[1]), min(int(u.shape[0]), int(lib().pcc_rows_padded(n)))
         if method == "split":
             self.slices = torch.empty(int(lib().pcc_split_slice_bytes(n, l)), dtype=torch.uint8, device=u.device)
             self.scale = torch.empty(self.rows, dtype=torch.float64, device=u.device)
