@@ -394,9 +394,8 @@ int launch_split(const int8_t *slices, const double *scale, int64_t n, int64_t l
   int rc = device_config(&dc);
   if (rc) return rc;
   const int64_t rows = pcc_rows_padded(n), k_blocks = (int64_t)ceil_div((uint64_t)l, (uint64_t)C::kRowBytes);
-  CUtensorMap map7, map4;
-  rc = encode_slice_map(slices, rows, k_blocks, 7, &map7);
-  if (rc == PCC_OK) rc = encode_slice_map(slices, rows, k_blocks, 4, &map4);
+  CUtensorMap map1;
+  rc = encode_slice_map(slices, rows, k_blocks, 1, &map1);
   if (rc) return rc;
   const uint64_t m_g = ceil_div((uint64_t)n, pcc::kTile);
   const uint64_t resident = (uint64_t)dc->sm_count * (uint64_t)(dc->split_ctas > 0 ? dc->split_ctas : 1);
@@ -405,7 +404,7 @@ int launch_split(const int8_t *slices, const double *scale, int64_t n, int64_t l
   uint32_t group = 1;
   while ((uint64_t)(group + 1) * (group + 1) <= grid) ++group;
   const pcc::TileOrder order = pcc::make_tile_order(m_g, tb, te, group);
-  pcc::syrk_split_kernel<LAYOUT><<<grid, C::kThreads, C::kSmemBytes, stream>>>(map7, map4, scale, n, l,
+  pcc::syrk_split_kernel<LAYOUT><<<grid, C::kThreads, C::kSmemBytes, stream>>>(map1, scale, n, l,
                                                                                (int)k_blocks, m_g, order, ep, split_dbg);
   PCC_CUDA(cudaGetLastError(), "syrk_split_kernel launch");
   return PCC_OK;

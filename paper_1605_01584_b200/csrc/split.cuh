@@ -49,7 +49,7 @@ struct SplitCfg {
   static constexpr int kEpiWarps = 8;
   static constexpr int kThreads = 32 * (2 + kEpiWarps);
   static constexpr uint32_t kTmemCols = 512;
-  static constexpr int kBarBytes = 8 * (2 * kStages + 2) + 16;
+  static constexpr int kBarBytes = 8 * (kStages * kSlices + kStages + 2) + 16;  // full per (stage, slice)
   static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + kBarBytes;
   static constexpr int64_t kMaxL = 8192;  // the error bound above holds up to here
   // Adaptive depth: a tile pair skips diagonal d = 9 (0-based sd = 7: 6 of
@@ -89,6 +89,104 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap *map
       "[%5];\n" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
       : "memory");
+}
+
+// ---- MMA schedules -------------------------------------------------------
+// An int8 MMA costs ~92 clk for N <= 128 but only 128 clk for N = 256 (the
+// MAC floor, profiles/r01_i8_mma_peak.log), so digit pairs (i, j), (i, j+1)
+// of neighbouring diagonals go out as one N = 256 MMA whose B operand is the
+// two consecutive slice tiles j, j+1 of the X band and whose two 128-column
+// halves land in neighbouring accumulators.  Entry = i | j << 3 | wide << 6 |
+// zero << 7; `zero` marks each accumulator's first write of a tile (no
+// accumulate at the first K step) and precedes every other entry touching
+// it.  Entries are ordered by the highest slice they read (the stage's
+// slices land one by one) and so that consecutive MMAs mostly target
+// different accumulators.  The integer sums are exact, so any schedule gives
+// the same bits.
+// Schedule S entry e (S = 0: pass 1, diagonals 0..3, 10 products; S = 1:
+// pass 0 at full depth, diagonals 4..7, 24 products; S = 2: pass 0 at
+// adaptive depth, diagonals 4..6, 18 products, accumulator 3 unused), as
+// i | j << 3 | wide << 6 | zero << 7 -- a constexpr switch so the unrolled
+// issue loop folds every entry into immediates.
+__host__ __device__ constexpr int sched_len(int S) { return S == 0 ? 6 : (S == 1 ? 13 : 12); }
+__host__ __device__ constexpr uint32_t sched_entry(int S, int e) {
+  if (S == 0) {
+    switch (e) {
+      case 0: return 2u | (0u << 3) | (1u << 6) | (1u << 7);  // (2, 0) wide zero
+      case 1: return 0u | (0u << 3) | (1u << 6) | (1u << 7);  // (0, 0) wide zero
+      case 2: return 1u | (2u << 3) | (0u << 6) | (0u << 7);  // (1, 2)
+      case 3: return 1u | (0u << 3) | (1u << 6) | (0u << 7);  // (1, 0) wide
+      case 4: return 3u | (0u << 3) | (0u << 6) | (0u << 7);  // (3, 0)
+      case 5: return 0u | (2u << 3) | (1u << 6) | (0u << 7);  // (0, 2) wide
+    }
+  }
+  if (S == 1) {
+    switch (e) {
+      case 0: return 3u | (1u << 3) | (1u << 6) | (1u << 7);  // (3, 1) wide zero
+      case 1: return 3u | (3u << 3) | (1u << 6) | (1u << 7);  // (3, 3) wide zero
+      case 2: return 2u | (2u << 3) | (1u << 6) | (0u << 7);  // (2, 2) wide
+      case 3: return 4u | (2u << 3) | (1u << 6) | (0u << 7);  // (4, 2) wide
+      case 4: return 4u | (0u << 3) | (1u << 6) | (0u << 7);  // (4, 0) wide
+      case 5: return 2u | (4u << 3) | (1u << 6) | (0u << 7);  // (2, 4) wide
+      case 6: return 1u | (3u << 3) | (1u << 6) | (0u << 7);  // (1, 3) wide
+      case 7: return 6u | (0u << 3) | (1u << 6) | (0u << 7);  // (6, 0) wide
+      case 8: return 0u | (4u << 3) | (1u << 6) | (0u << 7);  // (0, 4) wide
+      case 9: return 1u | (5u << 3) | (1u << 6) | (0u << 7);  // (1, 5) wide
+      case 10: return 5u | (0u << 3) | (1u << 6) | (0u << 7);  // (5, 0) wide
+      case 11: return 5u | (2u << 3) | (0u << 6) | (0u << 7);  // (5, 2)
+      case 12: return 0u | (6u << 3) | (0u << 6) | (0u << 7);  // (0, 6)
+    }
+  }
+  if (S == 2) {
+    switch (e) {
+      case 0: return 3u | (1u << 3) | (1u << 6) | (1u << 7);  // (3, 1) wide zero
+      case 1: return 3u | (3u << 3) | (0u << 6) | (1u << 7);  // (3, 3) zero
+      case 2: return 2u | (2u << 3) | (1u << 6) | (0u << 7);  // (2, 2) wide
+      case 3: return 2u | (4u << 3) | (0u << 6) | (0u << 7);  // (2, 4)
+      case 4: return 1u | (3u << 3) | (1u << 6) | (0u << 7);  // (1, 3) wide
+      case 5: return 4u | (2u << 3) | (0u << 6) | (0u << 7);  // (4, 2)
+      case 6: return 4u | (0u << 3) | (1u << 6) | (0u << 7);  // (4, 0) wide
+      case 7: return 1u | (5u << 3) | (0u << 6) | (0u << 7);  // (1, 5)
+      case 8: return 0u | (4u << 3) | (1u << 6) | (0u << 7);  // (0, 4) wide
+      case 9: return 0u | (6u << 3) | (0u << 6) | (0u << 7);  // (0, 6)
+      case 10: return 5u | (0u << 3) | (1u << 6) | (0u << 7);  // (5, 0) wide
+      case 11: return 6u | (0u << 3) | (0u << 6) | (0u << 7);  // (6, 0)
+    }
+  }
+  return 0;
+}
+
+
+// Issue one stage's MMAs for schedule S (0: diagonals 0..3; 1: 4..7; 2:
+// 4..6) in straight-line code: both K steps of the 64-byte rows (K step
+// outer, so consecutive MMAs alternate accumulators), each entry after
+// waiting for the stage's slices it reads (the slices land in order; the
+// barriers of (stage, slice) are 8 bytes apart from full0).
+template <int S>
+__device__ __forceinline__ void issue_stage(uint32_t tmem, uint32_t a, uint32_t b, bool first_k, uint32_t full0,
+                                            uint32_t phase) {
+  using C = SplitCfg;
+  constexpr uint32_t idesc = idesc_i8_s32<128, 128>(), idesc256 = idesc_i8_s32<128, 256>();
+  constexpr int s_lo = S == 0 ? 0 : 4;
+  const uint64_t desc0 = umma_desc_k_sw64(0);
+  int ready = -1;
+#pragma unroll
+  for (int ks = 0; ks < C::kKSub; ++ks) {
+#pragma unroll
+    for (int e = 0; e < sched_len(S); ++e) {
+      const uint32_t ent = sched_entry(S, e);
+      const uint32_t i = ent & 7u, j = (ent >> 3) & 7u, wide = (ent >> 6) & 1u, zero = ent >> 7;
+      const int need = (int)(i > j + wide ? i : j + wide);
+      if (ready < need) {
+        while (ready < need) mbar_wait(full0 + 8u * (uint32_t)(++ready), phase);
+        tc_fence_after();
+      }
+      const uint64_t da = desc0 + ((a + i * C::kSliceBytes + ks * C::kKStep) >> 4);
+      const uint64_t db = desc0 + ((b + j * C::kSliceBytes + ks * C::kKStep) >> 4);
+      umma_i8(tmem + 128u * (i + j - (uint32_t)s_lo), da, db, wide ? idesc256 : idesc,
+              (zero && first_k && ks == 0) ? 0u : 1u);
+    }
+  }
 }
 
 // ---- slicing: U rows -> int8 digit planes + per-row scale ------------------
@@ -138,17 +236,18 @@ __global__ void __launch_bounds__(256) split_rows_kernel(const double *__restric
 // ---- the contraction ----------------------------------------------------
 template <int LAYOUT>
 __global__ void __launch_bounds__(SplitCfg::kThreads, 1)
-    syrk_split_kernel(const __grid_constant__ CUtensorMap map7, const __grid_constant__ CUtensorMap map4,
-                      const double *__restrict__ scale, int64_t n, int64_t l, int k_blocks, uint64_t m_g,
+    syrk_split_kernel(const __grid_constant__ CUtensorMap map1, const double *__restrict__ scale, int64_t n, int64_t l, int k_blocks, uint64_t m_g,
                       TileOrder order, Epilogue ep, int dbg) {
   using C = SplitCfg;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t ring = (raw + 1023u) & ~1023u;  // 32-byte swizzle atoms: keep 1 KB alignment
   const uint32_t bars = ring + C::kStages * C::kStageBytes;
-  auto full_bar = [&](int s) { return bars + 8u * s; };
-  auto empty_bar = [&](int s) { return bars + 8u * (C::kStages + s); };
-  const uint32_t tfull = bars + 8u * (2 * C::kStages);
+  // one "full" barrier per (stage, slice): the MMAs of a stage start on the
+  // first slices while the later ones are still landing; one "empty" per stage
+  auto full_bar = [&](int s, int sl) { return bars + 8u * (s * C::kSlices + sl); };
+  auto empty_bar = [&](int s) { return bars + 8u * (C::kStages * C::kSlices + s); };
+  const uint32_t tfull = bars + 8u * (C::kStages * C::kSlices + C::kStages);
   const uint32_t tempty = tfull + 8u;
   const uint32_t tmem_slot = tempty + 8u;
   uint32_t *tmem_slot_ptr =
@@ -156,12 +255,14 @@ __global__ void __launch_bounds__(SplitCfg::kThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < C::kStages; ++s) mbar_init(full_bar(s), 1), mbar_init(empty_bar(s), 1);
+    for (int s = 0; s < C::kStages; ++s) {
+      for (int sl = 0; sl < C::kSlices; ++sl) mbar_init(full_bar(s, sl), 1);
+      mbar_init(empty_bar(s), 1);
+    }
     mbar_init(tfull, 1);
     mbar_init(tempty, C::kEpiWarps);
     mbar_fence_init();
-    tma_prefetch_desc(&map7);
-    tma_prefetch_desc(&map4);
+    tma_prefetch_desc(&map1);
   }
   if (warp == 1) tmem_alloc(tmem_slot, C::kTmemCols);
   tc_fence_before();
@@ -180,17 +281,20 @@ __global__ void __launch_bounds__(SplitCfg::kThreads, 1)
         uint64_t Y, X;
         tile_at(order, m_g, s, Y, X);
         for (int pass = 0; pass < 2; ++pass) {
-          const CUtensorMap *map = pass == 0 ? &map7 : &map4;
-          const uint32_t bytes = 2u * (pass == 0 ? 7u : 4u) * C::kSliceBytes;
+          const int n_sl = pass == 0 ? C::kSlices : 4;  // pass 1 reads digit slices 0..3 only
           for (int kb = 0; kb < k_blocks; ++kb) {
             mbar_wait(empty_bar(stage), phase ^ 1);
-            if (dbg == 1) {
-              mbar_arrive(full_bar(stage));
-            } else {
-            mbar_arrive_expect_tx(full_bar(stage), bytes);
             const uint32_t a = ring + stage * C::kStageBytes;
-            tma_load_3d(a, map, 0, (int32_t)(Y * kTile), kb * C::kSlices, full_bar(stage));
-            tma_load_3d(a + C::kOpBytes, map, 0, (int32_t)(X * kTile), kb * C::kSlices, full_bar(stage));
+            for (int sl = 0; sl < n_sl; ++sl) {  // slice by slice, in the order the MMAs need them
+              if (dbg == 1) {
+                mbar_arrive(full_bar(stage, sl));
+                continue;
+              }
+              mbar_arrive_expect_tx(full_bar(stage, sl), 2u * C::kSliceBytes);
+              tma_load_3d(a + sl * C::kSliceBytes, &map1, 0, (int32_t)(Y * kTile), kb * C::kSlices + sl,
+                          full_bar(stage, sl));
+              tma_load_3d(a + C::kOpBytes + sl * C::kSliceBytes, &map1, 0, (int32_t)(X * kTile),
+                          kb * C::kSlices + sl, full_bar(stage, sl));
             }
             if (++stage == C::kStages) stage = 0, phase ^= 1;
           }
@@ -199,8 +303,6 @@ __global__ void __launch_bounds__(SplitCfg::kThreads, 1)
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
-    constexpr uint32_t idesc = idesc_i8_s32<128, 128>();
-    const uint64_t desc0 = umma_desc_k_sw64(0);
     int stage = 0;
     uint32_t phase = 0, use = 0;
     for (uint64_t s = blockIdx.x; s < count; s += gridDim.x) {
@@ -213,23 +315,18 @@ __global__ void __launch_bounds__(SplitCfg::kThreads, 1)
           tc_fence_after();
           const int s_lo = pass == 0 ? 4 : 0;  // 0-based diagonal i + j (d - 2)
           for (int kb = 0; kb < k_blocks; ++kb) {
-            mbar_wait(full_bar(stage), phase);
-            tc_fence_after();
             const uint32_t a = ring + stage * C::kStageBytes, b = a + C::kOpBytes;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              if (pass == 0 && q > q_top) continue;  // adaptive depth: sd = 7 dropped
-              const int sd = s_lo + q;
-              const int i_lo = sd > 6 ? sd - 6 : 0, i_hi = sd < 6 ? sd : 6;
-              for (int i = i_lo; i <= i_hi; ++i) {
-#pragma unroll
-                for (int ks = 0; ks < C::kKSub; ++ks) {  // K step within the 64-byte swizzled rows: +32 B
-                  const uint64_t da = desc0 + ((a + i * C::kSliceBytes + ks * C::kKStep) >> 4);
-                  const uint64_t db = desc0 + ((b + (sd - i) * C::kSliceBytes + ks * C::kKStep) >> 4);
-                  if (dbg != 2)
-                    umma_i8(tmem + 128u * q, da, db, idesc, (kb > 0 || ks > 0 || i > i_lo) ? 1u : 0u);
-                }
-              }
+            // the pass's MMA schedule (kSched*), fully unrolled
+            const bool first_k = kb == 0;
+            if (dbg != 2) {
+              if (pass == 1)
+                issue_stage<0>(tmem, a, b, first_k, full_bar(stage, 0), phase);
+              else if (q_top == 3)
+                issue_stage<1>(tmem, a, b, first_k, full_bar(stage, 0), phase);
+              else
+                issue_stage<2>(tmem, a, b, first_k, full_bar(stage, 0), phase);
+            } else {
+              for (int sl = 0; sl < (pass == 1 ? 4 : C::kSlices); ++sl) mbar_wait(full_bar(stage, sl), phase);
             }
             umma_commit(empty_bar(stage));  // the slot is free once these MMAs have read it
             if (++stage == C::kStages) stage = 0, phase ^= 1;
