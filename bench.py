@@ -444,9 +444,9 @@ def run_b200(args, rank: int, world: int, local_rank: int) -> None:
             "max_abs_diff_vs_fp64_tensor_path": diff,
             "roofline": {"bound": "tensor", "achieved": i8_ach, "peak": i8_peak, "unit": "TOP/s",
                          "frac": i8_ach / i8_peak,
-                         "kernel": "syrk_split_kernel<packed> (TMA 3-D boxes of 7 digit planes, tcgen05.mma "
-                                   "kind::i8 M128 N128 K32, 4 s32 accumulators in TMEM, 2 K passes per tile, "
-                                   "adaptive depth 34/28 products)",
+                         "kernel": "syrk_split_kernel<packed> (TMA 3-D boxes per digit slice, tcgen05.mma "
+                                   "kind::i8 M128 N256/N128 K32 domino schedule, 4 s32 accumulators in TMEM, 2 K passes "
+                                   "per tile, adaptive depth 34/28 products)",
                          "algorithmic_ops_per_launch": i8_ops,
                          "peak_source": "measured int8 tcgen05.mma throughput on this pool's B200 "
                                         "(tools/i8_mma.cu, profiles/r01_i8_mma_peak.log: 128x256x32 shape; "

@@ -10,23 +10,28 @@
 //     u_y·u_x ≈ 2^(e_y+e_x) Σ_{d=2..9} 2^(-7d) · A_d,
 //     A_d = Σ_{i+j=d} S_i(y)·S_j(x)            (int8 dot products, exact in s32)
 // i.e. 34 int8 GEMM products (all i, j ≤ 7 with i + j ≤ 9), summed per
-// diagonal d in one s32 TMEM accumulator each (|A_d| ≤ 6·64²·l < 2³¹ for
-// l ≤ 8192... ≤ 2·10⁸ at l = 8192), combined in FP64 by Horner's rule in
-// the epilogue.  Error bound per coefficient, l ≤ 8192:
+// diagonal d in one s32 TMEM accumulator each (|A_d| ≤ 7·127·64·l < 2³¹ for
+// l ≤ 8192), combined in FP64 by Horner's rule in the epilogue.  Error
+// bound per coefficient at full depth, l ≤ 8192 (K2s):
 // representation ≤ 2·√l·2^-49 ≈ 3.2e-13, dropped products (i + j ≥ 10)
 // ≤ 5.7e-13, FP64 combination ~1e-16 — inside the north star's 1e-12.
 //
-// Layouts.  Slices: int8 [KB][7][R][32] (KB = ⌈l/32⌉ K blocks of 32, R =
-// padded rows), so a TMA box {32 B, 128 rows, 7 slices} is the 7 operand
-// tiles of one K step, each 4 KB, K-major with the 32-byte swizzle the
-// UMMA descriptor names.  Scales: double[R] = 2^(e_r - 7).
+// (1-based digit indices above; the code uses 0-based i, j = 0..6 and
+// diagonals sd = i + j = d - 2.)  Adaptive depth drops sd = 7 per tile pair
+// when its rows allow (split_drop_top); DESIGN.md §3 "K2s" has the bounds.
+//
+// Layouts.  Slices: int8 [KB][7][R][64] (KB = ⌈l/64⌉ K blocks of 64, R =
+// padded rows): one TMA box {64 B, 128 rows, 1 slice} is an 8 KB operand
+// tile of two MMA K steps, K-major with the 64-byte swizzle the UMMA
+// descriptor names.  Scales: double[R] = 2^(e_r - 7), 0 for all-zero rows.
 //
 // Kernel (one 128 x 128 GPU tile of the bijection per CTA at a time,
 // persistent, grouped L2-locality order like K2): warp 0 = TMA producer,
 // warp 1 = TMEM owner + MMA issuer (one thread), warps 2..9 = epilogue.
 // TMEM (512 columns) holds four 128 x 128 s32 accumulators, so each tile
-// takes two passes over K: pass 0 accumulates d = 6..9 (24 MMAs per K step,
-// slices 1..7), pass 1 d = 2..5 (10 MMAs, slices 1..4); the epilogue warps
+// takes two passes over K: pass 0 accumulates sd = 4..7 (slices 0..6),
+// pass 1 sd = 0..3 (slices 0..3), each with the "domino" schedules below
+// (N = 256 MMAs for neighbouring-diagonal digit pairs); the epilogue warps
 // fold pass 0 into FP64 registers (Horner) while pass 1 runs, then finish
 // and store through the same store_cell() as K2 (packed / dense / tiles).
 #pragma once
