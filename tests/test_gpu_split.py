@@ -269,3 +269,22 @@ def test_split_full_c2_vs_fp64_tensor_path():
     assert float((a - b).abs().max()) <= 2e-14
     del a, b
     torch.cuda.empty_cache()
+
+
+def test_split_mixed_depth_tiles_vs_oracle():
+    """Adaptive depth decided per tile pair: spiky rows (max|u| near 1) in one
+    GPU tile row force full depth (34 products) on every tile touching it,
+    the other tiles run at depth 28 -- all within 1e-12 of the reference, and
+    the host replica of the decision sees both depths."""
+    r = np.random.default_rng(21)
+    n, l = 600, 4096
+    x = r.standard_normal((n, l))
+    x[256:300, 7] += 400.0  # tile row 2: one dominant sample per row
+    u = _normalized(x)
+    con = _lib.Contraction("split", u, n, l).prepare_all(torch.cuda.current_stream().cuda_stream)
+    T = int(_lib.lib().pcc_gpu_tile_count(n))
+    prod = _lib.split_products(con.scale, n, l, 0, T)
+    assert 28 * T < prod < 34 * T, prod
+    ref, _ = oracle.allpairs(x, t=4)
+    got = pc.allpairs(pc.Dataset(values=x), **SPLIT).packed
+    assert float(np.abs(got - ref).max()) <= TOL
