@@ -255,13 +255,15 @@ class PackedFileWriterSink(ResultSink):
         self.close()
 
 
-def allpairs_to_file(dataset: Dataset, path, device=None) -> frozenset[int]:
+def allpairs_to_file(dataset: Dataset, path, device=None, *, exact: bool = False,
+                     method: str | None = None) -> frozenset[int]:
     """All-pairs PCC of ``dataset`` written straight to an ``LPCR`` file.
 
     The zero-variance set (needed for the header, which precedes the
     payload) comes from one normalisation pass; the streamed engine then
     downloads finished packed rows directly into the file's memory map.
-    Returns the zero-variance set.
+    ``exact`` / ``method``: the contraction (see ``allpairs``).  Returns the
+    zero-variance set.
     """
     import torch
 
@@ -270,6 +272,8 @@ def allpairs_to_file(dataset: Dataset, path, device=None) -> frozenset[int]:
     from .stream import run_stream
     from .transform import normalize_device
 
+    method = _lib.resolve_method(method, exact)
+    _lib.check_method_shape(method, dataset.l)
     dev = resolve_devices(None if device is None else [device])[0]
     n, l = dataset.n, dataset.l
     with torch.cuda.device(dev):
@@ -279,7 +283,7 @@ def allpairs_to_file(dataset: Dataset, path, device=None) -> frozenset[int]:
         payload = _create_result_file(path, n, zv)
         T = int(_lib.lib().pcc_gpu_tile_count(n))
         packed = torch.empty(sym_job_count(n), dtype=torch.float64, device=dev)
-        run_stream(x, n, l, dev, 0, T, packed, 0, torch.from_numpy(payload), 0)
+        run_stream(x, n, l, dev, 0, T, packed, 0, torch.from_numpy(payload), 0, method=method)
         payload.flush()
         del payload
     return zv

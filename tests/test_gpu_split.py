@@ -288,3 +288,19 @@ def test_split_mixed_depth_tiles_vs_oracle():
     ref, _ = oracle.allpairs(x, t=4)
     got = pc.allpairs(pc.Dataset(values=x), **SPLIT).packed
     assert float(np.abs(got - ref).max()) <= TOL
+
+
+def test_split_to_file_and_pipeline_sink(tmp_path, rng):
+    """method='split' through the LPCR file writer and the reference's
+    bounded pipeline into its file sink: the same bits as allpairs."""
+    x = random_values(rng, 777, 29, special_rows=True)
+    d = pc.Dataset(values=x)
+    ref = pc.allpairs(d, **SPLIT).packed
+    zv = pc.allpairs_to_file(d, tmp_path / "s.lpcr", **SPLIT)
+    back = pc.load_result(tmp_path / "s.lpcr")
+    assert np.array_equal(back.packed, ref) and back.zero_variance == zv == frozenset({1})
+    nd = pc.normalize(d)
+    g = pc.TileGeometry(n=777, t=4)
+    with pc.PackedFileWriterSink(tmp_path / "p.lpcr", g, nd.zero_variance) as sink:
+        pc.run_pipeline(nd, g, pc.plan_passes(0, g.total_tiles, 5000), sink, **SPLIT)
+    assert np.array_equal(pc.load_result(tmp_path / "p.lpcr").packed, ref)
