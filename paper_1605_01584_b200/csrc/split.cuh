@@ -203,9 +203,16 @@ __global__ void __launch_bounds__(256) split_rows_kernel(const double *__restric
   const int lane = threadIdx.x & 31;
   const int64_t r = row_lo + (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (r >= row_hi) return;
-  const double *row = u + r * ldu;
+  const double *row = u + r * ldu;  // rows start 256-byte aligned (ldu % 32 == 0)
   double m = 0.0;
-  for (int64_t k = lane; k < l; k += 32) m = fmax(m, fabs(row[k]));
+  {
+    const int64_t l2 = l & ~(int64_t)1;
+    for (int64_t k = 2 * lane; k < l2; k += 64) {
+      const double2 p = __ldg(reinterpret_cast<const double2 *>(row + k));
+      m = fmax(m, fmax(fabs(p.x), fabs(p.y)));
+    }
+    if ((l & 1) && lane == 0) m = fmax(m, fabs(row[l - 1]));
+  }
 #pragma unroll
   for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
   int e = 0;
@@ -214,16 +221,29 @@ __global__ void __launch_bounds__(256) split_rows_kernel(const double *__restric
     if (ldexp(m, 7 - e) >= 127.5) ++e;           // keep the leading digit within [-127, 127]
   }
   if (lane == 0) scale[r] = m > 0.0 ? ldexp(1.0, e - 7) : 0.0;  // all-zero rows: 0 (digits are 0 too)
+  // v = u * 2^(7-e): one exact multiply by a power of two (ldexp only when
+  // that power itself would not be a finite double -- not for normalised rows)
+  const bool pw_ok = 7 - e <= 1000;
+  const double pw = pw_ok ? ldexp(1.0, 7 - e) : 0.0;
   constexpr int W = SplitCfg::kRowBytes;
   const int64_t kb_count = (l + W - 1) / W;
   const int64_t plane = rows_total * W;          // bytes between slice planes
   for (int64_t k0 = 0; k0 < kb_count * W; k0 += 128) {
     const int64_t k = k0 + 4 * lane;
     if (k >= kb_count * W) break;
+    double x4[4];
+    if (k + 3 < l) {
+      const double2 p0 = __ldg(reinterpret_cast<const double2 *>(row + k));
+      const double2 p1 = __ldg(reinterpret_cast<const double2 *>(row + k + 2));
+      x4[0] = p0.x, x4[1] = p0.y, x4[2] = p1.x, x4[3] = p1.y;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) x4[j] = (k + j < l) ? row[k + j] : 0.0;
+    }
     uint32_t packed[SplitCfg::kSlices] = {};
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      double v = (k + j < l) ? ldexp(row[k + j], 7 - e) : 0.0;
+      double v = pw_ok ? x4[j] * pw : ldexp(x4[j], 7 - e);
 #pragma unroll
       for (int i = 0; i < SplitCfg::kSlices; ++i) {
         const double d = rint(v);
