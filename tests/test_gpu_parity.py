@@ -683,8 +683,9 @@ def test_exact_subprocess_workers_and_device_output(rng, monkeypatch):
 @settings(max_examples=40, deadline=None)
 def test_allpairs_property_vs_oracle(n, l, seed, dist):
     """Random shapes and value distributions (incl. small integers: ties,
-    constant rows, exact cancellations): the tensor path within 1e-12 of the
-    reference order, the exact mode bit-identical, the same zero-variance set."""
+    constant rows, exact cancellations): the tensor path and split mode within
+    1e-12 of the reference order, the exact mode bit-identical, the same
+    zero-variance set."""
     r = np.random.default_rng(seed)
     x = {"normal": lambda: r.standard_normal((n, l)),
          "lognormal": lambda: r.lognormal(0.0, 2.0, (n, l)),
@@ -696,6 +697,9 @@ def test_allpairs_property_vs_oracle(n, l, seed, dist):
     assert fast.zero_variance == frozenset(np.flatnonzero(zv).tolist())
     exact = pc.allpairs(d, exact=True)
     assert np.array_equal(exact.packed.view(np.uint64), ref.view(np.uint64))
+    split = pc.allpairs(d, method="split")
+    assert np.max(np.abs(split.packed - ref)) <= 1e-12
+    assert split.zero_variance == fast.zero_variance
 
 
 def test_normalize_broadcast_writes_every_destination(rng):
