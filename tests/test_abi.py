@@ -92,6 +92,24 @@ def test_sass_is_sm100a_and_uses_dmma():
     assert "SYNCS" in sass               # mbarrier ring
     assert "LDGSTS" in sass              # cp.async staging (K1, exact mode)
     assert "DMUL" in sass and "DADD" in sass  # exact mode / K1 chains (no FMA contraction)
+    assert "UTCIMMA" in sass             # split mode: tcgen05.mma kind::i8 (int8 tensor cores, TMEM)
+    assert "UTMALDG.3D" in sass          # split mode: per-slice TMA boxes of the digit planes
+    assert "UTCATOMSWS" in sass          # split mode: tcgen05.alloc (TMEM allocation)
+
+
+def test_split_entry_points_validate_before_device_work():
+    L = _lib.lib()
+    W = _lib.SPLIT_ROW_BYTES
+    # digit planes: 7 planes x padded rows x l rounded up to the 64-byte row segment
+    for n, l in [(1, 2), (300, 77), (16384, 4096), (10007, 1531)]:
+        assert L.pcc_split_slice_bytes(n, l) == 7 * L.pcc_rows_padded(n) * (-(-l // W) * W)
+    assert L.pcc_split_slice_bytes(0, 5) == 0
+    with pytest.raises(ValueError, match="l <= 8192"):
+        _lib.check(L.pcc_syrk_split_f64(None, None, 4, 8193, 0, 1, 0, None, 0, 0, 0, 0, 0, None))
+    with pytest.raises(ValueError, match="NULL"):
+        _lib.check(L.pcc_syrk_split_f64(None, None, 4, 100, 0, 1, 0, None, 0, 0, 0, 0, 0, None))
+    with pytest.raises(ValueError, match="tile size"):
+        _lib.check(L.pcc_compute_pass_split_f64(None, None, 10, 100, 0, 0, 1, None, None))
 
 
 @pytest.mark.parametrize("n", [1, 129, 300, 2000, 10007, 16384])
