@@ -190,6 +190,16 @@ int pcc_compute_pass_f64(const double *u, int64_t n, int64_t l, int64_t ldu, int
 int pcc_compute_pass_exact_f64(const double *u, int64_t n, int64_t l, int64_t ldu, int64_t t,
                                uint64_t j_lo, uint64_t j_hi, double *out, void *stream);
 
+/* pcc_normalize_rows_f64 fused with pcc_split_rows_f64: rows [row_lo,
+ * row_hi) of x (n x l, stride ldx, l <= 8192) are normalised exactly as the
+ * reference does (same bits as pcc_normalize_rows_f64) and written straight
+ * into split-mode digit planes and scales (the same bytes pcc_split_rows_f64
+ * makes from that U); U itself is not written.  A range ending at row n
+ * also zeroes the pad rows' digits and scales. */
+int pcc_normalize_split_rows_f64(const double *x, int64_t ldx, int64_t n, int64_t l,
+                                 uint8_t *zero_variance, int64_t row_lo, int64_t row_hi,
+                                 int8_t *slices, double *scale, void *stream);
+
 /* pcc_compute_pass_f64 from split-mode digit planes (pcc_split_rows_f64 over
  * every row the pass touches): the reference's pass-buffer layout, each
  * coefficient within 1e-12 of the reference's. */

@@ -59,6 +59,7 @@ EXPORTED_SYMBOLS = (
     "pcc_syrk_exact_f64",
     "pcc_split_slice_bytes",
     "pcc_split_rows_f64",
+    "pcc_normalize_split_rows_f64",
     "pcc_syrk_split_f64",
     "pcc_compute_pass_f64",
     "pcc_compute_pass_exact_f64",
@@ -116,6 +117,7 @@ def _bind(l: ctypes.CDLL) -> None:
         "pcc_syrk_exact_f64": (ctypes.c_int, [_vp, _i64, _i64, _i64, _u64, _u64, _i32, _vp, _i64, _u64, _i32, _u64, _u64, _vp]),
         "pcc_split_slice_bytes": (_u64, [_i64, _i64]),
         "pcc_split_rows_f64": (ctypes.c_int, [_vp, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _vp]),
+        "pcc_normalize_split_rows_f64": (ctypes.c_int, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _vp, _vp, _vp]),
         "pcc_syrk_split_f64": (ctypes.c_int, [_vp, _vp, _i64, _i64, _u64, _u64, _i32, _vp, _i64, _u64, _i32, _u64, _u64, _vp]),
         "pcc_compute_pass_f64": (ctypes.c_int, [_vp, _i64, _i64, _i64, _i64, _u64, _u64, _vp, _vp]),
         "pcc_compute_pass_exact_f64": (ctypes.c_int, [_vp, _i64, _i64, _i64, _i64, _u64, _u64, _vp, _vp]),
@@ -247,19 +249,33 @@ class Contraction:
     arguments of ``pcc_syrk_f64`` / ``pcc_compute_pass_f64`` after U and
     raise ``DeviceError`` on failure."""
 
-    def __init__(self, method: str, u, n: int, l: int):
+    def __init__(self, method: str, u, n: int, l: int, device=None):
         import torch
 
         if method not in METHODS:
             raise ValueError(f"unknown contraction method {method!r}, expected one of {METHODS}")
         check_method_shape(method, l)
+        if u is None and method != "split":
+            raise ValueError("only the split method runs without U (normalize_split)")
         self.method, self.u, self.n, self.l = method, u, int(n), int(l)
         # U may carry extra zero rows (the multi-GPU exchange pads to p blocks);
         # the digit planes cover pcc_rows_padded(n) rows
-        self.ldu, self.rows = int(u.shape[1]), min(int(u.shape[0]), int(lib().pcc_rows_padded(n)))
+        rows_pad = int(lib().pcc_rows_padded(n))
+        self.ldu = int(u.shape[1]) if u is not None else 0
+        self.rows = min(int(u.shape[0]), rows_pad) if u is not None else rows_pad
+        dev = u.device if u is not None else device
         if method == "split":
-            self.slices = torch.empty(int(lib().pcc_split_slice_bytes(n, l)), dtype=torch.uint8, device=u.device)
-            self.scale = torch.empty(self.rows, dtype=torch.float64, device=u.device)
+            self.slices = torch.empty(int(lib().pcc_split_slice_bytes(n, l)), dtype=torch.uint8, device=dev)
+            self.scale = torch.empty(self.rows, dtype=torch.float64, device=dev)
+
+    def normalize_split(self, x, ldx: int, flags, row_lo: int, row_hi: int, stream) -> None:
+        """Split method without U: normalise rows [row_lo, row_hi) of the
+        device matrix ``x`` straight into the digit planes
+        (``pcc_normalize_split_rows_f64``: the same bits as K1 followed by
+        ``prepare``); a range ending at row n also clears the pad rows."""
+        check(lib().pcc_normalize_split_rows_f64(x.data_ptr(), ldx, self.n, self.l, flags.data_ptr(), row_lo, row_hi,
+                                                 self.slices.data_ptr(), self.scale.data_ptr(), stream),
+              "normalize_split")
 
     def prepare(self, row_lo: int, row_hi: int, stream) -> None:
         if self.method != "split" or row_hi <= row_lo:

@@ -202,7 +202,14 @@ struct NormDests {
   double *u[kMaxNormDests];
   uint8_t *flags[kMaxNormDests];
   int n;
+  // kNormDigits mode (split mode, csrc/split.cuh): the normalised rows go
+  // straight into int8 radix-128 digit planes [KB][7][rows_total][64] and
+  // a power-of-two scale per row -- U itself is never written
+  int8_t *slices;
+  double *scale;
+  int64_t rows_total;
 };
+constexpr int kNormLocal = 0, kNormBcast = 1, kNormDigits = 2;
 
 __device__ __forceinline__ void bulk_copy_row(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
@@ -210,7 +217,7 @@ __device__ __forceinline__ void bulk_copy_row(uint32_t dst, const void *src, uin
                : "memory");
 }
 
-template <int kNormSmemThreads, bool BCAST = false>
+template <int kNormSmemThreads, int MODE = kNormLocal>
 __global__ void __launch_bounds__(kNormSmemThreads)
 normalize_rows_smem_kernel(const double *__restrict__ x, int64_t ldx, double *__restrict__ u, int64_t ldu,
                            uint8_t *__restrict__ zero_variance, int64_t l, int64_t row_lo, int64_t row_hi,
@@ -291,7 +298,7 @@ normalize_rows_smem_kernel(const double *__restrict__ x, int64_t ldx, double *__
     s_zero[row] = zero;
     s_mean[row] = mean;
     s_scale[row] = zero ? 0.0 : __dsqrt_rn(q);
-    if (BCAST) {
+    if (MODE == kNormBcast) {
       for (int d = 0; d < dests.n; ++d) dests.flags[d][r0 + row] = zero ? 1 : 0;
     } else {
       zero_variance[r0 + row] = zero ? 1 : 0;
@@ -300,12 +307,67 @@ normalize_rows_smem_kernel(const double *__restrict__ x, int64_t ldx, double *__
   __syncthreads();
   K1_MARK(1);
 
+  if (MODE == kNormDigits) {
+    // 3'. digit planes instead of U: per row the exact max |u| = RN(max |x -
+    //     mean| / scale) (division is monotone), its power-of-two scale, then
+    //     each thread turns 4 consecutive u values -- the same IEEE
+    //     operations as below, so the same bits as K1 + pcc_split_rows_f64 --
+    //     into 7 radix-128 digits, one 32-bit store per digit plane
+    __shared__ double s_wmax[kNormSmemThreads / 32];
+    constexpr int W = 64;  // SplitCfg::kRowBytes
+    const int64_t kpad = (l + W - 1) / W * W;
+    const int64_t plane = dests.rows_total * W;
+    for (int r = 0; r < rows; ++r) {
+      const double *ds = srow + (int64_t)r * l;
+      const bool zero = s_zero[r] != 0;
+      const double m0 = s_mean[r], sc = s_scale[r];
+      double dm = 0.0;
+      if (!zero)
+        for (int64_t k = tid; k < l; k += kNormSmemThreads) dm = fmax(dm, fabs(__dsub_rn(ds[k], m0)));
+#pragma unroll
+      for (int o = 16; o; o >>= 1) dm = fmax(dm, __shfl_xor_sync(0xffffffffu, dm, o));
+      if ((tid & 31) == 0) s_wmax[tid >> 5] = dm;
+      __syncthreads();
+      dm = 0.0;
+#pragma unroll
+      for (int w = 0; w < kNormSmemThreads / 32; ++w) dm = fmax(dm, s_wmax[w]);
+      __syncthreads();  // s_wmax is reused by the next row
+      const double m = zero ? 0.0 : __ddiv_rn(dm, sc);
+      int e = 0;
+      if (m > 0.0) {
+        frexp(m, &e);
+        if (ldexp(m, 7 - e) >= 127.5) ++e;  // keep the leading digit within [-127, 127]
+      }
+      if (tid == 0) dests.scale[r0 + r] = m > 0.0 ? ldexp(1.0, e - 7) : 0.0;
+      const double pw = m > 0.0 ? ldexp(1.0, 7 - e) : 0.0;  // 7 - e <= 14 for unit-norm rows
+      for (int64_t k = 4 * (int64_t)tid; k < kpad; k += 4 * kNormSmemThreads) {
+        uint32_t packed[7] = {};
+        if (m > 0.0) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            double v = (k + j < l) ? __ddiv_rn(__dsub_rn(ds[k + j], m0), sc) * pw : 0.0;
+#pragma unroll
+            for (int i = 0; i < 7; ++i) {
+              const double d = rint(v);
+              v = (v - d) * 128.0;  // exact
+              packed[i] |= ((uint32_t)(int32_t)d & 0xFFu) << (8 * j);
+            }
+          }
+        }
+        int8_t *dst = dests.slices + (k / W) * 7 * plane + (r0 + r) * W + (k % W);
+#pragma unroll
+        for (int i = 0; i < 7; ++i) *reinterpret_cast<uint32_t *>(dst + i * plane) = packed[i];
+      }
+    }
+    return;
+  }
+
   // 3. write U rows (coalesced): u = (x - mean) / scale, zero rows for zero
   //    variance, zero K padding
   for (int r = 0; r < rows; ++r) {
     const int64_t off = (r0 + r) * ldu;
     auto put = [&](int64_t k, double v) {  // one store, or one per destination
-      if (BCAST) {
+      if (MODE == kNormBcast) {
         for (int d = 0; d < dests.n; ++d) dests.u[d][off + k] = v;
       } else {
         u[off + k] = v;

@@ -456,7 +456,7 @@ int launch_syrk(const double *u, int64_t n, int64_t l, int64_t ldu, uint64_t tb,
 // Shared-memory-staged K1 launch (the default whenever a row fits), single
 // destination or broadcast to dests; kNotStaged if the row is too long.
 constexpr int kNotStaged = -1;
-template <bool BCAST>
+template <int MODE>
 int launch_normalize_staged(const double *x, int64_t ldx, double *u, int64_t ldu, uint8_t *zero_variance, int64_t l,
                             int64_t row_lo, int64_t row_hi, const pcc::NormDests &dests, cudaStream_t stream) {
   const uint64_t rows = (uint64_t)(row_hi - row_lo);
@@ -465,9 +465,9 @@ int launch_normalize_staged(const double *x, int64_t ldx, double *u, int64_t ldu
   static std::once_flag attr_once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(attr_once, [] {
-    const void *fns[] = {(const void *)pcc::normalize_rows_smem_kernel<64, BCAST>,
-                         (const void *)pcc::normalize_rows_smem_kernel<128, BCAST>,
-                         (const void *)pcc::normalize_rows_smem_kernel<256, BCAST>};
+    const void *fns[] = {(const void *)pcc::normalize_rows_smem_kernel<64, MODE>,
+                         (const void *)pcc::normalize_rows_smem_kernel<128, MODE>,
+                         (const void *)pcc::normalize_rows_smem_kernel<256, MODE>};
     for (const void *f : fns)
       if (attr_err == cudaSuccess)
         attr_err = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmPerSmem);
@@ -505,7 +505,7 @@ int launch_normalize_staged(const double *x, int64_t ldx, double *u, int64_t ldu
   static int regs = 0;
   if (regs == 0) {
     cudaFuncAttributes fa;
-    regs = cudaFuncGetAttributes(&fa, pcc::normalize_rows_smem_kernel<256, BCAST>) == cudaSuccess ? fa.numRegs : 72;
+    regs = cudaFuncGetAttributes(&fa, pcc::normalize_rows_smem_kernel<256, MODE>) == cudaSuccess ? fa.numRegs : 72;
   }
   const int64_t occ_smem = (228 * 1024) / ((int64_t)smem + 1024);
   int threads = 64;
@@ -518,13 +518,13 @@ int launch_normalize_staged(const double *x, int64_t ldx, double *u, int64_t ldu
   const uint64_t grid = ceil_div(rows, (uint64_t)per_cta);
   if (grid > 0x7FFFFFFFull) return fail(PCC_EINVAL, "too many rows");
   if (threads == 256)
-    pcc::normalize_rows_smem_kernel<256, BCAST><<<(unsigned)grid, 256, smem, stream>>>(
+    pcc::normalize_rows_smem_kernel<256, MODE><<<(unsigned)grid, 256, smem, stream>>>(
         x, ldx, u, ldu, zero_variance, l, row_lo, row_hi, per_cta, dests);
   else if (threads == 128)
-    pcc::normalize_rows_smem_kernel<128, BCAST><<<(unsigned)grid, 128, smem, stream>>>(
+    pcc::normalize_rows_smem_kernel<128, MODE><<<(unsigned)grid, 128, smem, stream>>>(
         x, ldx, u, ldu, zero_variance, l, row_lo, row_hi, per_cta, dests);
   else
-    pcc::normalize_rows_smem_kernel<64, BCAST><<<(unsigned)grid, 64, smem, stream>>>(
+    pcc::normalize_rows_smem_kernel<64, MODE><<<(unsigned)grid, 64, smem, stream>>>(
         x, ldx, u, ldu, zero_variance, l, row_lo, row_hi, per_cta, dests);
   PCC_CUDA(cudaGetLastError(), "normalize_rows_smem_kernel launch");
   return PCC_OK;
@@ -586,7 +586,7 @@ int pcc_normalize_rows_f64(const double *x, int64_t ldx, double *u, int64_t ldu,
   }();
   if (mode == 1) {
     const pcc::NormDests none{};
-    const int rc = launch_normalize_staged<false>(x, ldx, u, ldu, zero_variance, l, row_lo, row_hi, none,
+    const int rc = launch_normalize_staged<pcc::kNormLocal>(x, ldx, u, ldu, zero_variance, l, row_lo, row_hi, none,
                                                   (cudaStream_t)stream);
     if (rc != kNotStaged) return rc;
   }
@@ -618,10 +618,43 @@ int pcc_normalize_rows_bcast_f64(const double *x, int64_t ldx, double *const *u,
     d.flags[i] = zero_variance[i];
   }
   if (row_hi == row_lo) return PCC_OK;
-  const int rc = launch_normalize_staged<true>(x, ldx, nullptr, ldu, nullptr, l, row_lo, row_hi, d,
+  const int rc = launch_normalize_staged<pcc::kNormBcast>(x, ldx, nullptr, ldu, nullptr, l, row_lo, row_hi, d,
                                                (cudaStream_t)stream);
   if (rc == kNotStaged)
     return fail(PCC_EINVAL, "rows of %lld samples are too long for the broadcast normaliser", (long long)l);
+  return rc;
+}
+
+int pcc_normalize_split_rows_f64(const double *x, int64_t ldx, int64_t n, int64_t l, uint8_t *zero_variance,
+                                 int64_t row_lo, int64_t row_hi, int8_t *slices, double *scale, void *stream) {
+  if (l < 2) return fail(PCC_EINVAL, "need at least 2 samples per variable, got %lld", (long long)l);
+  if (l > pcc::SplitCfg::kMaxL)
+    return fail(PCC_EINVAL, "split mode is bounded to l <= %lld (got %lld)", (long long)pcc::SplitCfg::kMaxL,
+                (long long)l);
+  if (ldx < l) return fail(PCC_EINVAL, "ldx (%lld) must be >= l (%lld)", (long long)ldx, (long long)l);
+  if (n < 1 || row_lo < 0 || row_hi < row_lo || row_hi > n)
+    return fail(PCC_EINVAL, "bad row range [%lld, %lld) for n = %lld", (long long)row_lo, (long long)row_hi,
+                (long long)n);
+  if (!x || !zero_variance || !slices || !scale) return fail(PCC_EINVAL, "null pointer");
+  if (reinterpret_cast<uintptr_t>(slices) % 16 != 0) return fail(PCC_EINVAL, "slices must be 16-byte aligned");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t rows_total = pcc_rows_padded(n);
+  constexpr int64_t W = pcc::SplitCfg::kRowBytes;
+  if (row_hi == n && rows_total > n) {  // the range ends at the last row: pad rows get zero digits and scale 0
+    const int64_t kb = (l + W - 1) / W;
+    PCC_CUDA(cudaMemset2DAsync(slices + n * W, (size_t)(rows_total * W), 0, (size_t)((rows_total - n) * W),
+                               (size_t)(kb * pcc::SplitCfg::kSlices), s),
+             "cudaMemset2DAsync(pad digit rows)");
+    PCC_CUDA(cudaMemsetAsync(scale + n, 0, (size_t)(rows_total - n) * sizeof(double), s), "cudaMemsetAsync(pad scales)");
+  }
+  if (row_hi == row_lo) return PCC_OK;
+  pcc::NormDests d{};
+  d.slices = slices;
+  d.scale = scale;
+  d.rows_total = rows_total;
+  const int rc = launch_normalize_staged<pcc::kNormDigits>(x, ldx, nullptr, 0, zero_variance, l, row_lo, row_hi, d, s);
+  if (rc == kNotStaged)
+    return fail(PCC_EINVAL, "rows of %lld samples are too long for the fused normaliser", (long long)l);
   return rc;
 }
 

@@ -214,8 +214,8 @@ def run_stream(x, n: int, l: int, device: torch.device, tile_begin: int, tile_en
     the multi-GPU row exchange); ``x`` is then ignored and only the
     contraction passes and downloads run (top-down, no upload phase).
     ``method``: the contraction (``_lib.METHODS``; ``"exact"`` = the bit-exact
-    dot8 kernel, ``"split"`` = int8 digit planes made chunk by chunk right
-    after each chunk's normalisation).
+    dot8 kernel, ``"split"`` = int8 digit planes written chunk by chunk by
+    the normaliser itself -- no U; the returned ``u`` is then None).
     Returns ``(u, flags, x_device)`` after the host has synchronised
     (``x_device`` is None with ``resident``).
     """
@@ -238,13 +238,17 @@ def run_stream(x, n: int, l: int, device: torch.device, tile_begin: int, tile_en
         if resident is not None:
             u, flags = resident
             ldu = int(u.shape[1])
+        elif method == "split":
+            # no U: each chunk is normalised straight into the digit planes
+            u, ldu = None, 0
+            flags = torch.zeros(n, dtype=torch.uint8, device=device)
         else:
             rows_pad = int(L.pcc_rows_padded(n))
             ldu = int(L.pcc_ldu(l))
             u = torch.empty((rows_pad, ldu), dtype=torch.float64, device=device)
             flags = torch.zeros(n, dtype=torch.uint8, device=device)
             _lib.check(L.pcc_zero_rows_f64(ptr(u), ldu, n, rows_pad, s), "pad rows")
-        con = _lib.Contraction(method, u, n, l)
+        con = _lib.Contraction(method, u, n, l, device=device)
         if resident is not None:
             con.prepare_all(s)
 
@@ -350,10 +354,11 @@ def run_stream(x, n: int, l: int, device: torch.device, tile_begin: int, tile_en
                 if not pinned_in:
                     stage_in_ev[c % 2] = up
                 compute.wait_event(up)
-            if resident is None:
+            if resident is None and u is None:
+                con.normalize_split(xd, xd.stride(0), flags, lo, hi, s)
+            elif resident is None:
                 _lib.check(L.pcc_normalize_rows_f64(ptr(xd), xd.stride(0), ptr(u), ldu, ptr(flags), l, lo, hi, s),
                            "normalize")
-                con.prepare(lo, hi, s)
             normed = torch.cuda.Event()
             normed.record(compute)
             # every pass whose rows are now normalised, in plan order

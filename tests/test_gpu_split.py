@@ -304,3 +304,31 @@ def test_split_to_file_and_pipeline_sink(tmp_path, rng):
     with pc.PackedFileWriterSink(tmp_path / "p.lpcr", g, nd.zero_variance) as sink:
         pc.run_pipeline(nd, g, pc.plan_passes(0, g.total_tiles, 5000), sink, **SPLIT)
     assert np.array_equal(pc.load_result(tmp_path / "p.lpcr").packed, ref)
+
+
+@pytest.mark.parametrize("n,l", [(300, 77), (1, 2), (129, 64), (257, 8192), (1000, 1531)])
+def test_fused_normaliser_writes_the_same_digit_planes(rng, n, l):
+    """pcc_normalize_split_rows_f64 (K1 straight into digit planes, no U) vs
+    K1 + pcc_split_rows_f64: the same flags, scales and digit bytes, pad rows
+    and K padding zero; chunked calls (bottom chunk first) give the same."""
+    L = _lib.lib()
+    x = random_values(rng, n, l, special_rows=True)
+    xd = torch.from_numpy(x).cuda()
+    u = _normalized(x)
+    ref = _lib.Contraction("split", u, n, l).prepare_all(torch.cuda.current_stream().cuda_stream)
+    zv_ref = pc.normalize(pc.Dataset(values=x)).zero_flags
+    s = torch.cuda.current_stream().cuda_stream
+    for cuts in ([0, n], sorted({0, n // 3, (2 * n) // 3, n})):
+        con = _lib.Contraction("split", None, n, l, device=xd.device)
+        con.slices.fill_(0x55)
+        con.scale.fill_(float("nan"))
+        flags = torch.full((n,), 7, dtype=torch.uint8, device="cuda")
+        for lo, hi in reversed(list(zip(cuts, cuts[1:]))):
+            con.normalize_split(xd, l, flags, lo, hi, s)
+        torch.cuda.synchronize()
+        assert torch.equal(con.slices, ref.slices)
+        assert torch.equal(con.scale, ref.scale)
+        assert torch.equal(flags.bool().cpu(), zv_ref.bool().cpu())
+    rc = L.pcc_normalize_split_rows_f64(xd.data_ptr(), l, n, l, flags.data_ptr(), 0, n + 1, con.slices.data_ptr(),
+                                        con.scale.data_ptr(), None)
+    assert rc == 1
