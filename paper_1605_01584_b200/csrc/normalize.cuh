@@ -348,9 +348,10 @@ normalize_rows_smem_kernel(const double *__restrict__ x, int64_t ldx, double *__
             double v = (k + j < l) ? __ddiv_rn(__dsub_rn(ds[k + j], m0), sc) * pw : 0.0;
 #pragma unroll
             for (int i = 0; i < 7; ++i) {
-              const double d = rint(v);
-              v = (v - d) * 128.0;  // exact
-              packed[i] |= ((uint32_t)(int32_t)d & 0xFFu) << (8 * j);
+              const double t = __dadd_rn(v, 0x1.8p52);  // rint by the 1.5 * 2^52 shift
+              const double d = __dsub_rn(t, 0x1.8p52);
+              v = __dmul_rn(__dsub_rn(v, d), 128.0);   // exact
+              packed[i] |= ((uint32_t)__double2loint(t) & 0xFFu) << (8 * j);
             }
           }
         }
