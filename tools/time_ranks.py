@@ -13,6 +13,7 @@ from paper_1605_01584_b200.workloads import CONFIGS, make_config
 
 p = argparse.ArgumentParser(); p.add_argument("--configs", default="c1,c2,c3"); p.add_argument("--reps", type=int, default=3)
 p.add_argument("--ps", default="1,2,4,8")
+p.add_argument("--method", default="tensor", choices=("tensor", "split"))
 a = p.parse_args()
 L = _lib.lib()
 for cfg in a.configs.split(","):
@@ -35,12 +36,21 @@ for cfg in a.configs.split(","):
                 continue
             lo, hi = shard_span(n, tb, te)
             out = torch.empty(hi - lo, dtype=torch.float64, device="cuda")
-            def step():
-                u, f = normalize_device(x)
-                _lib.check(L.pcc_syrk_f64(ptr(u), n, l, u.shape[1], tb, te, 0, ptr(out), 0, lo, 0, 0, 0, stream_handle()))
+            if a.method == "split":
+                flags = torch.empty(n, dtype=torch.uint8, device="cuda")
+
+                def step():  # K1 fused with the digit planes + the split contraction
+                    con = _lib.Contraction("split", None, n, l, device=x.device)
+                    con.normalize_split(x, l, flags, 0, n, stream_handle())
+                    con.syrk(tb, te, 0, ptr(out), 0, lo, 0, 0, 0, stream_handle())
+            else:
+                def step():
+                    u, f = normalize_device(x)
+                    _lib.check(L.pcc_syrk_f64(ptr(u), n, l, u.shape[1], tb, te, 0, ptr(out), 0, lo, 0, 0, 0,
+                                              stream_handle()))
             worst = max(worst, timed(step))
             del out
         if P == 1:
             t1 = worst
-        print(f"{cfg} p={P}: max rank step {worst:9.3f} ms   efficiency {t1 / (P * worst) * 100:6.1f}%", flush=True)
+        print(f"{cfg} {a.method} p={P}: max rank step {worst:9.3f} ms   efficiency {t1 / (P * worst) * 100:6.1f}%", flush=True)
     del x; torch.cuda.empty_cache()
