@@ -1,31 +1,37 @@
 #!/usr/bin/env python
 """Benchmark of the all-pairs PCC hot path on B200 (BASELINE.json's metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--config c2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--config c4]
     python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 ... bench.py --gpus N
 
-One step = one pass of the hot path over the config's synthetic dataset:
-K1 normalisation of all n rows + K2 symmetric contraction of this rank's
-contiguous share of the GPU tile jobs (partition(T, N), distributed.py:76-92)
-with the packed epilogue.  Inputs are resident in HBM before the timed
-region; X and U (>= 537 MB at c2) exceed the 126 MB L2, so no flush is
-needed between steps.  Timing is CUDA events on the launching stream, W
-untimed warm-up steps, K timed steps between barrier+synchronize, max over
-ranks.  ``e2e`` times the public API (``allpairs`` / the per-worker shard
-call) with the pinned-host upload of X and the download of this rank's
-packed cells inside the timed region; for N > 1 each rank uploads only its
-row block of X and the normalised blocks are all-gathered over NCCL
-(distributed.exchange_normalize) before the contraction.
+Headline workload: c4 (n = 32,768 x l = 8,192 FP64), the configuration
+BASELINE.json quotes "at 1/2/4/8 GPUs" and the largest that fits one GPU;
+c2 is measured beside it (``extra_configs``).
 
-``--impl reference`` times the reference algorithm's CPU implementation
-(the bit-exact C port under oracle/, all host threads) on a bounded sample
-of the same workload -- the reference itself is Python+numba and not
-installable on the box.  Only rank 0 runs it.
+One step = one pass of the hot path over the config's synthetic dataset:
+K1 normalisation of the rows this rank's tiles read + K2 symmetric
+contraction of this rank's contiguous share of the GPU tile jobs
+(partition(T, N), distributed.py:76-92) with the packed epilogue.  Inputs
+are resident in HBM before the timed region; X and U (2.15 GB each at c4) exceed the
+126 MB L2, so no flush is needed between steps.  Timing is CUDA events on
+the launching stream, W untimed warm-up steps, K timed steps between
+barrier+synchronize, max over ranks.  ``e2e`` times the public API
+(``allpairs`` / the per-worker shard call) with the pinned-host upload of X
+and the download of this rank's packed cells inside the timed region; for
+N > 1 each rank uploads only its row block of X and one broadcast K1 kernel
+writes the normalised rows into every rank's U over peer memory.
+
+``--impl reference`` times the reference itself -- ``paircorr`` installed
+unmodified in baseline/_ref, its stock ``allpairs`` code path (normalize +
+run_pipeline over plan_passes + ResultAssembler, all host threads) -- on a
+bounded tile-id prefix of the same workload, and the bit-exact C port under
+oracle/ beside it.  Only rank 0 runs it.
 """
 
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -43,7 +49,9 @@ sys.path.insert(0, str(ROOT))
 # best measured int8 tcgen05.mma throughput on this pool's B200 (tools/i8_mma.cu,
 # profiles/r01_i8_mma_peak.log); MEASURED_PEAKS.json carries no int8 figure
 I8_PEAK_TOPS = 4122.9
-DEFAULT_CONFIG = "c2"  # BASELINE.json configs[1]: the single-GPU headline configuration
+DEFAULT_CONFIG = "c4"  # BASELINE.json configs[3]: quoted at 1/2/4/8 GPUs, the largest single-GPU config
+EXTRA_CONFIGS = "c2"  # device step also measured on these (configs[1])
+REF_DIR = ROOT / "baseline" / "_ref"
 
 
 def _env_int(name: str, default: int) -> int:
@@ -64,35 +72,50 @@ def parse_args(argv=None):
     p.add_argument("--no-split", action="store_true", help="skip the split-mode (int8 tensor core) measurement")
     p.add_argument("--no-pageable", action="store_true", help="skip the numpy-in / numpy-out e2e measurement")
     p.add_argument("--cpu-fraction", type=float, default=None,
-                   help="fraction of the reference t=4 tile range in the CPU sample")
+                   help="fraction of the reference t=4 tile range in the CPU sample (default: sized by time)")
+    p.add_argument("--ref-seconds", type=float, default=None,
+                   help="target seconds of host work per reference-arm step (default 4; cpu_baseline 12)")
+    p.add_argument("--extra-configs", default=EXTRA_CONFIGS,
+                   help="comma-separated configs whose device step is measured beside the headline ('' = none)")
+    p.add_argument("--u-exchange", choices=("local", "p2p"), default="local",
+                   help="N > 1 device step: 'local' = each rank normalises the rows its tiles read from its "
+                        "resident X; 'p2p' = each rank normalises its 1/N row block and one broadcast K1 kernel "
+                        "writes it into every rank's U over peer memory")
     return p.parse_args(argv)
 
 
-# --------------------------------------------------------------------------- CPU (oracle) leg
+# --------------------------------------------------------------------------- CPU legs
+
+def _prefix_pairs(n: int, t: int, hi: int) -> int:
+    """Cells y <= x < n inside reference t x t tiles [0, hi) (whole tile rows + a partial one)."""
+    from paper_1605_01584_b200.indexing import sym_job_coord
+
+    m = -(-n // t)
+    yt, xt = sym_job_coord(m, hi - 1)
+    pairs = 0
+    for r in range(yt + 1):
+        x_last = m - 1 if r < yt else xt
+        x_hi = min(n, (x_last + 1) * t)
+        for ry in range(t):
+            y = r * t + ry
+            if y >= n:
+                break
+            pairs += max(0, x_hi - max(y, r * t))
+    return pairs
+
 
 def cpu_sample(x: np.ndarray, fraction: float, threads: int) -> dict:
-    """Time the reference algorithm (bit-exact C port) on the host: normalize
-    all rows, then compute+scatter the first ``fraction`` of the t=4 tile range
-    (engine.py:46-52 with capacity = the sample).  Returns pairs/s."""
+    """Time the bit-exact C port of the reference (oracle/) on the host:
+    normalize all rows, then compute+scatter the first ``fraction`` of the
+    t=4 tile range (engine.py:46-52 with capacity = the sample)."""
     import oracle
-    from paper_1605_01584_b200.indexing import sym_job_coord
 
     n, l = x.shape
     t = 4
     m = -(-n // t)
     total = m * (m + 1) // 2
     hi = max(1, int(total * fraction))
-    # cells (y <= x < n) inside tiles [0, hi): whole tile rows + a partial one
-    yt, xt = sym_job_coord(m, hi - 1)
-    pairs = 0
-    for r in range(yt + 1):
-        x_last = m - 1 if r < yt else xt
-        for ry in range(t):
-            y = r * t + ry
-            if y >= n:
-                break
-            x_hi = min(n, (x_last + 1) * t)
-            pairs += max(0, x_hi - max(y, r * t))
+    pairs = _prefix_pairs(n, t, hi)
     t0 = time.perf_counter()
     u, _ = oracle.normalize(x, threads=threads)
     flat = oracle.compute_pass(u, t, 0, hi, threads=threads)
@@ -100,6 +123,83 @@ def cpu_sample(x: np.ndarray, fraction: float, threads: int) -> dict:
     oracle.scatter_range(packed, flat, 0, hi, m, t, n)
     dt = time.perf_counter() - t0
     return {"pairs": pairs, "seconds": dt, "pairs_per_s": pairs / dt, "tiles": hi, "total_tiles": total}
+
+
+def import_paircorr():
+    """The unmodified reference package from baseline/_ref (its numba cache
+    redirected out of the tree), or (None, reason)."""
+    if not (REF_DIR / "paircorr" / "__init__.py").exists():
+        return None, ("baseline/_ref/paircorr is not installed (python -m pip install --no-index --no-build-isolation "
+                      "--no-deps --target baseline/_ref <copy of /root/reference/pkg>)")
+    os.environ.setdefault("NUMBA_CACHE_DIR", os.path.join(tempfile.gettempdir(), "pcc_numba_cache"))
+    if str(REF_DIR) not in sys.path:
+        sys.path.insert(0, str(REF_DIR))
+    try:
+        import paircorr
+    except Exception as exc:  # noqa: BLE001 - reported in the JSON line
+        return None, f"import paircorr failed: {type(exc).__name__}: {exc}"
+    return paircorr, None
+
+
+class ReferenceSample:
+    """``paircorr.allpairs``'s stock single-worker path (engine.py:46-52):
+    ``normalize`` + ``run_pipeline(plan_passes(0, hi, default_capacity))``
+    into a ``ResultAssembler``, all host threads, over the tile-id prefix
+    [0, hi) of the reference's t = 4 tile matrix -- a bounded sample of the
+    same workload (tile jobs are equal-cost)."""
+
+    T = 4
+
+    def __init__(self, pc, x: np.ndarray, threads: int):
+        from paircorr.pipeline import ResultAssembler, plan_passes, run_pipeline
+
+        self.pc, self.threads = pc, threads
+        self._plan, self._run = plan_passes, run_pipeline
+        # JIT warm-up on a tiny input first (as test_acceptance.py:268-272)
+        pc.allpairs(pc.Dataset(np.random.default_rng(0).random((16, 16))), threads=threads)
+        self.ds = pc.Dataset(values=x)
+        self.n = x.shape[0]
+        self.geom = pc.TileGeometry(n=self.n, t=self.T)
+        self.capacity = pc.default_capacity(self.T)
+        self.asm = ResultAssembler(self.geom)  # one packed result, reused by every step
+
+    def run(self, hi: int) -> float:
+        t0 = time.perf_counter()
+        u = self.pc.normalize(self.ds, threads=self.threads)
+        self._run(u, self.geom, self._plan(0, hi, self.capacity), self.asm, threads=self.threads)
+        return time.perf_counter() - t0
+
+    def size_for(self, seconds: float) -> int:
+        """Tile prefix taking about ``seconds`` (one probe run; normalisation is a fixed cost)."""
+        total = self.geom.total_tiles
+        probe = max(1, min(total, total // 400))
+        t_norm = self.run(1)
+        t_probe = self.run(probe)
+        rate = probe / max(1e-6, t_probe - t_norm)
+        return int(max(1, min(total, (seconds - t_norm) * rate)))
+
+    def describe(self, hi: int, extra: str = "") -> str:
+        return (f"paircorr {getattr(self.pc, '__version__', '0.1.0')} from baseline/_ref (unmodified), stock allpairs "
+                f"path: normalize all {self.n} rows + run_pipeline(plan_passes(0, {hi}, {self.capacity})) + "
+                f"ResultAssembler over t=4 tiles [0, {hi}) of {self.geom.total_tiles} "
+                f"({_prefix_pairs(self.n, self.T, hi)} pairs), threads={self.threads}{extra}")
+
+
+def reference_baseline(x: np.ndarray, seconds: float, threads: int, reps: int = 1, warmup: int = 0) -> dict | None:
+    """One timed sample (median of ``reps``) of the real reference; None if it is not installed."""
+    pc, why = import_paircorr()
+    if pc is None:
+        return {"unavailable": why}
+    rs = ReferenceSample(pc, x, threads)
+    hi = rs.size_for(seconds)
+    for _ in range(warmup):
+        rs.run(hi)
+    secs = [rs.run(hi) for _ in range(reps)]
+    med = statistics.median(secs)
+    pairs = _prefix_pairs(rs.n, rs.T, hi)
+    return {"value": pairs / med, "unit": "pairs/s", "cores": threads, "kind": "reference",
+            "seconds": med, "steps": reps, "tiles": hi,
+            "sample": rs.describe(hi, f"; median of {reps} in {med:.2f} s, extrapolated as a rate")}
 
 
 def run_reference(args, rank: int, world: int) -> None:
@@ -111,39 +211,52 @@ def run_reference(args, rank: int, world: int) -> None:
     spec = CONFIGS[args.config]
     x = make_config(args.config)
     threads = oracle.default_threads()
-    frac = args.cpu_fraction or _default_ref_fraction(args.config)
-    for _ in range(args.warmup):
-        cpu_sample(x, frac / 4, threads)
-    samples = [cpu_sample(x, frac, threads) for _ in range(args.steps)]
-    secs = [s["seconds"] for s in samples]
-    pairs = samples[0]["pairs"]
-    value = pairs / statistics.median(secs)
-    sample_desc = (f"normalize all {spec.n} rows + compute_tile_range/scatter_range of reference t=4 tiles "
-                   f"[0, {samples[0]['tiles']}) of {samples[0]['total_tiles']} ({pairs} pairs), median of {len(secs)}")
-    line = {
+    base = {
         "impl": "reference",
         "metric": "pairs_per_sec",
-        "value": value,
         "unit": "pairs/s",
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": statistics.median(secs) * 1e3,
         "higher_is_better": True,
         "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic",
         "config": _config_dict(args.config, world),
-        "gflops": 2.0 * spec.l * pairs / statistics.median(secs) / 1e9,
-        "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": threads, "kind": "port", "sample": sample_desc},
-        "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    # the bit-exact C port beside it (oracle/; ~2.9x faster than numba paircorr)
+    frac = args.cpu_fraction or _default_ref_fraction(args.config)
+    port = cpu_sample(x, frac, threads)
+    port_line = {"value": port["pairs_per_s"], "unit": "pairs/s", "cores": threads, "kind": "port",
+                 "sample": f"bit-exact C port (oracle/): normalize + t=4 tiles [0, {port['tiles']}) of "
+                           f"{port['total_tiles']} = {port['pairs']} pairs in {port['seconds']:.2f} s"}
+    pc, why = import_paircorr()
+    if pc is None:
+        # fall back to the port as the timed reference implementation
+        value = port["pairs_per_s"]
+        line = dict(base, value=value, ms_per_step=port["seconds"] * 1e3,
+                    gflops=2.0 * spec.l * port["pairs"] / port["seconds"] / 1e9,
+                    cpu_baseline=dict(port_line), reference_unavailable=why)
+    else:
+        rs = ReferenceSample(pc, x, threads)
+        hi = rs.size_for(args.ref_seconds or 4.0)
+        for _ in range(args.warmup):
+            rs.run(max(1, hi // 8))
+        secs = [rs.run(hi) for _ in range(args.steps)]
+        med = statistics.median(secs)
+        pairs = _prefix_pairs(rs.n, rs.T, hi)
+        value = pairs / med
+        line = dict(base, value=value, ms_per_step=med * 1e3, gflops=2.0 * spec.l * pairs / med / 1e9,
+                    cpu_baseline={"value": value, "unit": "pairs/s", "cores": threads, "kind": "reference",
+                                  "sample": rs.describe(hi, f"; median of {len(secs)} steps")},
+                    port_baseline=port_line)
+    line["e2e"] = {"value": line["value"], "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
     print(json.dumps(line), flush=True)
 
 
 def _default_ref_fraction(cfg: str) -> float:
-    # ~3 s of 16-thread CPU work per step (the whole --steps/--warmup run ends within ~1 minute)
+    # ~3-10 s of 16-thread work for the C port
     return {"c1": 1.0, "c2": 1 / 4, "c3": 1.0, "c4": 1 / 64, "c5": 1 / 64}[cfg]
 
 
@@ -162,7 +275,9 @@ def _config_dict(cfg: str, world: int) -> dict:
         "parallelism": (f"tile-range partition over {world} GPU(s); device step: every rank normalises the "
                         "rows it needs from its resident X, no collective"
                         + ("; e2e: row-block upload + K1 broadcast of U over peer memory" if world > 1 else "")),
-        "l2_policy": "inputs larger than L2 (X and U >= 537 MB vs 126 MB L2); no flush",
+        "l2_policy": (f"inputs larger than L2 (X and U {spec.n * spec.l * 8 / 1e6:.0f} MB each vs 126 MB L2); no flush"
+                      if spec.n * spec.l * 8 > 126e6 else
+                      f"X and U ({spec.n * spec.l * 8 / 1e6:.0f} MB each) fit the 126 MB L2; small-config figure only"),
         "output": "packed upper triangle n(n+1)/2 f64, sharded per GPU range, kept on device",
     }
 
@@ -249,6 +364,77 @@ def _load_traffic(cfg: str):
         return None
 
 
+def _device_exchange_label(mode: str) -> str:
+    if mode == "local":
+        return ("local: X resident on every rank (the reference's worker model, worker.py:68-80); each rank "
+                "normalises exactly the rows its tile range reads (rank 0: all), no collective")
+    return ("p2p: each rank normalises its 1/N row block; one broadcast K1 kernel stores it into every rank's U "
+            "over CUDA IPC peer mappings (NVLink), then a barrier")
+
+
+def _device_step_config(cfg: str, rank: int, world: int, dev, args, barrier, max_over_ranks, peak: float) -> dict:
+    """Device step (K1 of the rows this rank reads + K2 of its tile share) of
+    another BASELINE config, timed like the headline: K steps between
+    barrier + synchronize, CUDA events, max over ranks."""
+    import torch
+
+    from paper_1605_01584_b200 import _lib
+    from paper_1605_01584_b200._device import ptr, stream_handle
+    from paper_1605_01584_b200.distributed import owned_runs, partition, shard_span
+    from paper_1605_01584_b200.indexing import sym_job_coord
+    from paper_1605_01584_b200.workloads import CONFIGS, make_config
+
+    L = _lib.lib()
+    spec = CONFIGS[cfg]
+    n, l = spec.n, spec.l
+    x = torch.from_numpy(make_config(cfg)).to(dev)
+    T = int(L.pcc_gpu_tile_count(n))
+    tb, te = partition(T, world)[rank]
+    lo, hi = shard_span(n, tb, te)
+    shard = torch.empty(max(1, hi - lo), dtype=torch.float64, device=dev)
+    cells = sum(b - a for a, b in owned_runs(n, tb, te))
+    ldu, rows_pad = int(L.pcc_ldu(l)), int(L.pcc_rows_padded(n))
+    u = torch.empty((rows_pad, ldu), dtype=torch.float64, device=dev)
+    flags = torch.zeros(n, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+    s = stream_handle(stream)
+    _lib.check(L.pcc_zero_rows_f64(ptr(u), ldu, n, rows_pad, s), "pad rows")
+    need_lo = (sym_job_coord(-(-n // _lib.GPU_TILE), tb)[0] * _lib.GPU_TILE) if te > tb else n
+
+    def step(ev=None):
+        if need_lo < n:
+            _lib.check(L.pcc_normalize_rows_f64(ptr(x), l, ptr(u), ldu, ptr(flags), l, need_lo, n, s), "normalize")
+        if ev is not None:
+            ev[0].record(stream)
+        if te > tb:
+            _lib.check(L.pcc_syrk_f64(ptr(u), n, l, ldu, tb, te, _lib.LAYOUT_PACKED, ptr(shard), 0, lo, 0, 0, 0, s),
+                       "syrk")
+        if ev is not None:
+            ev[1].record(stream)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    t0.record(stream)
+    for i in range(args.steps):
+        step(evs[i])
+    t1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms = max_over_ranks(t0.elapsed_time(t1) / args.steps)
+    syrk_ms = sum(a.elapsed_time(b) for a, b in evs) / args.steps if te > tb else 0.0
+    ach = 2.0 * l * cells / (syrk_ms * 1e-3) / 1e12 if syrk_ms > 0 else 0.0
+    total = n * (n + 1) // 2
+    return {"workload": f"{cfg}: n={n} x l={l} FP64, {spec.description}", "value": total / (ms * 1e-3),
+            "unit": "pairs/s", "ms_per_step": ms, "steps": args.steps,
+            "gflops": float(n) * n * l / (ms * 1e-3) / 1e9, "syrk_ms": max_over_ranks(syrk_ms),
+            "roofline": {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+                         "frac": ach / peak if peak else None, "traffic": _load_traffic(cfg)}}
+
+
 # --------------------------------------------------------------------------- GPU leg
 
 def run_b200(args, rank: int, world: int, local_rank: int) -> None:
@@ -258,7 +444,8 @@ def run_b200(args, rank: int, world: int, local_rank: int) -> None:
     import paper_1605_01584_b200 as pc
     from paper_1605_01584_b200 import _lib
     from paper_1605_01584_b200._device import ptr, stream_handle
-    from paper_1605_01584_b200.distributed import partition, shard_span, owned_runs, compute_worker
+    from paper_1605_01584_b200.distributed import partition, shard_span, owned_runs, compute_worker, row_slices
+    from paper_1605_01584_b200.indexing import sym_job_coord
     from paper_1605_01584_b200.workloads import CONFIGS, make_config
     from paper_1605_01584_b200.transform import normalize_device
 
@@ -294,17 +481,67 @@ def run_b200(args, rank: int, world: int, local_rank: int) -> None:
     total_pairs = n * (n + 1) // 2
     stream = torch.cuda.current_stream()
     s = stream_handle(stream)
+    ldu = int(L.pcc_ldu(l))
+    rows_pad = int(L.pcc_rows_padded(n))
+
+    # K1 of the device step.  N = 1, or --u-exchange local: this rank
+    # normalises, from its resident X, exactly the rows its tile range reads
+    # (tile rows >= its first one; rank 0 reads all of them).  --u-exchange
+    # p2p: this rank normalises only its 1/N row block and one broadcast K1
+    # kernel stores the rows into every rank's U over peer memory (CUDA IPC
+    # mappings opened once, before the timed region), then a barrier.
+    exchange_mode = "local" if world == 1 else args.u_exchange
+    peers_opened = 0
+    need_lo = (sym_job_coord(-(-n // _lib.GPU_TILE), tb)[0] * _lib.GPU_TILE) if te > tb else n
+    if exchange_mode == "local":
+        u_dev = torch.empty((rows_pad, ldu), dtype=torch.float64, device=dev)
+        flags_dev = torch.zeros(n, dtype=torch.uint8, device=dev)
+        _lib.check(L.pcc_zero_rows_f64(ptr(u_dev), ldu, n, rows_pad, s), "pad rows")
+        k1_rows = n - need_lo
+
+        def k1():
+            if need_lo < n:
+                _lib.check(L.pcc_normalize_rows_f64(ptr(x), l, ptr(u_dev), ldu, ptr(flags_dev), l, need_lo, n, s),
+                           "normalize")
+    else:
+        slices, S = row_slices(n, world)
+        r0, r1 = slices[rank]
+        k1_rows = r1 - r0
+        ubuf = _lib.DeviceBuffer(world * S * ldu * 8)
+        fbuf = _lib.DeviceBuffer(world * S)
+        u_dev = ubuf.tensor((world * S, ldu), "<f8")
+        flags_dev = fbuf.tensor((world * S,), "|u1")
+        _lib.check(L.pcc_zero_rows_f64(ptr(u_dev), ldu, n, world * S, s), "pad rows")
+        flags_dev.zero_()
+        handles = [None] * world
+        dist.all_gather_object(handles, (ubuf.ipc_handle(), fbuf.ipc_handle()))
+        peer_bufs = {q: (_lib.DeviceBuffer(handle=hu), _lib.DeviceBuffer(handle=hf))
+                     for q, (hu, hf) in enumerate(handles) if q != rank}
+        peers_opened = 2 * len(peer_bufs)
+        torch.cuda.synchronize()
+        dist.barrier()
+        us = [ubuf.address if q == rank else peer_bufs[q][0].address for q in range(world)]
+        fs = [fbuf.address if q == rank else peer_bufs[q][1].address for q in range(world)]
+        uarr = (ctypes.c_void_p * world)(*[a + 8 * r0 * ldu for a in us])
+        farr = (ctypes.c_void_p * world)(*[a + r0 for a in fs])
+
+        def k1():
+            if r1 > r0:
+                _lib.check(L.pcc_normalize_rows_bcast_f64(ptr(x) + 8 * r0 * l, l, uarr, farr, world, ldu, l, 0,
+                                                          r1 - r0, s), "normalize+broadcast")
+            stream.synchronize()
+            dist.barrier()  # every rank's rows have landed in every U
 
     def step(ev_pair=None):
-        u, flags = normalize_device(x)
+        k1()
         if ev_pair is not None:
             ev_pair[0].record(stream)
         if te > tb:
-            _lib.check(L.pcc_syrk_f64(ptr(u), n, l, u.shape[1], tb, te, _lib.LAYOUT_PACKED, ptr(shard), 0,
+            _lib.check(L.pcc_syrk_f64(ptr(u_dev), n, l, ldu, tb, te, _lib.LAYOUT_PACKED, ptr(shard), 0,
                                       span_lo, 0, 0, 0, s), "syrk")
         if ev_pair is not None:
             ev_pair[1].record(stream)
-        return u, flags
+        return u_dev, flags_dev
 
     # warm-up (also the first-touch of the allocator)
     for _ in range(max(3, args.warmup)):
@@ -354,10 +591,10 @@ def run_b200(args, rank: int, world: int, local_rank: int) -> None:
         shard_x = torch.empty_like(shard)
 
         def step_exact(ev=None):
-            u, _ = normalize_device(x)
+            k1()
             if ev is not None:
                 ev[0].record(stream)
-            _lib.check(L.pcc_syrk_exact_f64(ptr(u), n, l, u.shape[1], tb, te, _lib.LAYOUT_PACKED, ptr(shard_x), 0,
+            _lib.check(L.pcc_syrk_exact_f64(ptr(u_dev), n, l, ldu, tb, te, _lib.LAYOUT_PACKED, ptr(shard_x), 0,
                                             span_lo, 0, 0, 0, s), "syrk_exact")
             if ev is not None:
                 ev[1].record(stream)
@@ -404,7 +641,7 @@ def run_b200(args, rank: int, world: int, local_rank: int) -> None:
             con = _lib.Contraction("split", None, n, l, device=dev)
             if ev is not None:
                 ev[0].record(stream)
-            con.normalize_split(x, l, flags_s, 0, n, s)
+            con.normalize_split(x, l, flags_s, need_lo, n, s)
             if ev is not None:
                 ev[1].record(stream)
             con.syrk(tb, te, _lib.LAYOUT_PACKED, ptr(shard_s), 0, span_lo, 0, 0, 0, s, "syrk_split")
@@ -531,24 +768,31 @@ def run_b200(args, rank: int, world: int, local_rank: int) -> None:
         e2e_pageable = {"value": total_pairs / t_np, "unit": "pairs/s", "ms_per_step": t_np * 1e3, "steps": 3,
                         "what": "allpairs(Dataset(numpy X)) returning a freshly allocated numpy result"}
 
-    # ---- CPU baseline (rank 0, N=1 only)
+    # ---- CPU baseline (rank 0, N=1 only): the reference itself (paircorr from
+    # baseline/_ref, stock allpairs path, all host threads) on a ~12 s tile
+    # prefix of the same X; the bit-exact C port (oracle/) if it is absent
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         import oracle
 
         threads = oracle.default_threads()
-        # ~10-30 s of host work: the whole c1/c2/c3 job, a prefix of c4/c5
-        frac = args.cpu_fraction or {"c1": 1.0, "c2": 1.0, "c3": 1.0, "c4": 1 / 16, "c5": 1 / 16}[args.config]
-        res = cpu_sample(x_host, frac, threads)
-        cpu = {
-            "value": res["pairs_per_s"],
-            "unit": "pairs/s",
-            "cores": threads,
-            "kind": "port",
-            "sample": (f"bit-exact C port of the reference (oracle/), {threads} threads: normalize all rows + "
-                       f"t=4 tiles [0, {res['tiles']}) of {res['total_tiles']} = {res['pairs']} pairs in "
-                       f"{res['seconds']:.2f} s"),
-        }
+        cpu = reference_baseline(x_host, args.ref_seconds or 12.0, threads)
+        if "unavailable" in cpu:
+            why = cpu["unavailable"]
+            frac = args.cpu_fraction or {"c1": 1.0, "c2": 1.0, "c3": 1.0, "c4": 1 / 16, "c5": 1 / 16}[args.config]
+            res = cpu_sample(x_host, frac, threads)
+            cpu = {
+                "value": res["pairs_per_s"], "unit": "pairs/s", "cores": threads, "kind": "port",
+                "sample": (f"bit-exact C port of the reference (oracle/), {threads} threads: normalize all rows + "
+                           f"t=4 tiles [0, {res['tiles']}) of {res['total_tiles']} = {res['pairs']} pairs in "
+                           f"{res['seconds']:.2f} s"),
+                "reference_unavailable": why,
+            }
+
+    # ---- the device step on the other BASELINE configs (same rank / world)
+    extra = {}
+    for cfg in [c for c in (args.extra_configs or "").split(",") if c and c != args.config]:
+        extra[cfg] = _device_step_config(cfg, rank, world, dev, args, barrier, max_over_ranks, peak)
 
     # kernels of the timed region, all ranks: K1 + the contraction's 1-2 launches per step
     launches = args.steps * (1 + (_lib.syrk_launches(n, tb, te) if te > tb else 0))
@@ -557,6 +801,15 @@ def run_b200(args, rank: int, world: int, local_rank: int) -> None:
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         launches = int(t.item())
     value = total_pairs / (ms_step * 1e-3)
+    rank_devices, k1_rows_all = [dev_index], [k1_rows]
+    if world > 1:
+        gathered = [None] * world
+        dist.all_gather_object(gathered, (dev_index, k1_rows))
+        rank_devices = [g[0] for g in gathered]
+        k1_rows_all = [g[1] for g in gathered]
+        if rank == 0:
+            print(f"bench: world_size={world} rank devices={rank_devices} device-step U exchange={exchange_mode} "
+                  f"peer mappings opened on rank 0={peers_opened}", file=sys.stderr, flush=True)
     if rank == 0:
         line = {
             "metric": "pairs_per_sec",
@@ -572,7 +825,11 @@ def run_b200(args, rank: int, world: int, local_rank: int) -> None:
             "dtype": "f64",
             "data": "synthetic",
             "config": dict(_config_dict(args.config, world),
-                           **({"u_exchange": _exchange_label(ndev, world)} if world > 1 else {})),
+                           **({"u_exchange_e2e": _exchange_label(ndev, world),
+                               "u_exchange_device_step": _device_exchange_label(exchange_mode),
+                               "world_size": world, "rank_devices": rank_devices,
+                               "peer_mappings_opened_rank0": peers_opened,
+                               "k1_rows_per_rank": k1_rows_all} if world > 1 else {})),
             "gflops": float(n) * n * l / (ms_step * 1e-3) / 1e9,
             "roofline_fp64_frac_of_step": (float(n) * n * l / world / (ms_step * 1e-3) / 1e12) / peak,
             "syrk_ms": syrk_avg_ms,
@@ -583,6 +840,7 @@ def run_b200(args, rank: int, world: int, local_rank: int) -> None:
             "gpu_launches": launches,
             "exact_mode": exact_mode,
             "split_mode": split_mode,
+            "extra_configs": extra,
             "e2e_pageable": e2e_pageable,
             "clocks": clock,
         }

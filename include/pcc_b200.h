@@ -111,6 +111,12 @@ int pcc_ipc_get_handle(const void *ptr, unsigned char *handle /* 64 bytes */);
 int pcc_ipc_open_handle(const unsigned char *handle /* 64 bytes */, void **ptr);
 int pcc_ipc_close_handle(void *ptr);
 
+/* Let kernels running on `device` load/store `peer`'s memory (in-process
+ * multi-GPU exchange: the broadcast normaliser writes U rows into every
+ * device's buffer over NVLink).  OK if device == peer or already enabled;
+ * PCC_ECUDA if the two GPUs have no peer path. */
+int pcc_enable_peer_access(int device, int peer);
+
 /* Zero rows [row_lo, row_hi) of U (the pad rows up to pcc_rows_padded(n)). */
 int pcc_zero_rows_f64(double *u, int64_t ldu, int64_t row_lo, int64_t row_hi, void *stream);
 
@@ -166,11 +172,12 @@ int pcc_syrk_split_f64(const int8_t *slices, const double *scale, int64_t n, int
                        int64_t ld_out, uint64_t out_base, int32_t ref_t, uint64_t ref_begin,
                        uint64_t ref_end, void *stream);
 
-/* Same as pcc_syrk_f64 with an explicit contraction kernel shape (0 = the
- * production default; 1..4 = the alternatives measured in DESIGN.md).  Every
- * shape computes each cell with the same K order, so all variants produce
- * bitwise identical results; this entry point exists for tuning.
- * PCC_VARIANT_EXACT selects the bit-exact dot8 kernel (pcc_syrk_exact_f64). */
+/* Same as pcc_syrk_f64 with an explicit contraction kernel: 0 = the
+ * production kernel, PCC_VARIANT_EXACT = the bit-exact dot8 kernel
+ * (pcc_syrk_exact_f64); anything else is PCC_EINVAL.  The tools build of the
+ * same source (tools/Makefile -> tools/libpcc_tune.so) also accepts the
+ * measured alternative shapes 1..14 of DESIGN.md's tuning table; every shape
+ * computes each cell with the same K order (bitwise identical results). */
 int pcc_syrk_f64_variant(int32_t variant, const double *u, int64_t n, int64_t l, int64_t ldu,
                          uint64_t tile_begin, uint64_t tile_end, int32_t layout, double *out,
                          int64_t ld_out, uint64_t out_base, int32_t ref_t, uint64_t ref_begin,

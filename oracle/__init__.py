@@ -65,6 +65,7 @@ def lib():
         l.oracle_compute_pass.argtypes = [_dp, _i64, _i64, _i64, _i64, _i64, _dp, ctypes.c_int]
         l.oracle_compute_tile_range.argtypes = [_dp, _i64, _dp, _i64, _i64, _i64, _i64, _i64, _i64]
         l.oracle_scatter_range.argtypes = [_dp, _dp, _i64, _i64, _i64, _i64, _i64]
+        l.oracle_scatter_range_span.argtypes = [_dp, _i64, _dp, _i64, _i64, _i64, _i64, _i64]
         l.oracle_allpairs_naive.argtypes = [_dp, _i64, _i64, _dp, ctypes.c_int]
         l.oracle_constant_row_flags.argtypes = [_dp, _i64, _i64, _u8p]
         l.oracle_allpairs.restype = ctypes.c_int
@@ -160,6 +161,28 @@ def compute_pass(u, t: int, j_start: int, j_end: int, threads: int | None = None
 def scatter_range(packed: np.ndarray, values, first_tile: int, count: int, m: int, t: int, n: int) -> None:
     values = _f64(values)
     lib().oracle_scatter_range(_d(packed), _d(values), first_tile, count, m, t, n)
+
+
+def packed_rows_span(u, y_lo: int, y_hi: int, t: int = 4, threads: int | None = None) -> np.ndarray:
+    """The reference's packed values of rows [y_lo, y_hi) -- the packed span
+    [F(y_lo), F(y_hi)) -- computed exactly as its engine does: compute_pass
+    over the t x t tile rows covering those rows (tiles.py:133-199) and
+    scatter_range of them (_kernels.py:322-348) into the span (sampled
+    full-size parity; ``y_lo`` and ``y_hi`` multiples of t, or y_hi = n)."""
+    u = _f64(u)
+    n = u.shape[0]
+    if not (0 <= y_lo < y_hi <= n) or y_lo % t or (y_hi % t and y_hi != n):
+        raise ValueError(f"row range [{y_lo}, {y_hi}) must be t-aligned inside [0, {n}]")
+    m = -(-n // t)
+    tr_lo, tr_hi = y_lo // t, -(-y_hi // t)
+    j_lo = tr_lo * (2 * m - tr_lo + 1) // 2
+    j_hi = tr_hi * (2 * m - tr_hi + 1) // 2
+    flat = compute_pass(u, t, j_lo, j_hi, threads)
+    lo = y_lo * (2 * n - y_lo + 1) // 2
+    hi = y_hi * (2 * n - y_hi + 1) // 2
+    span = np.full(hi - lo, np.nan, dtype=np.float64)
+    lib().oracle_scatter_range_span(_d(span), lo, _d(flat), j_lo, j_hi - j_lo, m, t, n)
+    return span
 
 
 def allpairs(x, t: int = 4, capacity: int | None = None, threads: int | None = None,

@@ -53,6 +53,7 @@ EXPORTED_SYMBOLS = (
     "pcc_ipc_get_handle",
     "pcc_ipc_open_handle",
     "pcc_ipc_close_handle",
+    "pcc_enable_peer_access",
     "pcc_zero_rows_f64",
     "pcc_syrk_f64",
     "pcc_syrk_f64_variant",
@@ -112,6 +113,7 @@ def _bind(l: ctypes.CDLL) -> None:
         "pcc_ipc_get_handle": (ctypes.c_int, [_vp, ctypes.c_char_p]),
         "pcc_ipc_open_handle": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(_vp)]),
         "pcc_ipc_close_handle": (ctypes.c_int, [_vp]),
+        "pcc_enable_peer_access": (ctypes.c_int, [ctypes.c_int, ctypes.c_int]),
         "pcc_syrk_f64": (ctypes.c_int, [_vp, _i64, _i64, _i64, _u64, _u64, _i32, _vp, _i64, _u64, _i32, _u64, _u64, _vp]),
         "pcc_syrk_f64_variant": (ctypes.c_int, [_i32, _vp, _i64, _i64, _i64, _u64, _u64, _i32, _vp, _i64, _u64, _i32, _u64, _u64, _vp]),
         "pcc_syrk_exact_f64": (ctypes.c_int, [_vp, _i64, _i64, _i64, _u64, _u64, _i32, _vp, _i64, _u64, _i32, _u64, _u64, _vp]),

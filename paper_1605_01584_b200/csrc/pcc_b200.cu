@@ -44,11 +44,15 @@ struct DeviceConfig {
   int sm_count = 0;
   int cc_major = 0, cc_minor = 0;
   int max_smem_optin = 0;
-  int syrk_ctas_per_sm = 0;
-  int variant_ctas[16] = {0};
+  int syrk_ctas_per_sm = 0;  // production contraction, grouped order
+  int syrk_id_ctas = 0;      // the same kernel in bijection id order (PCC_SYRK_ORDER=id)
   int quad_ctas = 0;
   int exact_ctas = 0;
   int split_ctas = 0;
+  int norm_regs[3] = {0, 0, 0};  // registers of normalize_rows_smem_kernel<256, MODE>
+#ifdef PCC_TUNING_VARIANTS
+  int variant_ctas[16] = {0};
+#endif
   size_t total_mem = 0;
 };
 
@@ -56,31 +60,18 @@ constexpr int kMaxDevices = 64;
 DeviceConfig g_dev[kMaxDevices];
 std::mutex g_dev_mu;
 
-// Contraction kernel shapes.  Variant 0 is the production default (TMA +
-// mbarrier ring); the others are kept for the measured comparison in
-// DESIGN.md (pcc_syrk_f64_variant) and only instantiated for the packed
-// layout.
-using V0 = pcc::SyrkCfg<2, 4, 8, 4, 16, 6>;  // TMA + mbarrier, 8 warps 64x32, BK 16 x 6 stages, stage-level fragments,
-                                              // grouped tile order (default)
-using V1 = pcc::SyrkCfg<2, 4, 8, 4, 16, 4>;  // cp.async + __syncthreads, 8 warps 64x32, BK 16 x 4
-using V2 = pcc::SyrkCfg<4, 4, 4, 4, 16, 4>;  // cp.async, 16 warps 32x32
-using V3 = pcc::SyrkCfg<2, 4, 8, 4, 32, 3>;  // cp.async, BK 32 x 3
-using V4 = pcc::SyrkCfg<4, 2, 4, 8, 16, 4>;  // cp.async, 8 warps 32x64
-using V5 = pcc::SyrkCfg<2, 4, 8, 4, 8, 12>;  // TMA, BK 8 x 12 stages
-using V6 = pcc::SyrkCfg<2, 4, 8, 4, 16, 7>;  // TMA, BK 16 x 7 stages
-using V7 = pcc::SyrkCfg<2, 4, 8, 4, 32, 3>;  // TMA, BK 32 x 3 stages
-using V8 = pcc::SyrkCfg<4, 2, 4, 8, 16, 6>;  // TMA, 8 warps 32x64
-using V9 = pcc::SyrkCfg<4, 4, 4, 4, 16, 6>;  // TMA, 16 warps 32x32
-using V10 = pcc::SyrkCfg<2, 4, 8, 4, 16, 6, 5>;  // TMA, producer 5 steps ahead
-using V11 = pcc::SyrkCfg<2, 4, 8, 4, 16, 6, 6>;  // TMA, producer 6 steps ahead (ring-limited)
-// V12 = V0 visiting tiles in plain bijection id order (the previous default;
-//       production visits them in the grouped L2-locality order)
-// V13 = V0 with half-stage skew between the two warps of each SMSP
-// V14 = V0 loading fragments slab by slab (the previous production inner loop)
-constexpr int kNumVariants = 15;
+// Production contraction shape: TMA + mbarrier ring, 8 warps 64x32, BK 16 x 6
+// stages, stage-level fragments, grouped tile order.  The measured
+// alternatives of DESIGN.md's tuning table are compiled only into the tools
+// build (tools/Makefile: -DPCC_TUNING_VARIANTS -> tools/libpcc_tune.so).
+using V0 = pcc::SyrkCfg<2, 4, 8, 4, 16, 6>;
 // Tail kernel: 64 x 64 quadrants of the GPU tiles of the last partial wave,
 // 4 warps (32 x 32 each), two CTAs per SM -- same per-cell arithmetic.
 using VQ = pcc::SyrkCfg<2, 2, 4, 4, 16, 6>;
+#ifdef PCC_TUNING_VARIANTS
+struct DeviceConfig;
+int configure_tuning_variants(DeviceConfig &c);
+#endif
 
 template <class C, int LAYOUT, bool GROUPED = false>
 int configure_tma_one(int *ctas) {
@@ -197,25 +188,22 @@ int configure_split(int *ctas) {
   return rc;
 }
 
-template <class C, int LAYOUT>
-int configure_one(int *ctas) {
-  PCC_CUDA(cudaFuncSetAttribute(pcc::syrk_kernel<C, LAYOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                C::kSmemBytes),
-           "cudaFuncSetAttribute(syrk smem)");
-  PCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas, pcc::syrk_kernel<C, LAYOUT>, C::kThreads,
-                                                         C::kSmemBytes),
-           "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+// K1 staged kernels: shared-memory opt-in (per device -- function attributes
+// belong to the device's context) and the register count the launch uses to
+// pick its CTA width.
+constexpr int kNormSmemPerSm = 224 * 1024;
+template <int MODE>
+int configure_normalize(int *regs) {
+  const void *fns[] = {(const void *)pcc::normalize_rows_smem_kernel<64, MODE>,
+                       (const void *)pcc::normalize_rows_smem_kernel<128, MODE>,
+                       (const void *)pcc::normalize_rows_smem_kernel<256, MODE>};
+  for (const void *f : fns)
+    PCC_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kNormSmemPerSm),
+             "cudaFuncSetAttribute(normalize smem)");
+  cudaFuncAttributes fa;
+  PCC_CUDA(cudaFuncGetAttributes(&fa, pcc::normalize_rows_smem_kernel<256, MODE>), "cudaFuncGetAttributes(normalize)");
+  *regs = fa.numRegs;
   return PCC_OK;
-}
-
-template <class C>
-int configure_variant(int *ctas) {
-  int c0 = 0, c1 = 0, c2 = 0;
-  int rc = configure_one<C, pcc::kLayoutPacked>(&c0);
-  if (rc == PCC_OK) rc = configure_one<C, pcc::kLayoutDense>(&c1);
-  if (rc == PCC_OK) rc = configure_one<C, pcc::kLayoutTiles>(&c2);
-  *ctas = c0 < c1 ? (c0 < c2 ? c0 : c2) : (c1 < c2 ? c1 : c2);
-  return rc;
 }
 
 // Per-device one-time setup (smem opt-in, occupancy); returns the config of
@@ -241,43 +229,23 @@ int device_config(const DeviceConfig **out, int device = -1) {
       return fail(PCC_ECUDA, "device %d is sm_%d%d; this library is built for sm_100a (B200) only", device,
                   p.major, p.minor);
     }
-    int rc = configure_tma_variant<V0, true>(&c.variant_ctas[0]);
-    if (rc == PCC_OK) rc = configure_tma_variant<V0, false>(&c.variant_ctas[12]);
+    int rc = configure_tma_variant<V0, true>(&c.syrk_ctas_per_sm);
+    if (rc == PCC_OK) rc = configure_tma_variant<V0, false>(&c.syrk_id_ctas);
     if (rc == PCC_OK) rc = configure_tma_variant<VQ>(&c.quad_ctas);
     if (rc == PCC_OK) rc = configure_exact(&c.exact_ctas);
     if (rc == PCC_OK) rc = configure_split(&c.split_ctas);
-    if (rc == PCC_OK) rc = configure_one<V1, pcc::kLayoutPacked>(&c.variant_ctas[1]);
-    if (rc == PCC_OK) rc = configure_one<V2, pcc::kLayoutPacked>(&c.variant_ctas[2]);
-    if (rc == PCC_OK) rc = configure_one<V3, pcc::kLayoutPacked>(&c.variant_ctas[3]);
-    if (rc == PCC_OK) rc = configure_one<V4, pcc::kLayoutPacked>(&c.variant_ctas[4]);
-    if (rc == PCC_OK) rc = configure_tma_one<V5, pcc::kLayoutPacked>(&c.variant_ctas[5]);
-    if (rc == PCC_OK) rc = configure_tma_one<V6, pcc::kLayoutPacked>(&c.variant_ctas[6]);
-    if (rc == PCC_OK) rc = configure_tma_one<V7, pcc::kLayoutPacked>(&c.variant_ctas[7]);
-    if (rc == PCC_OK) rc = configure_tma_one<V8, pcc::kLayoutPacked>(&c.variant_ctas[8]);
-    if (rc == PCC_OK) rc = configure_tma_one<V9, pcc::kLayoutPacked>(&c.variant_ctas[9]);
-    if (rc == PCC_OK) rc = configure_tma_one<V10, pcc::kLayoutPacked>(&c.variant_ctas[10]);
-    if (rc == PCC_OK) rc = configure_tma_one<V11, pcc::kLayoutPacked>(&c.variant_ctas[11]);
-    if (rc == PCC_OK) {
-      using TL = pcc::TmaLayout<V0>;
-      auto kfn = pcc::syrk_tma_kernel<V0, pcc::kLayoutPacked, false>;
-      PCC_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, TL::kSmemBytes), "attr(V12)");
-      PCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.variant_ctas[12], kfn, TL::kThreads, TL::kSmemBytes),
-               "occupancy(V12)");
-      auto kfn14 = pcc::syrk_tma_kernel<V0, pcc::kLayoutPacked, false, false, false>;
-      PCC_CUDA(cudaFuncSetAttribute(kfn14, cudaFuncAttributeMaxDynamicSharedMemorySize, TL::kSmemBytes), "attr(V14)");
-      PCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.variant_ctas[14], kfn14, TL::kThreads, TL::kSmemBytes),
-               "occupancy(V14)");
-      auto kfn13 = pcc::syrk_tma_kernel<V0, pcc::kLayoutPacked, false, true>;
-      PCC_CUDA(cudaFuncSetAttribute(kfn13, cudaFuncAttributeMaxDynamicSharedMemorySize, TL::kSmemBytes), "attr(V13)");
-      PCC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.variant_ctas[13], kfn13, TL::kThreads, TL::kSmemBytes),
-               "occupancy(V13)");
-    }
+    if (rc == PCC_OK) rc = configure_normalize<pcc::kNormLocal>(&c.norm_regs[pcc::kNormLocal]);
+    if (rc == PCC_OK) rc = configure_normalize<pcc::kNormBcast>(&c.norm_regs[pcc::kNormBcast]);
+    if (rc == PCC_OK) rc = configure_normalize<pcc::kNormDigits>(&c.norm_regs[pcc::kNormDigits]);
+#ifdef PCC_TUNING_VARIANTS
+    if (rc == PCC_OK) rc = configure_tuning_variants(c);
+#endif
     if (prev != device) cudaSetDevice(prev);
     if (rc != PCC_OK) return rc;
-    c.syrk_ctas_per_sm = c.variant_ctas[0];
-    for (int v = 0; v < kNumVariants; ++v)
-      if (c.variant_ctas[v] < 1) return fail(PCC_ECUDA, "contraction variant %d cannot be resident on device %d", v, device);
+    if (c.syrk_ctas_per_sm < 1 || c.syrk_id_ctas < 1 || c.quad_ctas < 1)
+      return fail(PCC_ECUDA, "the FP64 contraction cannot be resident on device %d", device);
     if (c.exact_ctas < 1) return fail(PCC_ECUDA, "exact contraction cannot be resident on device %d", device);
+    if (c.split_ctas < 1) return fail(PCC_ECUDA, "split contraction cannot be resident on device %d", device);
     c.ready = true;
   }
   *out = &c;
@@ -295,19 +263,6 @@ int check_u(const double *u, int64_t n, int64_t l, int64_t ldu) {
     return fail(PCC_EINVAL, "ldu %lld must be even and >= pcc_ldu(l) = %lld", (long long)ldu, (long long)pcc_ldu(l));
   if (u == nullptr || (reinterpret_cast<uintptr_t>(u) & 15))
     return fail(PCC_EINVAL, "u must be a non-null 16-byte aligned device pointer");
-  return PCC_OK;
-}
-
-template <class C, int LAYOUT>
-int launch_cfg(const double *u, int64_t n, int64_t l, int64_t ldu, uint64_t tb, uint64_t te, const pcc::Epilogue &ep,
-               cudaStream_t stream, int ctas_per_sm, int sm_count) {
-  const uint64_t m_g = ceil_div((uint64_t)n, pcc::kTile);
-  const int k_tiles = (int)ceil_div((uint64_t)l, C::BK);
-  const uint64_t resident = (uint64_t)sm_count * (uint64_t)ctas_per_sm;
-  const uint64_t tiles = te - tb;
-  const unsigned grid = (unsigned)(tiles < resident ? tiles : resident);
-  pcc::syrk_kernel<C, LAYOUT><<<grid, C::kThreads, C::kSmemBytes, stream>>>(u, n, ldu, k_tiles, m_g, tb, te, ep);
-  PCC_CUDA(cudaGetLastError(), "syrk_kernel launch");
   return PCC_OK;
 }
 
@@ -410,6 +365,10 @@ int launch_split(const int8_t *slices, const double *scale, int64_t n, int64_t l
   return PCC_OK;
 }
 
+#ifdef PCC_TUNING_VARIANTS
+#include "../../tools/syrk_variants.inc"
+#endif
+
 template <int LAYOUT>
 int launch_syrk(const double *u, int64_t n, int64_t l, int64_t ldu, uint64_t tb, uint64_t te,
                 const pcc::Epilogue &ep, cudaStream_t stream, int variant = 0) {
@@ -418,39 +377,23 @@ int launch_syrk(const double *u, int64_t n, int64_t l, int64_t ldu, uint64_t tb,
   int rc = device_config(&dc);
   if (rc) return rc;
   if (variant == PCC_VARIANT_EXACT) return launch_exact<LAYOUT>(u, n, l, ldu, tb, te, ep, stream, dc);
-  const int sms = dc->sm_count;
-  const int *vc = dc->variant_ctas;
   if (variant == 0) {
     static const bool id_order = [] {  // A/B knob for the tile order, read once
       const char *e = getenv("PCC_SYRK_ORDER");
       return e != nullptr && strcmp(e, "id") == 0;
     }();
-    if (id_order) return launch_tma_cfg<V0, LAYOUT, false>(u, n, l, ldu, tb, te, ep, stream, vc[0], sms, dc->quad_ctas);
-    return launch_tma_cfg<V0, LAYOUT, true>(u, n, l, ldu, tb, te, ep, stream, vc[0], sms, dc->quad_ctas);
+    if (id_order)
+      return launch_tma_cfg<V0, LAYOUT, false>(u, n, l, ldu, tb, te, ep, stream, dc->syrk_id_ctas, dc->sm_count,
+                                               dc->quad_ctas);
+    return launch_tma_cfg<V0, LAYOUT, true>(u, n, l, ldu, tb, te, ep, stream, dc->syrk_ctas_per_sm, dc->sm_count,
+                                            dc->quad_ctas);
   }
-  if (LAYOUT != pcc::kLayoutPacked)
-    return fail(PCC_EINVAL, "contraction variant %d is only built for the packed layout", variant);
-  switch (variant) {
-    case 1: return launch_cfg<V1, pcc::kLayoutPacked>(u, n, l, ldu, tb, te, ep, stream, vc[1], sms);
-    case 2: return launch_cfg<V2, pcc::kLayoutPacked>(u, n, l, ldu, tb, te, ep, stream, vc[2], sms);
-    case 3: return launch_cfg<V3, pcc::kLayoutPacked>(u, n, l, ldu, tb, te, ep, stream, vc[3], sms);
-    case 4: return launch_cfg<V4, pcc::kLayoutPacked>(u, n, l, ldu, tb, te, ep, stream, vc[4], sms);
-    case 5: return launch_tma_cfg<V5, pcc::kLayoutPacked>(u, n, l, ldu, tb, te, ep, stream, vc[5], sms);
-    case 6: return launch_tma_cfg<V6, pcc::kLayoutPacked>(u, n, l, ldu, tb, te, ep, stream, vc[6], sms);
-    case 7: return launch_tma_cfg<V7, pcc::kLayoutPacked>(u, n, l, ldu, tb, te, ep, stream, vc[7], sms);
-    case 8: return launch_tma_cfg<V8, pcc::kLayoutPacked>(u, n, l, ldu, tb, te, ep, stream, vc[8], sms);
-    case 9: return launch_tma_cfg<V9, pcc::kLayoutPacked>(u, n, l, ldu, tb, te, ep, stream, vc[9], sms);
-    case 10: return launch_tma_cfg<V10, pcc::kLayoutPacked>(u, n, l, ldu, tb, te, ep, stream, vc[10], sms);
-    case 11: return launch_tma_cfg<V11, pcc::kLayoutPacked>(u, n, l, ldu, tb, te, ep, stream, vc[11], sms);
-    case 12:
-      return launch_tma_cfg<V0, pcc::kLayoutPacked, false>(u, n, l, ldu, tb, te, ep, stream, vc[12], sms,
-                                                           dc->quad_ctas);
-    case 13: return launch_tma_cfg<V0, pcc::kLayoutPacked, false, true>(u, n, l, ldu, tb, te, ep, stream, vc[13], sms);
-    case 14:
-      return launch_tma_cfg<V0, pcc::kLayoutPacked, false, false, false>(u, n, l, ldu, tb, te, ep, stream, vc[14], sms);
-    default:
-      return fail(PCC_EINVAL, "unknown contraction variant %d (0..%d, or PCC_VARIANT_EXACT)", variant, kNumVariants - 1);
-  }
+#ifdef PCC_TUNING_VARIANTS
+  return launch_tuning_variant<LAYOUT>(variant, u, n, l, ldu, tb, te, ep, stream, dc);
+#else
+  return fail(PCC_EINVAL, "unknown contraction variant %d (0 or PCC_VARIANT_EXACT; the measured tuning shapes are "
+              "built into tools/libpcc_tune.so only)", variant);
+#endif
 }
 
 // Shared-memory-staged K1 launch (the default whenever a row fits), single
@@ -461,18 +404,10 @@ int launch_normalize_staged(const double *x, int64_t ldx, double *u, int64_t ldu
                             int64_t row_lo, int64_t row_hi, const pcc::NormDests &dests, cudaStream_t stream) {
   const uint64_t rows = (uint64_t)(row_hi - row_lo);
   const int64_t row_bytes = l * (int64_t)sizeof(double);
-  constexpr int64_t kSmPerSmem = 224 * 1024;
-  static std::once_flag attr_once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(attr_once, [] {
-    const void *fns[] = {(const void *)pcc::normalize_rows_smem_kernel<64, MODE>,
-                         (const void *)pcc::normalize_rows_smem_kernel<128, MODE>,
-                         (const void *)pcc::normalize_rows_smem_kernel<256, MODE>};
-    for (const void *f : fns)
-      if (attr_err == cudaSuccess)
-        attr_err = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmPerSmem);
-  });
-  if (attr_err != cudaSuccess) return cuda_fail(attr_err, "cudaFuncSetAttribute(normalize smem)");
+  constexpr int64_t kSmPerSmem = kNormSmemPerSm;
+  const DeviceConfig *dc = nullptr;
+  const int cfg_rc = device_config(&dc);  // smem opt-in + register count of this device
+  if (cfg_rc) return cfg_rc;
   // Shared-memory staging in natural order: as many CTAs per SM as rows allow
   // (4, 3, 2, then 1 CTA/SM), up to 8 rows per CTA.
   int per_cta = 0;
@@ -502,11 +437,7 @@ int launch_normalize_staged(const double *x, int64_t ldx, double *u, int64_t ldu
   }();
   // Widest CTA whose register footprint still lets every smem-resident CTA
   // run (measured, profiles/r01_normalize.log: c2 -> 128, c4 -> 256).
-  static int regs = 0;
-  if (regs == 0) {
-    cudaFuncAttributes fa;
-    regs = cudaFuncGetAttributes(&fa, pcc::normalize_rows_smem_kernel<256, MODE>) == cudaSuccess ? fa.numRegs : 72;
-  }
+  const int regs = dc->norm_regs[MODE] > 0 ? dc->norm_regs[MODE] : 72;
   const int64_t occ_smem = (228 * 1024) / ((int64_t)smem + 1024);
   int threads = 64;
   for (int t : {256, 128})
@@ -689,6 +620,28 @@ int pcc_ipc_open_handle(const unsigned char *handle, void **ptr) {
 
 int pcc_ipc_close_handle(void *ptr) {
   if (ptr) PCC_CUDA(cudaIpcCloseMemHandle(ptr), "cudaIpcCloseMemHandle");
+  return PCC_OK;
+}
+
+int pcc_enable_peer_access(int device, int peer) {
+  int count = 0;
+  PCC_CUDA(cudaGetDeviceCount(&count), "cudaGetDeviceCount");
+  if (device < 0 || peer < 0 || device >= count || peer >= count)
+    return fail(PCC_EINVAL, "devices (%d, %d) outside [0, %d)", device, peer, count);
+  if (device == peer) return PCC_OK;
+  int can = 0;
+  PCC_CUDA(cudaDeviceCanAccessPeer(&can, device, peer), "cudaDeviceCanAccessPeer");
+  if (!can) return fail(PCC_ECUDA, "device %d cannot access device %d's memory (no peer path)", device, peer);
+  int prev = 0;
+  PCC_CUDA(cudaGetDevice(&prev), "cudaGetDevice");
+  PCC_CUDA(cudaSetDevice(device), "cudaSetDevice");
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+  cudaSetDevice(prev);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();  // clear the sticky-free "already enabled" status
+    return PCC_OK;
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceEnablePeerAccess");
   return PCC_OK;
 }
 
@@ -950,7 +903,7 @@ int pcc_syrk_launches(int64_t n, uint64_t tile_begin, uint64_t tile_end, int32_t
   int rc = device_config(&dc);
   if (rc) return rc;
   const uint64_t tiles = tile_end - tile_begin;
-  const uint64_t resident = (uint64_t)dc->sm_count * (uint64_t)dc->variant_ctas[0];
+  const uint64_t resident = (uint64_t)dc->sm_count * (uint64_t)dc->syrk_ctas_per_sm;
   const uint64_t tail = quad_tail(tiles, resident, dc->sm_count, dc->quad_ctas);
   *launches = (tiles > tail ? 1 : 0) + (tail > 0 ? 1 : 0);
   return PCC_OK;
@@ -964,31 +917,39 @@ int pcc_probe_fp64_peak(double *tflops) {
   double *scratch = nullptr;
   cudaStream_t s = nullptr;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
-  PCC_CUDA(cudaMalloc(&scratch, sizeof(double)), "cudaMalloc");
-  PCC_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
-  PCC_CUDA(cudaEventCreate(&e0), "cudaEventCreate");
-  PCC_CUDA(cudaEventCreate(&e1), "cudaEventCreate");
+  // every resource is released on every path (the probe can run many times)
+  auto release = [&] {
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+    if (s) cudaStreamDestroy(s);
+    if (scratch) cudaFree(scratch);
+  };
+  auto bail = [&](cudaError_t e, const char *what) {
+    release();
+    return cuda_fail(e, what);
+  };
+  cudaError_t e;
+  if ((e = cudaMalloc(&scratch, sizeof(double))) != cudaSuccess) return bail(e, "cudaMalloc");
+  if ((e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)) != cudaSuccess) return bail(e, "cudaStreamCreate");
+  if ((e = cudaEventCreate(&e0)) != cudaSuccess) return bail(e, "cudaEventCreate");
+  if ((e = cudaEventCreate(&e1)) != cudaSuccess) return bail(e, "cudaEventCreate");
   const int threads = 512, iters = 4000;
   const int grid = dc->sm_count * 2;
   pcc::dmma_probe_kernel<<<grid, threads, 0, s>>>(scratch, 200);  // warm-up
+  if ((e = cudaGetLastError()) != cudaSuccess) return bail(e, "dmma_probe_kernel launch");
   float best = 1e30f;
   for (int rep = 0; rep < 3; ++rep) {
     cudaEventRecord(e0, s);
     pcc::dmma_probe_kernel<<<grid, threads, 0, s>>>(scratch, iters);
     cudaEventRecord(e1, s);
-    cudaError_t e = cudaEventSynchronize(e1);
-    if (e != cudaSuccess) return cuda_fail(e, "dmma_probe_kernel");
+    if ((e = cudaEventSynchronize(e1)) != cudaSuccess) return bail(e, "dmma_probe_kernel");
     float ms = 0.f;
     cudaEventElapsedTime(&ms, e0, e1);
     if (ms < best) best = ms;
   }
   const double flops = 2.0 * 256.0 * 8.0 * iters * (double)(threads / 32) * grid;
   *tflops = flops / ((double)best * 1e-3) / 1e12;
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
-  cudaStreamDestroy(s);
-  cudaFree(scratch);
-  PCC_CUDA(cudaGetLastError(), "dmma_probe_kernel");
+  release();
   return PCC_OK;
 }
 

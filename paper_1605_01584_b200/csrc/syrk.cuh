@@ -11,8 +11,8 @@
 //
 // Tile: 128 x 128 cells per CTA, 8 warps in a 2 x 4 grid, each warp owns a
 // 64 x 32 sub-tile = 8 x 4 DMMA 8x8 accumulators (64 doubles per thread).
-// K is staged 16 doubles at a time through a 4-deep cp.async ring (32 KB
-// per stage, 128 KB total), stored as 8-double "slabs": smem[slab][row][8].
+// K is staged 16 doubles at a time through a 6-deep TMA ring (32 KB per
+// stage), stored as 8-double "slabs": smem[slab][row][8].
 // Fragment loads are one 16-byte LDS per thread per 8x8 operand tile; a
 // quarter-warp (the LDS.128 phase) touches rows r, r+1 x 4 chunks = 128
 // distinct bytes, so the layout is bank-conflict free without padding.
@@ -83,108 +83,6 @@ __device__ __forceinline__ void store_cell(const Epilogue &ep, uint64_t y, uint6
     const uint64_t jr = row_prefix(ep.ref_m, yt) + xt - yt;
     if (jr >= ep.ref_begin && jr < ep.ref_end)
       ep.out[(jr - ep.ref_begin) * t * t + (y - yt * t) * t + (x - xt * t)] = v;
-  }
-}
-
-template <class C, int LAYOUT>
-__global__ void __launch_bounds__(C::kThreads, 1)
-syrk_kernel(const double *__restrict__ u, int64_t n, int64_t ldu, int k_tiles, uint64_t m_g,
-            uint64_t tile_begin, uint64_t tile_end, Epilogue ep) {
-  static_assert(C::kEdge == kTile, "the cp.async kernels compute whole 128 x 128 tiles");
-  extern __shared__ __align__(128) double smem[];
-  const int tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5;
-  const int wm = warp / C::WARPS_N, wn = warp % C::WARPS_N;
-  const int g = lane >> 2, tig = lane & 3;
-  const uint32_t smem_base = smem_u32(smem);
-
-  // Copy assignment: thread tid owns 16-byte chunk q = tid % (BK/2) of rows
-  // tid / (BK/2) + kRowsPerPass * i, for both operands.
-  const int cq = tid % C::kChunksPerRow;
-  const int crow = tid / C::kChunksPerRow;
-  const uint32_t copy_soff =
-      (uint32_t)((((cq >> 2) * kTile + crow) * kSlab + (cq & 3) * 2) * sizeof(double));
-
-  for (uint64_t J = tile_begin + blockIdx.x; J < tile_end; J += gridDim.x) {
-    const uint64_t Y = tile_row(m_g, J);
-    const uint64_t X = J + Y - row_prefix(m_g, Y);
-    const double *ga = u + (int64_t)(Y * kTile + crow) * ldu + cq * 2;
-    const double *gb = u + (int64_t)(X * kTile + crow) * ldu + cq * 2;
-
-    auto load_stage = [&](int slot, int kt) {
-      const uint32_t s = smem_base + (uint32_t)(slot * C::kStageDoubles * sizeof(double)) + copy_soff;
-      const int64_t k0 = (int64_t)kt * C::BK;
-#pragma unroll
-      for (int i = 0; i < C::kPasses; ++i) {
-        const int64_t roff = (int64_t)(C::kRowsPerPass * i) * ldu + k0;
-        const uint32_t so = (uint32_t)(C::kRowsPerPass * i * kSlab * sizeof(double));
-        cp_async_16(s + so, ga + roff);
-        cp_async_16(s + so + (uint32_t)(C::kOpDoubles * sizeof(double)), gb + roff);
-      }
-    };
-
-    double acc[C::MI][C::NI][2];
-#pragma unroll
-    for (int mi = 0; mi < C::MI; ++mi)
-#pragma unroll
-      for (int ni = 0; ni < C::NI; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
-
-#pragma unroll
-    for (int s = 0; s < C::STAGES - 1; ++s) {
-      if (s < k_tiles) load_stage(s, s);
-      cp_async_commit();
-    }
-
-    for (int kt = 0; kt < k_tiles; ++kt) {
-      cp_async_wait<C::STAGES - 2>();
-      __syncthreads();
-      const int nk = kt + C::STAGES - 1;
-      if (nk < k_tiles) load_stage(nk % C::STAGES, nk);
-      cp_async_commit();
-
-      const double *sA = smem + (kt % C::STAGES) * C::kStageDoubles + (wm * C::MI * 8 + g) * kSlab + tig * 2;
-      const double *sB = smem + (kt % C::STAGES) * C::kStageDoubles + C::kOpDoubles + (wn * C::NI * 8 + g) * kSlab +
-                         tig * 2;
-#pragma unroll
-      for (int slab = 0; slab < C::kSlabs; ++slab) {
-        double2 a[C::MI], b[C::NI];
-#pragma unroll
-        for (int mi = 0; mi < C::MI; ++mi)
-          a[mi] = *reinterpret_cast<const double2 *>(sA + slab * kTile * kSlab + mi * 8 * kSlab);
-#pragma unroll
-        for (int ni = 0; ni < C::NI; ++ni)
-          b[ni] = *reinterpret_cast<const double2 *>(sB + slab * kTile * kSlab + ni * 8 * kSlab);
-#pragma unroll
-        for (int mi = 0; mi < C::MI; ++mi)
-#pragma unroll
-          for (int ni = 0; ni < C::NI; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], a[mi].x, b[ni].x);
-#pragma unroll
-        for (int mi = 0; mi < C::MI; ++mi)
-#pragma unroll
-          for (int ni = 0; ni < C::NI; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], a[mi].y, b[ni].y);
-      }
-    }
-    cp_async_wait<0>();
-    __syncthreads();  // ring slots are rewritten by the next tile's prologue
-
-    // Fused epilogue: cells y <= x < n straight from the accumulators.
-    const uint64_t un = (uint64_t)n;
-    const uint64_t y0 = Y * kTile + wm * C::MI * 8 + g;
-    const uint64_t x0 = X * kTile + wn * C::NI * 8 + 2 * tig;
-#pragma unroll
-    for (int mi = 0; mi < C::MI; ++mi) {
-      const uint64_t y = y0 + mi * 8;
-      if (y >= un) continue;
-      const uint64_t prb = (LAYOUT == kLayoutPacked) ? row_prefix(un, y) - y - ep.out_base : 0;
-#pragma unroll
-      for (int ni = 0; ni < C::NI; ++ni) {
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const uint64_t x = x0 + ni * 8 + e;
-          if (x >= y && x < un) store_cell<LAYOUT>(ep, y, x, prb, acc[mi][ni][e]);
-        }
-      }
-    }
   }
 }
 

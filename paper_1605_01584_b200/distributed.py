@@ -5,9 +5,11 @@ Mirrors ``paircorr.distributed`` (/root/reference/pkg/src/paircorr/distributed.p
 contiguous chunks of ``ceil(T/p)`` tile ids, trailing workers possibly empty
 (distributed.py:76-92; the paper's static distribution) --
 applied to the 128 x 128 GPU tile matrix.  A worker is one GPU driven by one
-host thread (ctypes releases the GIL); every worker normalises the full
-dataset itself (the reference's worker model, worker.py:68-80) and
-contracts only its tile range, so there is no collective in the data path.
+host thread (ctypes releases the GIL).  With several devices each device
+uploads only its block of rows of X and one broadcast normalisation kernel
+writes the normalised rows into every device's U over NVLink peer memory
+(``normalize_on_devices``); the workers then contract only their tile
+ranges, so there is no collective in the contraction.
 Results stay sharded on the devices (``ShardedResult``) or are gathered
 into one packed host array; every packed cell belongs to exactly one tile
 and every tile to exactly one worker, so the gathered result is bitwise
@@ -336,22 +338,107 @@ def _run_subprocess(dataset: Dataset, dataset_path: str, geom: TileGeometry, p: 
 
 
 def compute_shard(x_host, n: int, l: int, a: WorkerAssignment, device: torch.device,
-                  x_device: torch.Tensor | None = None, method: str = "tensor") -> tuple[Shard, torch.Tensor]:
-    """Worker body: upload, normalise everything, contract ``a``'s tile range.
+                  x_device: torch.Tensor | None = None, method: str = "tensor",
+                  normalized: tuple | None = None) -> tuple[Shard, torch.Tensor]:
+    """Worker body: contract ``a``'s tile range on ``device``.
 
+    ``normalized`` = ``(u, flags)`` already on the device (``normalize_on_devices``),
+    or ``(u, flags, contraction)`` to share one prepared ``_lib.Contraction``
+    between the workers of a device; else X is uploaded and normalised here.
     Returns the shard and the device zero-variance flags; asynchronous on
     the device's current stream.
     """
     with torch.cuda.device(device):
-        x = x_device if x_device is not None else as_device_f64(x_host, device)
-        u, flags = normalize_device(x)
+        if normalized is None:
+            x = x_device if x_device is not None else as_device_f64(x_host, device)
+            u, flags = normalize_device(x)
+            con = None
+        else:
+            u, flags = normalized[0], normalized[1]
+            con = normalized[2] if len(normalized) > 2 else None
         lo, hi = shard_span(n, a.start, a.stop)
         vals = torch.empty(max(hi - lo, 1), dtype=torch.float64, device=device)
         if a.stop > a.start:
-            con = _lib.Contraction(method, u, n, l).prepare_all(stream_handle())
+            if con is None:
+                con = _lib.Contraction(method, u, n, l).prepare_all(stream_handle())
             con.syrk(a.start, a.stop, _lib.LAYOUT_PACKED, ptr(vals), 0, lo, 0, 0, 0, stream_handle(),
                      f"worker {a.worker_index}")
         return Shard(a.worker_index, device, a.start, a.stop, lo, vals), flags
+
+
+def _rows_of(x_host, r0: int, r1: int) -> torch.Tensor:
+    """Rows [r0, r1) of the host / device matrix as a float64 torch tensor view."""
+    if isinstance(x_host, torch.Tensor):
+        t = x_host if x_host.dtype == torch.float64 else x_host.to(torch.float64)
+    else:
+        t = torch.from_numpy(np.ascontiguousarray(x_host, dtype=np.float64))
+    return t[r0:r1]
+
+
+def normalize_on_devices(x_host, n: int, l: int, devs: list[torch.device]) -> list[tuple[torch.Tensor, torch.Tensor]]:
+    """K1 for in-process workers: one ``(u, flags)`` per entry of ``devs``.
+
+    One entry: upload X, normalise (``normalize_device``).  Several: entry q
+    uploads only its ``row_slices`` block of X (1/p of it over its own PCIe
+    link) and ONE broadcast K1 kernel (``pcc_normalize_rows_bcast_f64``)
+    stores each normalised row into every entry's U -- peer stores over
+    NVLink between distinct GPUs (``pcc_enable_peer_access``), local stores
+    when entries share a device.  U has ``p S`` rows (pad rows zero), flags
+    ``p S`` entries.  Same bits as ``normalize_device`` on every entry.
+    """
+    L = _lib.lib()
+    p = len(devs)
+    if p == 1:
+        with torch.cuda.device(devs[0]):
+            return [normalize_device(as_device_f64(x_host, devs[0]))]
+    if p > 16:  # kMaxNormDests
+        out = []
+        for d in devs:
+            with torch.cuda.device(d):
+                out.append(normalize_device(as_device_f64(x_host, d)))
+        return out
+    slices, S = row_slices(n, p)
+    ldu = int(L.pcc_ldu(l))
+    bufs = []
+    for d in devs:
+        with torch.cuda.device(d):
+            u = torch.empty((p * S, ldu), dtype=torch.float64, device=d)
+            flags = torch.zeros(p * S, dtype=torch.uint8, device=d)
+            _lib.check(L.pcc_zero_rows_f64(ptr(u), ldu, n, p * S, stream_handle()), "pad rows")
+            bufs.append((u, flags))
+    idx = sorted({d.index for d in devs})
+    for a in idx:
+        for b in idx:
+            _lib.check(L.pcc_enable_peer_access(a, b), f"peer access {a} -> {b}")
+    for d in idx:  # every buffer allocated and zero-padded before any peer writes
+        torch.cuda.synchronize(d)
+    errors: list[BaseException | None] = [None] * p
+
+    def run(q: int) -> None:
+        d = devs[q]
+        r0, r1 = slices[q]
+        try:
+            if r1 <= r0:
+                return
+            with torch.cuda.device(d):
+                xd = as_device_f64(_rows_of(x_host, r0, r1), d)
+                uarr = (ctypes.c_void_p * p)(*[ptr(u) + 8 * r0 * ldu for u, _ in bufs])
+                farr = (ctypes.c_void_p * p)(*[ptr(f) + r0 for _, f in bufs])
+                _lib.check(L.pcc_normalize_rows_bcast_f64(ptr(xd), xd.stride(0), uarr, farr, p, ldu, l, 0, r1 - r0,
+                                                          stream_handle()), f"device slot {q} normalize+broadcast")
+                torch.cuda.current_stream().synchronize()
+        except BaseException as exc:  # noqa: BLE001 - re-raised below
+            errors[q] = exc
+
+    ts = [threading.Thread(target=run, args=(q,)) for q in range(p)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for q, exc in enumerate(errors):
+        if exc is not None:
+            raise WorkerError(f"device slot {q} failed to normalise rows {slices[q]}: {exc}", worker_index=q) from exc
+    return bufs
 
 
 def stream_shard(x_host, n: int, l: int, a: WorkerAssignment, device: torch.device, host_out=None,
@@ -602,17 +689,29 @@ def run_workers(
     shards: list[Shard | None] = [None] * p
     flags: list[torch.Tensor | None] = [None] * p
     errors: list[BaseException | None] = [None] * p
+    # one device slot per entry of devs (at most one per worker): K1 once per
+    # slot -- row blocks + broadcast over NVLink with several -- then every
+    # worker contracts its range against its slot's U
+    slots = devs[:p]
+    normed = normalize_on_devices(dataset.values, n, l, slots)
+    cons: list = [None] * len(slots)
 
     def run_one(a: WorkerAssignment) -> None:
-        dev = devs[a.worker_index % len(devs)]
+        q = a.worker_index % len(slots)
+        dev = slots[q]
         try:
-            shards[a.worker_index], flags[a.worker_index] = compute_shard(dataset.values, n, l, a, dev, method=method)
+            u, fl = normed[q]
+            shards[a.worker_index], flags[a.worker_index] = compute_shard(
+                dataset.values, n, l, a, dev, method=method, normalized=(u, fl, cons[q]))
             with torch.cuda.device(dev):
                 torch.cuda.current_stream().synchronize()
         except BaseException as exc:  # noqa: BLE001 - re-raised as WorkerError below
             errors[a.worker_index] = exc
 
-    if p == 1 or len(devs) == 1:
+    for q, (u, _) in enumerate(normed):  # split method: digit planes once per slot
+        with torch.cuda.device(slots[q]):
+            cons[q] = _lib.Contraction(method, u, n, l).prepare_all(stream_handle())
+    if len(slots) == 1:
         for a in assignments:
             run_one(a)
     else:
@@ -630,6 +729,6 @@ def run_workers(
                 unfinished_range=(a.start, a.stop),
             ) from exc
     check_coverage([(a.start, a.stop, a.stop) for a in assignments], gpu_geometry(n).total_tiles)
-    zv = frozenset(np.flatnonzero(flags[0].cpu().numpy()).tolist())
+    zv = frozenset(np.flatnonzero(normed[0][1][:n].cpu().numpy()).tolist())
     result = ShardedResult(n=n, shards=[s for s in shards if s is not None], zero_variance=zv)
     return result.gather(out) if gather else result

@@ -202,7 +202,9 @@ def allpairs(
 
     Reference arguments keep their meaning and validation; ``workers > 1``
     splits the GPU tile range across that many workers (one host thread
-    each, round-robin over ``devices``).  Extensions:
+    each, round-robin over ``devices``); ``backend="subprocess"`` runs them
+    as GPU worker processes speaking the reference's framed protocol
+    (``run_workers``, as engine.py:46-56 routes it).  Extensions:
 
     * ``devices``: ``None`` (current device), a device count, or a list;
     * ``output``: ``"packed"`` (reference layout, returns ``CorrelationResult``)
@@ -225,6 +227,7 @@ def allpairs(
       ~2.4x the tensor path's speed; l <= 8192) or ``"exact"`` (same as
       ``exact=True``).
     """
+    source = dataset  # a path stays a path for subprocess workers (engine.py:55-56)
     if not isinstance(dataset, Dataset):
         from .fileio import load_dataset
 
@@ -243,6 +246,14 @@ def allpairs(
     method = _lib.resolve_method(method, exact)
     _lib.check_method_shape(method, dataset.l)
     devs = resolve_devices(devices)
+    if backend == "subprocess":
+        # the reference routes workers > 1 or backend != "in_process" to
+        # run_workers(dataset, geom, workers, backend, capacity, threads)
+        # (engine.py:46-56): GPU worker processes on the framed protocol
+        if output != "packed" or keep_on_device:
+            raise ValueError("backend='subprocess' returns the gathered packed result "
+                             "(output='packed', keep_on_device=False)")
+        return run_workers(source, geom, workers, "subprocess", capacity, threads, devices=devs, method=method)
     if (workers > 1 or len(devs) > 1) and output == "packed" and not keep_on_device:
         return run_workers(dataset, geom, max(workers, len(devs)), backend="cuda", devices=devs, out=out,
                            method=method)

@@ -1,6 +1,7 @@
-"""bench.py's reference arm runs on the CPU (the bit-exact C port, all host
-threads): check its JSON line carries the contract's keys, and that under
-torchrun rank 0 alone reports."""
+"""bench.py's reference arm runs on the CPU (the reference package itself from
+baseline/_ref when installed, else the bit-exact C port; all host threads):
+check its JSON line carries the contract's keys, and that under torchrun
+rank 0 alone reports."""
 
 import json
 import os
@@ -16,7 +17,7 @@ KEYS = {"impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_
 
 def _run(*args):
     return subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--config", "c1",
-                           "--steps", "1", "--warmup", "1", "--cpu-fraction", "0.05", *args],
+                           "--steps", "1", "--warmup", "1", "--cpu-fraction", "0.05", "--ref-seconds", "0.5", *args],
                           capture_output=True, text=True, env=dict(os.environ), cwd=ROOT, timeout=300)
 
 
@@ -26,7 +27,11 @@ def test_reference_arm_json_line():
     line = json.loads(out.stdout.strip().splitlines()[-1])
     assert KEYS <= set(line)
     assert line["impl"] == "reference" and line["unit"] == "pairs/s" and line["value"] > 0
-    assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
+    assert line["cpu_baseline"]["kind"] in ("reference", "port") and line["cpu_baseline"]["cores"] >= 1
+    if line["cpu_baseline"]["kind"] == "reference":  # paircorr itself timed, the C port beside it
+        assert "paircorr" in line["cpu_baseline"]["sample"] and line["port_baseline"]["kind"] == "port"
+    else:
+        assert "reference_unavailable" in line
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
     assert line["config"]["workload"].startswith("c1")
 
@@ -43,7 +48,7 @@ def test_reference_arm_under_torchrun_prints_one_line():
     out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
                           "--master-addr", "127.0.0.1", "--master-port", str(port), str(ROOT / "bench.py"),
                           "--impl", "reference", "--gpus", "2", "--config", "c1", "--steps", "1", "--warmup", "1",
-                          "--cpu-fraction", "0.05"], capture_output=True, text=True, cwd=ROOT, timeout=300)
+                          "--cpu-fraction", "0.05", "--ref-seconds", "0.5"], capture_output=True, text=True, cwd=ROOT, timeout=300)
     assert out.returncode == 0, out.stderr[-2000:]
     lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
     assert len(lines) == 1

@@ -514,6 +514,57 @@ def test_subprocess_gpu_workers_match_single_engine(rng, monkeypatch):
     assert hi - lo > 0 and ei.value.worker_index in (0, 1)
 
 
+def test_allpairs_backend_subprocess_routes_to_worker_processes(rng, monkeypatch):
+    """allpairs(..., backend="subprocess") runs GPU worker processes on the
+    reference's protocol, as engine.py:46-56 routes it: same bits as the
+    in-process engine, and PAIRCORR_FAIL_AFTER_PASSES reaches the workers
+    through the drop-in entry point (WorkerError with the unfinished range)."""
+    x = random_values(rng, 300, 20, special_rows=True)
+    d = pc.Dataset(values=x)
+    ref = pc.allpairs(d)
+    for workers in (1, 2):
+        got = pc.allpairs(d, workers=workers, backend="subprocess", capacity=500, threads=2)
+        assert np.array_equal(got.packed, ref.packed) and got.zero_variance == ref.zero_variance
+    monkeypatch.setenv("PAIRCORR_FAIL_AFTER_PASSES", "1")
+    with pytest.raises(pc.WorkerError) as ei:
+        pc.allpairs(d, workers=2, backend="subprocess", capacity=500)
+    lo, hi = ei.value.unfinished_range
+    assert hi > lo and ei.value.worker_index in (0, 1)
+
+
+@pytest.mark.parametrize("method", ["tensor", "split", "exact"])
+def test_run_workers_device_slots_exchange_bitwise(rng, method):
+    """In-process multi-device workers: each device slot uploads only its row
+    block of X and one broadcast K1 kernel writes the normalised rows into
+    every slot's U (distributed.normalize_on_devices; peer stores over NVLink
+    between GPUs, local stores when slots share a GPU, as here) -- every
+    coefficient bitwise equal to the single-device engine."""
+    x = random_values(rng, 700, 45, special_rows=True)
+    ref = pc.allpairs(pc.Dataset(values=x), method=method)
+    for devs, p in (([0, 0], 2), ([0, 0, 0], 5), ([0], 3)):
+        for values in (x, torch.from_numpy(x).pin_memory(), torch.from_numpy(x).cuda()):
+            got = pc.run_workers(pc.Dataset(values=values), None, p, devices=devs, method=method)
+            assert np.array_equal(got.packed, ref.packed), (devs, p, method)
+            assert got.zero_variance == ref.zero_variance == frozenset({1})
+    n_dev = torch.cuda.device_count()
+    if n_dev >= 2:  # the real multi-GPU path: peer access + per-device kernel setup
+        got = pc.allpairs(pc.Dataset(values=x), devices=2, method=method)
+        assert np.array_equal(got.packed, ref.packed)
+
+
+def test_normalize_on_devices_rows_bit_exact(rng):
+    from paper_1605_01584_b200.distributed import normalize_on_devices
+
+    x = random_values(rng, 1100, 33, special_rows=True)
+    u_ref, zv_ref = oracle.normalize(x)
+    outs = normalize_on_devices(x, 1100, 33, [torch.device("cuda", 0)] * 3)
+    assert len(outs) == 3
+    for u, flags in outs:
+        assert np.array_equal(u[:1100, :33].cpu().numpy(), u_ref)
+        assert float(u[1100:].abs().max()) == 0.0 and float(u[:, 33:].abs().max()) == 0.0
+        assert np.array_equal(flags[:1100].cpu().numpy().astype(bool), zv_ref)
+
+
 def test_acceptance_criterion_2_random_datasets_vs_naive_oracle():
     """The reference's acceptance criterion 2 (test_acceptance.py:88-113):
     50 random datasets with planted constant / negated / affine rows, random

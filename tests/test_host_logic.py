@@ -447,3 +447,32 @@ def test_split_bound_rejected_before_any_device_work():
         pc.allpairs(pc.Dataset(values=x), method="split")
     with pytest.raises(ValueError, match="method"):
         pc.allpairs(pc.Dataset(values=x[:, :10]), method="fp32")
+
+
+def test_allpairs_routes_backend_like_the_reference(monkeypatch, tmp_path):
+    """engine.py:46-56: workers > 1 or backend != "in_process" goes to
+    run_workers(dataset, geom, workers, backend, capacity, threads); a path
+    stays a path so subprocess workers load the file themselves."""
+    from paper_1605_01584_b200 import engine
+
+    calls = []
+    monkeypatch.setattr(engine, "resolve_devices", lambda devices=None: [torch.device("cuda", 0)])
+    monkeypatch.setattr(engine, "run_workers", lambda *a, **k: calls.append((a, k)) or "routed")
+    x = np.random.default_rng(0).random((10, 5))
+    ds = pc.Dataset(values=x)
+    assert engine.allpairs(ds, workers=2, backend="subprocess", capacity=3, threads=2) == "routed"
+    a, k = calls[-1]
+    assert a[0] is ds and a[1].n == 10 and a[2:] == (2, "subprocess", 3, 2) and k["method"] == "tensor"
+    assert engine.allpairs(ds, backend="subprocess") == "routed"
+    a, _ = calls[-1]
+    assert a[2:4] == (1, "subprocess") and a[4] == engine.default_capacity(4)
+    path = tmp_path / "d.lpcc"
+    pc.save_dataset(path, ds)
+    engine.allpairs(path, workers=3, backend="subprocess")
+    assert calls[-1][0][0] == path
+    assert engine.allpairs(ds, workers=2) == "routed"  # in-process workers: the CUDA thread backend
+    assert calls[-1][1]["backend"] == "cuda"
+    with pytest.raises(ValueError, match="subprocess"):
+        engine.allpairs(ds, backend="subprocess", output="dense")
+    with pytest.raises(ValueError, match="backend"):
+        engine.allpairs(ds, backend="mpi")

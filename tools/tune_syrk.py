@@ -1,11 +1,17 @@
 """Time every contraction kernel shape (pcc_syrk_f64_variant) on the BASELINE
-configs and check they agree bit for bit.  Prints one line per (config, variant)."""
+configs and check they agree bit for bit.  Prints one line per (config, variant).
+
+The tuning shapes 1..14 are not in the product library: this tool loads the
+tools build (``make -C tools`` -> tools/libpcc_tune.so, the same source with
+-DPCC_TUNING_VARIANTS)."""
 
 import argparse
 import sys
 from pathlib import Path
 
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
+import ctypes  # noqa: E402
 
 import torch  # noqa: E402
 
@@ -15,13 +21,22 @@ from paper_1605_01584_b200.transform import normalize_device  # noqa: E402
 from paper_1605_01584_b200.workloads import CONFIGS, make_config  # noqa: E402
 
 
+def _check(L, rc):
+    if rc != 0:
+        raise RuntimeError(L.pcc_last_error().decode())
+
+
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("--configs", default="c2,c3")
     p.add_argument("--variants", default="0,1,2,3,4")
     p.add_argument("--reps", type=int, default=3)
     a = p.parse_args()
-    L = _lib.lib()
+    tune_path = Path(__file__).resolve().parent / "libpcc_tune.so"
+    if not tune_path.exists():
+        raise SystemExit("build the tools library first: make -C tools")
+    L = ctypes.CDLL(str(tune_path))
+    _lib._bind(L)
     peak = _lib.probe_fp64_peak()
     print(f"DMMA probe peak {peak:.2f} TFLOP/s", flush=True)
     for cfg in a.configs.split(","):
@@ -38,7 +53,7 @@ def main():
             for r in range(a.reps + 1):
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
-                _lib.check(L.pcc_syrk_f64_variant(v, ptr(u), n, l, u.shape[1], 0, T, 0, ptr(out), 0, 0, 0, 0, 0, s))
+                _check(L, L.pcc_syrk_f64_variant(v, ptr(u), n, l, u.shape[1], 0, T, 0, ptr(out), 0, 0, 0, 0, 0, s))
                 e1.record()
                 torch.cuda.synchronize()
                 if r:
