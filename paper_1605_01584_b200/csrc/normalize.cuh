@@ -108,6 +108,28 @@ __device__ __forceinline__ double lane_sum(const double *p, int nsteps) {
   return s;
 }
 
+// u = a / b bit-identical to IEEE division (__ddiv_rn), one FMA correction
+// instead of a full division per element: with y = RN(1/b) (one __drcp_rn
+// per row) and q0 = RN(a y), q = RN(q0 + (a - b q0) y) is the correctly rounded
+// quotient (Markstein's correction step; a - b q0 is exact by FMA) as long as
+// no intermediate underflows -- guarded here to |a| >= 2^-520 and b in
+// [2^-500, 2^500]; everything else (zeros, huge or tiny values) takes
+// __ddiv_rn.  tools/div_check.cu compares the two on 3e10 random pairs.
+struct RowDiv {
+  double b, y;
+  bool fast;
+};
+__device__ __forceinline__ RowDiv row_div(double b) {
+  return RowDiv{b, __drcp_rn(b), b >= 0x1p-500 && b <= 0x1p500};
+}
+__device__ __forceinline__ double div_rn(double a, const RowDiv &d) {
+  if (d.fast && fabs(a) >= 0x1p-520) {
+    const double q0 = __dmul_rn(a, d.y);
+    return __fma_rn(__fma_rn(-q0, d.b, a), d.y, q0);
+  }
+  return __ddiv_rn(a, d.b);
+}
+
 constexpr int kNormThreads = 256;
 constexpr int kNormRowsPerCta = kNormThreads / 8;
 
@@ -155,7 +177,8 @@ normalize_rows_kernel(const double *__restrict__ x, int64_t ldx, double *__restr
     return;
   }
   const double scale = __dsqrt_rn(ssd);
-  for (k = lane8; k < l; k += 8) ur[k] = __ddiv_rn(__dsub_rn(__ldg(xr + k), mean), scale);
+  const RowDiv dv = row_div(scale);
+  for (k = lane8; k < l; k += 8) ur[k] = div_rn(__dsub_rn(__ldg(xr + k), mean), dv);
   for (k = l + lane8; k < ldu; k += 8) ur[k] = 0.0;
 }
 
@@ -239,16 +262,20 @@ normalize_rows_smem_kernel(const double *__restrict__ x, int64_t ldx, double *__
   __shared__ __align__(8) uint64_t s_bar;
   const bool bulk = (((reinterpret_cast<uintptr_t>(x) | (uintptr_t)(ldx * 8)) & 15) == 0) && (l % 2 == 0);
   if (bulk) {
+    // one issuing thread per row: bulk copies issued by one thread complete
+    // one after another (tools/bulk_bw.cu), so the rows go out in parallel
+    const uint32_t bar = smem_u32(&s_bar);
     if (tid == 0) {
-      const uint32_t bar = smem_u32(&s_bar);
-      mbar_init(bar, 1);
+      mbar_init(bar, (uint32_t)rows);
       mbar_fence_init();
-      mbar_arrive_expect_tx(bar, (uint32_t)(rows * l * sizeof(double)));
-      for (int r = 0; r < rows; ++r)
-        bulk_copy_row(sbase + (uint32_t)(r * l * sizeof(double)), x + (r0 + r) * ldx, (uint32_t)(l * sizeof(double)),
-                      bar);
-      mbar_wait(bar, 0);
     }
+    __syncthreads();
+    if (tid < rows) {
+      mbar_arrive_expect_tx(bar, (uint32_t)(l * sizeof(double)));
+      bulk_copy_row(sbase + (uint32_t)(tid * l * sizeof(double)), x + (r0 + tid) * ldx, (uint32_t)(l * sizeof(double)),
+                    bar);
+    }
+    if (tid == 0) mbar_wait(bar, 0);
   }
   for (int r = 0; r < rows && !bulk; ++r) {
     const double *xr = x + (r0 + r) * ldx;
@@ -340,12 +367,13 @@ normalize_rows_smem_kernel(const double *__restrict__ x, int64_t ldx, double *__
       }
       if (tid == 0) dests.scale[r0 + r] = m > 0.0 ? ldexp(1.0, e - 7) : 0.0;
       const double pw = m > 0.0 ? ldexp(1.0, 7 - e) : 0.0;  // 7 - e <= 14 for unit-norm rows
+      const RowDiv dv = row_div(sc);
       for (int64_t k = 4 * (int64_t)tid; k < kpad; k += 4 * kNormSmemThreads) {
         uint32_t packed[7] = {};
         if (m > 0.0) {
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            double v = (k + j < l) ? __ddiv_rn(__dsub_rn(ds[k + j], m0), sc) * pw : 0.0;
+            double v = (k + j < l) ? div_rn(__dsub_rn(ds[k + j], m0), dv) * pw : 0.0;
 #pragma unroll
             for (int i = 0; i < 7; ++i) {
               const double t = __dadd_rn(v, 0x1.8p52);  // rint by the 1.5 * 2^52 shift
@@ -378,20 +406,21 @@ normalize_rows_smem_kernel(const double *__restrict__ x, int64_t ldx, double *__
     if (s_zero[r]) {
       for (int64_t k = tid; k < ldu; k += kNormSmemThreads) put(k, 0.0);
     } else {
-      const double sc = s_scale[r], m = s_mean[r];
+      const double m = s_mean[r];
+      const RowDiv dv = row_div(s_scale[r]);
       // u = (x - mean) / scale; four independent divisions per iteration keep
       // more of their latency in flight
       constexpr int64_t T = kNormSmemThreads;
       int64_t k = tid;
       for (; k + 3 * T < l; k += 4 * T) {
-        const double q0 = __ddiv_rn(__dsub_rn(ds[k], m), sc), q1 = __ddiv_rn(__dsub_rn(ds[k + T], m), sc);
-        const double q2 = __ddiv_rn(__dsub_rn(ds[k + 2 * T], m), sc), q3 = __ddiv_rn(__dsub_rn(ds[k + 3 * T], m), sc);
+        const double q0 = div_rn(__dsub_rn(ds[k], m), dv), q1 = div_rn(__dsub_rn(ds[k + T], m), dv);
+        const double q2 = div_rn(__dsub_rn(ds[k + 2 * T], m), dv), q3 = div_rn(__dsub_rn(ds[k + 3 * T], m), dv);
         put(k, q0);
         put(k + T, q1);
         put(k + 2 * T, q2);
         put(k + 3 * T, q3);
       }
-      for (; k < l; k += T) put(k, __ddiv_rn(__dsub_rn(ds[k], m), sc));
+      for (; k < l; k += T) put(k, div_rn(__dsub_rn(ds[k], m), dv));
       for (k = l + tid; k < ldu; k += kNormSmemThreads) put(k, 0.0);
     }
   }

@@ -209,7 +209,18 @@ int configure_normalize(int *regs) {
 // Per-device one-time setup (smem opt-in, occupancy); returns the config of
 // the calling thread's current device.
 int device_config(const DeviceConfig **out, int device = -1) {
-  if (device < 0) PCC_CUDA(cudaGetDevice(&device), "cudaGetDevice");
+  if (device < 0) {
+    PCC_CUDA(cudaGetDevice(&device), "cudaGetDevice");
+    // A fresh host thread has no current driver context until a runtime call
+    // binds the device's primary context; the driver entry points used below
+    // (cuTensorMapEncodeTiled) need one.  cudaSetDevice binds it (once per
+    // thread and device).
+    static thread_local int bound = -1;
+    if (bound != device) {
+      PCC_CUDA(cudaSetDevice(device), "cudaSetDevice");
+      bound = device;
+    }
+  }
   if (device >= kMaxDevices) return fail(PCC_EINVAL, "device %d out of range", device);
   std::lock_guard<std::mutex> lock(g_dev_mu);
   DeviceConfig &c = g_dev[device];
@@ -550,7 +561,7 @@ int pcc_normalize_rows_bcast_f64(const double *x, int64_t ldx, double *const *u,
   }
   if (row_hi == row_lo) return PCC_OK;
   const int rc = launch_normalize_staged<pcc::kNormBcast>(x, ldx, nullptr, ldu, nullptr, l, row_lo, row_hi, d,
-                                               (cudaStream_t)stream);
+                                                (cudaStream_t)stream);
   if (rc == kNotStaged)
     return fail(PCC_EINVAL, "rows of %lld samples are too long for the broadcast normaliser", (long long)l);
   return rc;

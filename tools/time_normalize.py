@@ -10,6 +10,7 @@ from paper_1605_01584_b200.workloads import CONFIGS, make_config
 
 def main():
     p = argparse.ArgumentParser(); p.add_argument("--configs", default="c1,c2,c3,c4,c5"); p.add_argument("--reps", type=int, default=5)
+    p.add_argument("--check", action="store_true", help="also compare U and the flags bit for bit with the CPU oracle")
     a = p.parse_args()
     L = _lib.lib()
     peaks = {}
@@ -33,6 +34,15 @@ def main():
             e1.record(); torch.cuda.synchronize()
             if r: best = min(best, e0.elapsed_time(e1))
         byt = 8.0 * n * l * 2
+        if a.check:
+            import numpy as np
+            sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+            import oracle
+            xh = make_config(cfg)
+            u_ref, zv_ref = oracle.normalize(xh)
+            same = np.array_equal(u[:n, :l].cpu().numpy().view(np.uint64), u_ref.view(np.uint64)) and \
+                np.array_equal(fl.cpu().numpy().astype(bool), zv_ref) and float(u[:, l:].abs().max() if ldu > l else 0) == 0.0
+            print(f"{cfg}: bit-exact vs oracle: {same}", flush=True)
         print(f"{cfg}: normalize {best*1e3:8.1f} us  {byt/best/1e6:7.1f} GB/s algorithmic  {byt/best/1e6/hbm*100:5.1f}% of HBM {hbm:.0f} GB/s", flush=True)
         del x, u, fl; torch.cuda.empty_cache()
 
