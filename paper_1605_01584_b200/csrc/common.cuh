@@ -109,6 +109,23 @@ __host__ __device__ inline void tile_at(const TileOrder &o, uint64_t m, uint64_t
   X = J + Y - row_prefix(m, Y);
 }
 
+// Split-mode digits (split.cuh): the 7 balanced radix-128 digits of v in
+// (-128, 128), d_i = rint(128^i r_i) with r_0 = v, r_{i+1} = r_i - d_i 128^-i
+// (round to nearest, ties to even; every step exact).  Written with the shift
+// constants C_i = 1.5 * 2^(52 - 7i): t = RN(r + C_i) rounds r to a multiple of
+// 128^-i, so the digit is the low byte of t's bit pattern and t - C_i is
+// d_i 128^-i exactly -- three FP64 operations per digit.  Digit i of
+// element j (0..3) goes to byte j of packed[i].
+__device__ __forceinline__ void split_digits7(double v, int j, uint32_t packed[7]) {
+  constexpr double C[7] = {0x1.8p52, 0x1.8p45, 0x1.8p38, 0x1.8p31, 0x1.8p24, 0x1.8p17, 0x1.8p10};
+#pragma unroll
+  for (int i = 0; i < 7; ++i) {
+    const double t = __dadd_rn(v, C[i]);
+    v = __dsub_rn(v, __dsub_rn(t, C[i]));
+    packed[i] |= ((uint32_t)__double2loint(t) & 0xFFu) << (8 * j);
+  }
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

@@ -32,8 +32,9 @@ namespace pcc {
 // sequential -- runs at FP64-add latency instead of load latency.
 // SSD = false: sum8 lane + constancy test against `ref` (= x[0]);
 // SSD = true:  ssd8 lane with `ref` = mean.
-template <bool SSD, int PF>
-__device__ __forceinline__ double lane_chain(const double *p, int64_t nsteps64, double ref, bool &varies) {
+template <bool SSD, int PF, bool DMAX = false>
+__device__ __forceinline__ double lane_chain(const double *p, int64_t nsteps64, double ref, bool &varies,
+                                             double *dmax = nullptr) {
   const int nsteps = (int)nsteps64;
   const int full = (nsteps / PF) * PF;
   double s = 0.0;
@@ -56,6 +57,7 @@ __device__ __forceinline__ double lane_chain(const double *p, int64_t nsteps64, 
       if (SSD) {
         const double d = __dsub_rn(cur[i], ref);
         s = __dadd_rn(s, __dmul_rn(d, d));
+        if (DMAX) *dmax = fmax(*dmax, fabs(d));
       } else {
         s = __dadd_rn(s, cur[i]);
         varies |= (cur[i] != ref);
@@ -67,6 +69,7 @@ __device__ __forceinline__ double lane_chain(const double *p, int64_t nsteps64, 
     if (SSD) {
       const double d = __dsub_rn(v, ref);
       s = __dadd_rn(s, __dmul_rn(d, d));
+      if (DMAX) *dmax = fmax(*dmax, fabs(d));
     } else {
       s = __dadd_rn(s, v);
       varies |= (v != ref);
@@ -299,6 +302,32 @@ normalize_rows_smem_kernel(const double *__restrict__ x, int64_t ldx, double *__
   //    (every element vs the first; OR of the 8 lanes), the mean, then ssd8
   //    with the centring d = x - mean inline (the subtract and square are off
   //    the dependent add chain).  No CTA barrier between the phases.
+  // Digit planes need max |x - mean| per row = max(RN(xmax - mean), RN(mean -
+  // xmin)) (RN is monotone and odd), so the row's min and max -- order-free --
+  // are taken by the warps that run no lane chains, while the chains run.
+  constexpr int kWarps = kNormSmemThreads / 32;
+  __shared__ double s_min[kWarps][kNormSmemMaxRows], s_max[kWarps][kNormSmemMaxRows];
+  const int chain_warps = (rows * 8 + 31) / 32;
+  if (MODE == kNormDigits && (tid >> 5) >= chain_warps) {
+    const int fw = (tid >> 5) - chain_warps, nfw = kWarps - chain_warps;
+    for (int r = 0; r < rows; ++r) {
+      const double *ds = srow + (int64_t)r * l;
+      double lo = ds[0], hi = ds[0];
+      for (int64_t k = fw * 32 + (tid & 31); k < l; k += nfw * 32) {
+        lo = fmin(lo, ds[k]);
+        hi = fmax(hi, ds[k]);
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+      }
+      if ((tid & 31) == 0) {
+        s_min[tid >> 5][r] = lo;
+        s_max[tid >> 5][r] = hi;
+      }
+    }
+  }
   const int lane8 = tid & 7;
   const int row = tid >> 3;
   const bool active = row < rows;
@@ -340,25 +369,41 @@ normalize_rows_smem_kernel(const double *__restrict__ x, int64_t ldx, double *__
     //     each thread turns 4 consecutive u values -- the same IEEE
     //     operations as below, so the same bits as K1 + pcc_split_rows_f64 --
     //     into 7 radix-128 digits, one 32-bit store per digit plane
-    __shared__ double s_wmax[kNormSmemThreads / 32];
     constexpr int W = 64;  // SplitCfg::kRowBytes
     const int64_t kpad = (l + W - 1) / W * W;
     const int64_t plane = dests.rows_total * W;
+    const int nfw = kWarps - chain_warps;
+    if (nfw == 0) {  // every warp ran chains: min / max now, by all threads
+      for (int r = 0; r < rows; ++r) {
+        const double *ds = srow + (int64_t)r * l;
+        double lo = ds[0], hi = ds[0];
+        for (int64_t k = tid; k < l; k += kNormSmemThreads) {
+          lo = fmin(lo, ds[k]);
+          hi = fmax(hi, ds[k]);
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+          hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        }
+        if ((tid & 31) == 0) {
+          s_min[tid >> 5][r] = lo;
+          s_max[tid >> 5][r] = hi;
+        }
+      }
+      __syncthreads();
+    }
+    const int w0 = nfw == 0 ? 0 : chain_warps, w1 = kWarps;
     for (int r = 0; r < rows; ++r) {
       const double *ds = srow + (int64_t)r * l;
       const bool zero = s_zero[r] != 0;
       const double m0 = s_mean[r], sc = s_scale[r];
-      double dm = 0.0;
-      if (!zero)
-        for (int64_t k = tid; k < l; k += kNormSmemThreads) dm = fmax(dm, fabs(__dsub_rn(ds[k], m0)));
-#pragma unroll
-      for (int o = 16; o; o >>= 1) dm = fmax(dm, __shfl_xor_sync(0xffffffffu, dm, o));
-      if ((tid & 31) == 0) s_wmax[tid >> 5] = dm;
-      __syncthreads();
-      dm = 0.0;
-#pragma unroll
-      for (int w = 0; w < kNormSmemThreads / 32; ++w) dm = fmax(dm, s_wmax[w]);
-      __syncthreads();  // s_wmax is reused by the next row
+      double lo = s_min[w0][r], hi = s_max[w0][r];
+      for (int w = w0 + 1; w < w1; ++w) {
+        lo = fmin(lo, s_min[w][r]);
+        hi = fmax(hi, s_max[w][r]);
+      }
+      const double dm = fmax(__dsub_rn(hi, m0), __dsub_rn(m0, lo));  // = max_k |RN(x_k - mean)|
       const double m = zero ? 0.0 : __ddiv_rn(dm, sc);
       int e = 0;
       if (m > 0.0) {
@@ -372,16 +417,7 @@ normalize_rows_smem_kernel(const double *__restrict__ x, int64_t ldx, double *__
         uint32_t packed[7] = {};
         if (m > 0.0) {
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            double v = (k + j < l) ? div_rn(__dsub_rn(ds[k + j], m0), dv) * pw : 0.0;
-#pragma unroll
-            for (int i = 0; i < 7; ++i) {
-              const double t = __dadd_rn(v, 0x1.8p52);  // rint by the 1.5 * 2^52 shift
-              const double d = __dsub_rn(t, 0x1.8p52);
-              v = __dmul_rn(__dsub_rn(v, d), 128.0);   // exact
-              packed[i] |= ((uint32_t)__double2loint(t) & 0xFFu) << (8 * j);
-            }
-          }
+          for (int j = 0; j < 4; ++j) split_digits7((k + j < l) ? div_rn(__dsub_rn(ds[k + j], m0), dv) * pw : 0.0, j, packed);
         }
         int8_t *dst = dests.slices + (k / W) * 7 * plane + (r0 + r) * W + (k % W);
 #pragma unroll

@@ -242,18 +242,7 @@ __global__ void __launch_bounds__(256) split_rows_kernel(const double *__restric
     }
     uint32_t packed[SplitCfg::kSlices] = {};
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      double v = pw_ok ? x4[j] * pw : ldexp(x4[j], 7 - e);
-#pragma unroll
-      for (int i = 0; i < SplitCfg::kSlices; ++i) {
-        // round to the nearest integer, ties to even (= rint) by the 1.5 * 2^52
-        // shift: the digit is then also the low byte of t's bit pattern
-        const double t = __dadd_rn(v, 0x1.8p52);
-        const double d = __dsub_rn(t, 0x1.8p52);
-        v = __dmul_rn(__dsub_rn(v, d), 128.0);   // exact: fractional part, times a power of two
-        packed[i] |= ((uint32_t)__double2loint(t) & 0xFFu) << (8 * j);
-      }
-    }
+    for (int j = 0; j < 4; ++j) split_digits7(pw_ok ? x4[j] * pw : ldexp(x4[j], 7 - e), j, packed);
     const int64_t kb = k / W;
     int8_t *dst = slices + (kb * SplitCfg::kSlices) * plane + r * W + (k % W);
 #pragma unroll

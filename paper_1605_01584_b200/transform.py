@@ -10,9 +10,10 @@ order, exact constant-row test, ``ssd == 0.0`` guard, IEEE division and
 square root.
 
 Device layout of U: ``pcc_rows_padded(n) x pcc_ldu(l)`` row-major float64
-(rows padded to the 128-row GPU tile, K padded to 16 doubles = 128 bytes so
-every row starts on a cache line); the pad is zero, which leaves every dot
-product unchanged.
+(rows padded to the 128-row GPU tile, K padded to PCC_K_ALIGN = 32 doubles =
+256 bytes so every row starts on a cache-line pair and every TMA box of the
+contraction stays in bounds); the pad is zero, which leaves every dot product
+unchanged.
 """
 
 from __future__ import annotations
