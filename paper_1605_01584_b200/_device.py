@@ -11,7 +11,13 @@ import torch
 
 from .errors import DeviceError
 
-__all__ = ["require_cuda", "resolve_devices", "stream_handle", "as_device_f64", "ptr"]
+__all__ = ["require_cuda", "resolve_devices", "stream_handle", "as_device_f64", "ptr", "nvtx"]
+
+
+def nvtx(name: str):
+    """NVTX range around a host-side phase (visible in Nsight Systems / ncu
+    --nvtx timelines): ``with nvtx("pcc.allpairs"): ...``."""
+    return torch.cuda.nvtx.range(name)
 
 
 def require_cuda() -> None:

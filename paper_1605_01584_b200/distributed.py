@@ -31,7 +31,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._device import as_device_f64, ptr, resolve_devices, stream_handle
+from ._device import as_device_f64, nvtx, ptr, resolve_devices, stream_handle
 from .errors import IntegrityError, WorkerError
 from .indexing import sym_job_coord, sym_job_count
 from .tiles import CorrelationResult, TileGeometry
@@ -617,7 +617,8 @@ def compute_worker(dataset: Dataset, p: int, worker_index: int, device=None, out
         if host.numel() < hi_span - lo_span:
             raise ValueError(f"out holds {host.numel()} values, shard needs {hi_span - lo_span}")
     if group is not None and p > 1:
-        u, flags = exchange_normalize(dataset.values, n, l, worker_index, p, dev, group, exchange=exchange)
+        with nvtx("pcc.compute_worker.exchange_normalize"):
+            u, flags = exchange_normalize(dataset.values, n, l, worker_index, p, dev, group, exchange=exchange)
         lo, hi = shard_span(n, a.start, a.stop)
         with torch.cuda.device(dev):
             vals = torch.empty(max(hi - lo, 1), dtype=torch.float64, device=dev)
@@ -693,7 +694,8 @@ def run_workers(
     # slot -- row blocks + broadcast over NVLink with several -- then every
     # worker contracts its range against its slot's U
     slots = devs[:p]
-    normed = normalize_on_devices(dataset.values, n, l, slots)
+    with nvtx("pcc.run_workers.normalize_on_devices"):
+        normed = normalize_on_devices(dataset.values, n, l, slots)
     cons: list = [None] * len(slots)
 
     def run_one(a: WorkerAssignment) -> None:
@@ -712,8 +714,9 @@ def run_workers(
         with torch.cuda.device(slots[q]):
             cons[q] = _lib.Contraction(method, u, n, l).prepare_all(stream_handle())
     if len(slots) == 1:
-        for a in assignments:
-            run_one(a)
+        with nvtx("pcc.run_workers.contract"):
+            for a in assignments:
+                run_one(a)
     else:
         ts = [threading.Thread(target=run_one, args=(a,)) for a in assignments]
         for t in ts:

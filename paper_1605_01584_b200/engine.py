@@ -26,7 +26,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._device import as_device_f64, ptr, resolve_devices, stream_handle
+from ._device import as_device_f64, nvtx, ptr, resolve_devices, stream_handle
 from .distributed import BACKENDS, run_workers
 from .indexing import sym_job_count
 from .stream import run_stream
@@ -227,6 +227,13 @@ def allpairs(
       ~2.4x the tensor path's speed; l <= 8192) or ``"exact"`` (same as
       ``exact=True``).
     """
+    with nvtx("pcc.allpairs"):
+        return _allpairs(dataset, tile_size, capacity, threads, workers, backend, buffer_budget, devices, output,
+                         keep_on_device, out, chunk_rows, exact, method)
+
+
+def _allpairs(dataset, tile_size, capacity, threads, workers, backend, buffer_budget, devices, output, keep_on_device,
+              out, chunk_rows, exact, method):
     source = dataset  # a path stays a path for subprocess workers (engine.py:55-56)
     if not isinstance(dataset, Dataset):
         from .fileio import load_dataset

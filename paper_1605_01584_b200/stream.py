@@ -221,6 +221,7 @@ def run_stream(x, n: int, l: int, device: torch.device, tile_begin: int, tile_en
     """
 
     def mark(label, stream):
+        torch.cuda.nvtx.mark(f"pcc.stream.{label}")
         if trace is not None:
             ev = torch.cuda.Event(enable_timing=True)
             ev.record(stream)
