@@ -252,7 +252,7 @@ __global__ void __launch_bounds__(256) split_rows_kernel(const double *__restric
 
 // ---- the contraction ----------------------------------------------------
 template <int LAYOUT>
-__global__ void __maxnreg__(200)
+__global__ void __launch_bounds__(SplitCfg::kThreads, 1)
     syrk_split_kernel(const __grid_constant__ CUtensorMap map1, const double *__restrict__ scale, int64_t n, int64_t l, int k_blocks, uint64_t m_g,
                       TileOrder order, Epilogue ep, int dbg) {
   using C = SplitCfg;
