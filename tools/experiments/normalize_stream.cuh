@@ -57,10 +57,10 @@ __device__ unsigned long long g_k1s_probe[8];
 #endif
 
 struct K1Stream {
-  static constexpr int kWin = 512;       // doubles per row window
+  static constexpr int kWin = 1024;      // doubles per row window
   static constexpr int kRows = 4;        // rows per chain warp (8 lanes each)
   // ring depth (windows in flight per chain warp): 6 with 1-2 chain warps, 3 with 3-4
-  __host__ __device__ static constexpr int stages(int cw) { return cw <= 2 ? 6 : 3; }
+  __host__ __device__ static constexpr int stages(int cw) { return cw <= 2 ? 3 : 1; }
   static constexpr int kHand = 2;        // handoff slots per chain warp (chain -> output warps)
   static constexpr int kApplyWarps = 8;  // output warps per CTA
   static constexpr int kStageDoubles = kRows * kWin;
@@ -388,7 +388,7 @@ normalize_rows_stream_kernel(const double *__restrict__ x, int64_t ldx, double *
           double v4[4] = {a0.x, a0.y, a1.x, a1.y};
 #pragma unroll
           for (int i = 0; i < 4; ++i)
-            v4[i] = (k + i < l && !zero) ? __dmul_rn(__ddiv_rn(__dsub_rn(v4[i], m), sc), pw) : 0.0;
+            v4[i] = (k + i < l && !zero) ? __dmul_rn(div_rn(__dsub_rn(v4[i], m), row_div(sc)), pw) : 0.0;
           uint32_t packed[7];
           digits4(v4, m, sc, pw, pw > 0.0, packed);
           int8_t *dst = dests.slices + (k / W) * 7 * plane + (r0 + rr) * W + (k % W);
@@ -408,47 +408,36 @@ normalize_rows_stream_kernel(const double *__restrict__ x, int64_t ldx, double *
         // chunk's U 16-byte loads in flight while this chunk is divided and
         // stored; the chunk sequence runs over the group's rows and the zero
         // K padding (l and ldu are even, so a 16-byte pair never straddles l)
-        constexpr int U = 4, CH = 2 * AT * U;
-        const int64_t chunks_row = (ldu + CH - 1) / CH;
-        const int64_t nchunks = rows * chunks_row;
-        auto load = [&](int64_t q, double2 (&v)[U]) {
-          const int rr = (int)(q / chunks_row);
-          const int64_t k = (q - rr * chunks_row) * CH + 2 * ta;
-          const double *xr = x + (r0 + rr) * ldx;
-#pragma unroll
-          for (int i = 0; i < U; ++i)
-            v[i] = (k + 2 * AT * i < l) ? __ldcs(reinterpret_cast<const double2 *>(xr + k + 2 * AT * i))
-                                        : make_double2(0.0, 0.0);
-        };
-        auto emit = [&](int64_t q, double2 (&v)[U]) {
-          const int rr = (int)(q / chunks_row);
-          const int64_t k = (q - rr * chunks_row) * CH + 2 * ta;
-          const double m = hs[rr], sc = hs[C::kRows + rr];
+        constexpr int U = 16, CH = 2 * AT * U;
+        for (int rr = 0; rr < rows; ++rr) {
+          const double m = hs[rr];
           const bool zero = hs[3 * C::kRows + rr] != 0.0;
+          const RowDiv dv = row_div(hs[C::kRows + rr]);
+          const double *xr = x + (r0 + rr) * ldx;
           const int64_t off = (r0 + rr) * ldu;
+          for (int64_t k0 = 2 * (int64_t)ta; k0 < ldu; k0 += CH) {
+            double2 v[U];
 #pragma unroll
-          for (int i = 0; i < U; ++i) {
-            const int64_t kk = k + 2 * AT * i;
-            if (kk >= ldu) continue;
-            double2 o = make_double2(0.0, 0.0);
-            if (!zero && kk < l) {
-              o.x = __ddiv_rn(__dsub_rn(v[i].x, m), sc);
-              o.y = __ddiv_rn(__dsub_rn(v[i].y, m), sc);
+            for (int i = 0; i < U; ++i) {
+              const int64_t kk = k0 + 2 * AT * i;
+              v[i] = (kk < l) ? __ldcs(reinterpret_cast<const double2 *>(xr + kk)) : make_double2(0.0, 0.0);
             }
-            if (MODE == kNormBcast) {
-              for (int d = 0; d < dests.n; ++d) __stcs(reinterpret_cast<double2 *>(dests.u[d] + off + kk), o);
-            } else {
-              __stcs(reinterpret_cast<double2 *>(u + off + kk), o);
+#pragma unroll
+            for (int i = 0; i < U; ++i) {
+              const int64_t kk = k0 + 2 * AT * i;
+              if (kk >= ldu) continue;
+              double2 o = make_double2(0.0, 0.0);
+              if (!zero && kk < l) {
+                o.x = div_rn(__dsub_rn(v[i].x, m), dv);
+                o.y = div_rn(__dsub_rn(v[i].y, m), dv);
+              }
+              if (MODE == kNormBcast) {
+                for (int d = 0; d < dests.n; ++d) __stcs(reinterpret_cast<double2 *>(dests.u[d] + off + kk), o);
+              } else {
+                __stcs(reinterpret_cast<double2 *>(u + off + kk), o);
+              }
             }
           }
-        };
-        double2 va[U], vb[U];
-        if (nchunks > 0) load(0, va);
-        for (int64_t q = 0; q < nchunks; q += 2) {
-          if (q + 1 < nchunks) load(q + 1, vb);
-          emit(q, va);
-          if (q + 2 < nchunks) load(q + 2, va);
-          if (q + 1 < nchunks) emit(q + 1, vb);
         }
       }
       __syncwarp();

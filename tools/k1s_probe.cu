@@ -55,7 +55,6 @@ int main(int argc, char **argv) {
   cudaMemcpy(x, h.data(), n * l * 8, cudaMemcpyHostToDevice);
   run<1>(x, u, f, n, l, ldu);
   run<2>(x, u, f, n, l, ldu);
-  run<3>(x, u, f, n, l, ldu);
-  run<4>(x, u, f, n, l, ldu);
+
   return 0;
 }
