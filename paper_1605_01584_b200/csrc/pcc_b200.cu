@@ -346,7 +346,8 @@ int launch_exact(const double *u, int64_t n, int64_t l, int64_t ldu, uint64_t tb
   return PCC_OK;
 }
 
-static const int split_dbg = [] {  // experiment knob: 1 = no TMA loads, 2 = no MMAs (wrong results)
+static const int split_dbg = [] {  // experiment knob (wrong results): 1 = no TMA loads, 2 = no MMAs,
+                                   // 3 = no TMA loads and no epilogue, 4 = no MMAs and no epilogue
   const char *e = getenv("PCC_SPLIT_DEBUG");
   return e ? atoi(e) : 0;
 }();

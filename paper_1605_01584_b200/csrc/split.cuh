@@ -30,7 +30,8 @@
 // warp 1 = TMEM owner + MMA issuer (one thread), warps 2..9 = epilogue.
 // TMEM (512 columns) holds four 128 x 128 s32 accumulators, so each tile
 // takes two passes over K: pass 0 accumulates sd = 4..7 (slices 0..6),
-// pass 1 sd = 0..3 (slices 0..3), each with the "domino" schedules below
+// pass 1 sd = 0..3 (slices 0..3) -- at adaptive depth sd = 3..6 (slices
+// 0..6), then sd = 0..2 (slices 0..2) -- each with the "domino" schedules below
 // (N = 256 MMAs for neighbouring-diagonal digit pairs); the epilogue warps
 // fold pass 0 into FP64 registers (Horner) while pass 1 runs, then finish
 // and store through the same store_cell() as K2 (packed / dense / tiles).
@@ -108,12 +109,22 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap *map
 // slices land one by one) and so that consecutive MMAs mostly target
 // different accumulators.  The integer sums are exact, so any schedule gives
 // the same bits.
-// Schedule S entry e (S = 0: pass 1, diagonals 0..3, 10 products; S = 1:
-// pass 0 at full depth, diagonals 4..7, 24 products; S = 2: pass 0 at
-// adaptive depth, diagonals 4..6, 18 products, accumulator 3 unused), as
-// i | j << 3 | wide << 6 | zero << 7 -- a constexpr switch so the unrolled
-// issue loop folds every entry into immediates.
-__host__ __device__ constexpr int sched_len(int S) { return S == 0 ? 6 : (S == 1 ? 13 : 12); }
+// Schedule S entry e, as i | j << 3 | wide << 6 | zero << 7 -- a constexpr
+// switch so the unrolled issue loop folds every entry into immediates:
+//   full depth (34 products):      pass 0 = S 1, diagonals 4..7 (24 products,
+//                                  slices 0..6); pass 1 = S 0, diagonals 0..3
+//                                  (10 products, slices 0..3);
+//   adaptive depth (28 products):  pass 0 = S 3, diagonals 3..6 (22 products,
+//                                  slices 0..6); pass 1 = S 2, diagonals 0..2
+//                                  (6 products, slices 0..2, accumulator 3 unused).
+// Either way the epilogue's Horner chain runs from the top diagonal down to 0
+// in the same order (pass 0's accumulators, then pass 1's), so the split of
+// the diagonals between the passes does not change a bit of the result; the
+// adaptive split loads 10 digit slices per K block instead of 11 and issues
+// 22 N = 256 + 4 N = 128 MMAs per K step pair instead of 20 + 16.
+__host__ __device__ constexpr int sched_len(int S) { return S == 0 ? 6 : (S == 1 ? 13 : (S == 2 ? 4 : 12)); }
+// First diagonal of schedule S (its accumulator 0).
+__host__ __device__ constexpr int sched_lo(int S) { return S == 1 ? 4 : (S == 3 ? 3 : 0); }
 __host__ __device__ constexpr uint32_t sched_entry(int S, int e) {
   if (S == 0) {
     switch (e) {
@@ -142,19 +153,27 @@ __host__ __device__ constexpr uint32_t sched_entry(int S, int e) {
       case 12: return 0u | (6u << 3) | (0u << 6) | (0u << 7);  // (0, 6)
     }
   }
-  if (S == 2) {
+  if (S == 2) {  // adaptive depth, second pass: diagonals 0..2 (6 products, accumulator 3 unused)
     switch (e) {
-      case 0: return 3u | (1u << 3) | (1u << 6) | (1u << 7);  // (3, 1) wide zero
-      case 1: return 3u | (3u << 3) | (0u << 6) | (1u << 7);  // (3, 3) zero
-      case 2: return 2u | (2u << 3) | (1u << 6) | (0u << 7);  // (2, 2) wide
-      case 3: return 2u | (4u << 3) | (0u << 6) | (0u << 7);  // (2, 4)
-      case 4: return 1u | (3u << 3) | (1u << 6) | (0u << 7);  // (1, 3) wide
-      case 5: return 4u | (2u << 3) | (0u << 6) | (0u << 7);  // (4, 2)
-      case 6: return 4u | (0u << 3) | (1u << 6) | (0u << 7);  // (4, 0) wide
-      case 7: return 1u | (5u << 3) | (0u << 6) | (0u << 7);  // (1, 5)
-      case 8: return 0u | (4u << 3) | (1u << 6) | (0u << 7);  // (0, 4) wide
-      case 9: return 0u | (6u << 3) | (0u << 6) | (0u << 7);  // (0, 6)
-      case 10: return 5u | (0u << 3) | (1u << 6) | (0u << 7);  // (5, 0) wide
+      case 0: return 0u | (0u << 3) | (1u << 6) | (1u << 7);  // (0, 0) wide zero
+      case 1: return 2u | (0u << 3) | (0u << 6) | (1u << 7);  // (2, 0) zero
+      case 2: return 1u | (0u << 3) | (1u << 6) | (0u << 7);  // (1, 0) wide
+      case 3: return 0u | (2u << 3) | (0u << 6) | (0u << 7);  // (0, 2)
+    }
+  }
+  if (S == 3) {  // adaptive depth, first pass: diagonals 3..6 (22 products)
+    switch (e) {
+      case 0: return 2u | (1u << 3) | (1u << 6) | (1u << 7);  // (2, 1) wide zero
+      case 1: return 3u | (2u << 3) | (1u << 6) | (1u << 7);  // (3, 2) wide zero
+      case 2: return 3u | (0u << 3) | (1u << 6) | (0u << 7);  // (3, 0) wide
+      case 3: return 1u | (2u << 3) | (1u << 6) | (0u << 7);  // (1, 2) wide
+      case 4: return 2u | (3u << 3) | (1u << 6) | (0u << 7);  // (2, 3) wide
+      case 5: return 0u | (3u << 3) | (1u << 6) | (0u << 7);  // (0, 3) wide
+      case 6: return 4u | (2u << 3) | (0u << 6) | (0u << 7);  // (4, 2)
+      case 7: return 4u | (0u << 3) | (1u << 6) | (0u << 7);  // (4, 0) wide
+      case 8: return 1u | (4u << 3) | (1u << 6) | (0u << 7);  // (1, 4) wide
+      case 9: return 5u | (0u << 3) | (1u << 6) | (0u << 7);  // (5, 0) wide
+      case 10: return 0u | (5u << 3) | (1u << 6) | (0u << 7);  // (0, 5) wide
       case 11: return 6u | (0u << 3) | (0u << 6) | (0u << 7);  // (6, 0)
     }
   }
@@ -172,7 +191,7 @@ __device__ __forceinline__ void issue_stage(uint32_t tmem, uint32_t a, uint32_t 
                                             uint32_t phase) {
   using C = SplitCfg;
   constexpr uint32_t idesc = idesc_i8_s32<128, 128>(), idesc256 = idesc_i8_s32<128, 256>();
-  constexpr int s_lo = S == 0 ? 0 : 4;
+  constexpr int s_lo = sched_lo(S);
   const uint64_t desc0 = umma_desc_k_sw64(0);
   int ready = -1;
 #pragma unroll
@@ -291,19 +310,21 @@ __global__ void __launch_bounds__(SplitCfg::kThreads, 1)
 
   if (warp == 0) {
     // ---------------- TMA producer ----------------
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      for (uint64_t s = blockIdx.x; s < count; s += gridDim.x) {
-        uint64_t Y, X;
-        tile_at(order, m_g, s, Y, X);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (uint64_t s = blockIdx.x; s < count; s += gridDim.x) {
+      uint64_t Y, X;
+      tile_at(order, m_g, s, Y, X);
+      const bool drop = split_drop_top(scale, Y, X, lane, l_f, sqrt_l);  // whole warp
+      if (lane == 0) {
         for (int pass = 0; pass < 2; ++pass) {
-          const int n_sl = pass == 0 ? C::kSlices : 4;  // pass 1 reads digit slices 0..3 only
+          // pass 0 reads all digit slices; pass 1 slices 0..3 (full depth) or 0..2 (adaptive)
+          const int n_sl = pass == 0 ? C::kSlices : (drop ? 3 : 4);
           for (int kb = 0; kb < k_blocks; ++kb) {
             mbar_wait(empty_bar(stage), phase ^ 1);
             const uint32_t a = ring + stage * C::kStageBytes;
             for (int sl = 0; sl < n_sl; ++sl) {  // slice by slice, in the order the MMAs need them
-              if (dbg == 1) {
+              if (dbg == 1 || dbg == 3) {
                 mbar_arrive(full_bar(stage, sl));
                 continue;
               }
@@ -317,6 +338,7 @@ __global__ void __launch_bounds__(SplitCfg::kThreads, 1)
           }
         }
       }
+      __syncwarp();
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
@@ -325,25 +347,27 @@ __global__ void __launch_bounds__(SplitCfg::kThreads, 1)
     for (uint64_t s = blockIdx.x; s < count; s += gridDim.x) {
       uint64_t Y, X;
       tile_at(order, m_g, s, Y, X);
-      const int q_top = split_drop_top(scale, Y, X, lane, l_f, sqrt_l) ? 2 : 3;
+      const bool drop = split_drop_top(scale, Y, X, lane, l_f, sqrt_l);
       if (lane == 0) {
         for (int pass = 0; pass < 2; ++pass, ++use) {
           mbar_wait(tempty, (use & 1) ^ 1);  // the epilogue has drained the accumulators
           tc_fence_after();
-          const int s_lo = pass == 0 ? 4 : 0;  // 0-based diagonal i + j (d - 2)
           for (int kb = 0; kb < k_blocks; ++kb) {
             const uint32_t a = ring + stage * C::kStageBytes, b = a + C::kOpBytes;
-            // the pass's MMA schedule (kSched*), fully unrolled
+            // the pass's MMA schedule (sched_entry), fully unrolled
             const bool first_k = kb == 0;
-            if (dbg != 2) {
-              if (pass == 1)
-                issue_stage<0>(tmem, a, b, first_k, full_bar(stage, 0), phase);
-              else if (q_top == 3)
+            if (dbg != 2 && dbg != 4) {
+              if (pass == 0 && !drop)
                 issue_stage<1>(tmem, a, b, first_k, full_bar(stage, 0), phase);
+              else if (pass == 0)
+                issue_stage<3>(tmem, a, b, first_k, full_bar(stage, 0), phase);
+              else if (!drop)
+                issue_stage<0>(tmem, a, b, first_k, full_bar(stage, 0), phase);
               else
                 issue_stage<2>(tmem, a, b, first_k, full_bar(stage, 0), phase);
             } else {
-              for (int sl = 0; sl < (pass == 1 ? 4 : C::kSlices); ++sl) mbar_wait(full_bar(stage, sl), phase);
+              for (int sl = 0; sl < (pass == 1 ? (drop ? 3 : 4) : C::kSlices); ++sl)
+                mbar_wait(full_bar(stage, sl), phase);
             }
             umma_commit(empty_bar(stage));  // the slot is free once these MMAs have read it
             if (++stage == C::kStages) stage = 0, phase ^= 1;
@@ -365,23 +389,25 @@ __global__ void __launch_bounds__(SplitCfg::kThreads, 1)
     for (uint64_t s = blockIdx.x; s < count; s += gridDim.x) {
       uint64_t Y, X;
       tile_at(order, m_g, s, Y, X);
-      const int q_top = split_drop_top(scale, Y, X, lane, l_f, sqrt_l) ? 2 : 3;
+      // pass 1's top accumulator: diagonal 3 (full depth) or 2 (adaptive);
+      // pass 0 always fills all four (diagonals 4..7 or 3..6)
+      const int top1 = split_drop_top(scale, Y, X, lane, l_f, sqrt_l) ? 2 : 3;
       double t[64];
 #pragma unroll
       for (int pass = 0; pass < 2; ++pass, ++use) {
         mbar_wait(tfull, use & 1);
         tc_fence_after();
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < 4 && dbg < 3; ++c) {
 #pragma unroll
           for (int q = 3; q >= 0; --q) {
-            if (pass == 0 && q > q_top) continue;
+            if (pass == 1 && q > top1) continue;
             int32_t v[16];
             tmem_ld16(tmem + lane_base + 128u * q + (uint32_t)(64 * half + 16 * c), v);
             tmem_ld_wait();
 #pragma unroll
             for (int j = 0; j < 16; ++j)
-              t[16 * c + j] = (pass == 0 && q == q_top) ? (double)v[j] : fma(t[16 * c + j], 0.0078125, (double)v[j]);
+              t[16 * c + j] = (pass == 0 && q == 3) ? (double)v[j] : fma(t[16 * c + j], 0.0078125, (double)v[j]);
           }
         }
         tc_fence_before();
@@ -389,14 +415,46 @@ __global__ void __launch_bounds__(SplitCfg::kThreads, 1)
         if (lane == 0) mbar_arrive(tempty);
       }
       const uint64_t y = Y * kTile + 32 * quad + lane;
-      if (y < un) {
+      if (y < un && dbg < 3) {
         const double sy = scale[y];
         const uint64_t prb = (LAYOUT == kLayoutPacked) ? row_prefix(un, y) - y - ep.out_base : 0;
         const uint64_t x0 = X * kTile + 64 * half;
+        if (LAYOUT == kLayoutPacked) {
+          // the row's cells [max(x0, y), min(x0 + 64, n)) are contiguous in the
+          // packed triangle: 16-byte stores (two cells per request) on the
+          // aligned pairs, single cells at the ends
+          const uint64_t xa = x0 > y ? x0 : y, xb = x0 + 64 < un ? x0 + 64 : un;
+          if (xa < xb) {
+            const int ja = (int)(xa - x0), jb = (int)(xb - x0);
+            double *row = ep.out + prb + x0;
+            auto cell = [&](int j) { return t[j] * sy * __ldg(scale + x0 + j); };
+            auto one = [&](int j) {
+              if (j >= ja && j < jb) __stcs(row + j, cell(j));
+            };
+            auto pair = [&](int j) {
+              if (j >= ja && j + 1 < jb) {
+                __stcs(reinterpret_cast<double2 *>(row + j), make_double2(cell(j), cell(j + 1)));
+              } else {
+                one(j);
+                one(j + 1);
+              }
+            };
+            if (((prb + x0) & 1) == 0) {
 #pragma unroll
-        for (int j = 0; j < 64; ++j) {
-          const uint64_t x = x0 + j;
-          if (x >= y && x < un) store_cell<LAYOUT>(ep, y, x, prb, t[j] * sy * __ldg(scale + x));
+              for (int j = 0; j < 64; j += 2) pair(j);
+            } else {
+              one(0);
+#pragma unroll
+              for (int j = 1; j < 63; j += 2) pair(j);
+              one(63);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 64; ++j) {
+            const uint64_t x = x0 + j;
+            if (x >= y && x < un) store_cell<LAYOUT>(ep, y, x, prb, t[j] * sy * __ldg(scale + x));
+          }
         }
       }
     }
