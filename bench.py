@@ -584,6 +584,62 @@ def run_b200(args, rank: int, world: int, local_rank: int) -> None:
         "algorithmic_flops_per_launch": flops_launch,
     }
 
+    # ---- end to end through the public API (pinned X upload + packed download inside)
+    e2e_steps = args.e2e_steps if args.e2e_steps is not None else max(args.steps, 5)
+    host_out = torch.empty(total_pairs if world == 1 else max(1, span_hi - span_lo), dtype=torch.float64,
+                           pin_memory=True)
+    ds = pc.Dataset(values=x_pinned)
+    if world == 1:
+        def api_call():
+            return pc.allpairs(ds, out=host_out)
+    else:
+        # U exchange for the e2e leg: by default one broadcast K1 kernel writes
+        # each rank's rows into every rank's U over peer memory (CUDA IPC, NVLink
+        # between GPUs); PCC_EXCHANGE=collective uses K1 + NCCL all_gather
+        # instead (host-staged gloo when ranks share a GPU)
+        exchange = os.environ.get("PCC_EXCHANGE", "p2p")
+        if exchange == "collective" and ndev >= world:
+            exch_group = dist.new_group(backend="nccl")
+        else:
+            exch_group = dist.group.WORLD
+
+        def api_call():
+            return compute_worker(ds, world, rank, dev, out=host_out, group=exch_group, exchange=exchange)
+    api_call()  # warm-up
+    barrier()
+    wall = []
+    with ClockSampler(dev_index) as clocks_e2e:
+        for _ in range(e2e_steps):
+            torch.cuda.synchronize()
+            barrier()
+            a = time.perf_counter()
+            r = api_call()
+            wall.append(time.perf_counter() - a)
+    e2e_s = max_over_ranks(statistics.median(wall))
+    clock_e2e = clocks_e2e.summary()
+    if world == 1:
+        # sanity: the API result matches the device-timed shard bit for bit
+        assert np.array_equal(r.packed.numpy()[:1000], shard[:1000].cpu().numpy())
+    h2d = n * l * 8  # world == 1: all of X; N > 1: one row block of X per rank
+    d2h = total_pairs * 8
+
+    # ---- the reference's calling convention: plain numpy in, numpy result
+    # allocated by the call (pageable memory, staged through pinned slots)
+    e2e_pageable = None
+    if world == 1 and not args.no_pageable:
+        ds_np = pc.Dataset(values=x_host)
+        pc.allpairs(ds_np)  # warm-up
+        walls = []
+        for _ in range(3):
+            torch.cuda.synchronize()
+            a = time.perf_counter()
+            r_np = pc.allpairs(ds_np)
+            walls.append(time.perf_counter() - a)
+            del r_np
+        t_np = statistics.median(walls)
+        e2e_pageable = {"value": total_pairs / t_np, "unit": "pairs/s", "ms_per_step": t_np * 1e3, "steps": 3,
+                        "what": "allpairs(Dataset(numpy X)) returning a freshly allocated numpy result"}
+
     # ---- bit-exact mode (allpairs(exact=True)): K1 + the dot8 contraction on the
     # FP64 CUDA cores, same shard, device-timed like the step above
     exact_mode = None
@@ -693,80 +749,26 @@ def run_b200(args, rank: int, world: int, local_rank: int) -> None:
         }
         del shard_s
         torch.cuda.synchronize()
-
-    # ---- end to end through the public API (pinned X upload + packed download inside)
-    e2e_steps = args.e2e_steps if args.e2e_steps is not None else max(args.steps, 5)
-    host_out = torch.empty(total_pairs if world == 1 else max(1, span_hi - span_lo), dtype=torch.float64,
-                           pin_memory=True)
-    ds = pc.Dataset(values=x_pinned)
-    if world == 1:
-        def api_call():
-            return pc.allpairs(ds, out=host_out)
-    else:
-        # U exchange for the e2e leg: by default one broadcast K1 kernel writes
-        # each rank's rows into every rank's U over peer memory (CUDA IPC, NVLink
-        # between GPUs); PCC_EXCHANGE=collective uses K1 + NCCL all_gather
-        # instead (host-staged gloo when ranks share a GPU)
-        exchange = os.environ.get("PCC_EXCHANGE", "p2p")
-        if exchange == "collective" and ndev >= world:
-            exch_group = dist.new_group(backend="nccl")
-        else:
-            exch_group = dist.group.WORLD
-
-        def api_call():
-            return compute_worker(ds, world, rank, dev, out=host_out, group=exch_group, exchange=exchange)
-    api_call()  # warm-up
-    barrier()
-    wall = []
-    for _ in range(e2e_steps):
-        torch.cuda.synchronize()
-        barrier()
-        a = time.perf_counter()
-        r = api_call()
-        wall.append(time.perf_counter() - a)
-    e2e_s = max_over_ranks(statistics.median(wall))
-    if world == 1:
-        # sanity: the API result matches the device-timed shard bit for bit
-        assert np.array_equal(r.packed.numpy()[:1000], shard[:1000].cpu().numpy())
-    if split_mode is not None:
         # the same public call with method="split"
-        if world == 1:
-            def api_split():
-                return pc.allpairs(ds, out=host_out, method="split")
-        else:
-            def api_split():
-                return compute_worker(ds, world, rank, dev, out=host_out, group=exch_group, exchange=exchange,
-                                      method="split")
-        api_split()
-        wall_s = []
-        for _ in range(e2e_steps):
-            torch.cuda.synchronize()
-            barrier()
-            a = time.perf_counter()
+        if True:
+            if world == 1:
+                def api_split():
+                    return pc.allpairs(ds, out=host_out, method="split")
+            else:
+                def api_split():
+                    return compute_worker(ds, world, rank, dev, out=host_out, group=exch_group, exchange=exchange,
+                                          method="split")
             api_split()
-            wall_s.append(time.perf_counter() - a)
-        e2e_split = max_over_ranks(statistics.median(wall_s))
-        split_mode["e2e"] = {"value": total_pairs / e2e_split, "unit": "pairs/s", "ms_per_step": e2e_split * 1e3,
-                             "steps": e2e_steps, "h2d_bytes_per_step": n * l * 8, "d2h_bytes_per_step": total_pairs * 8}
-    h2d = n * l * 8  # world == 1: all of X; N > 1: one row block of X per rank
-    d2h = total_pairs * 8
-
-    # ---- the reference's calling convention: plain numpy in, numpy result
-    # allocated by the call (pageable memory, staged through pinned slots)
-    e2e_pageable = None
-    if world == 1 and not args.no_pageable:
-        ds_np = pc.Dataset(values=x_host)
-        pc.allpairs(ds_np)  # warm-up
-        walls = []
-        for _ in range(3):
-            torch.cuda.synchronize()
-            a = time.perf_counter()
-            r_np = pc.allpairs(ds_np)
-            walls.append(time.perf_counter() - a)
-            del r_np
-        t_np = statistics.median(walls)
-        e2e_pageable = {"value": total_pairs / t_np, "unit": "pairs/s", "ms_per_step": t_np * 1e3, "steps": 3,
-                        "what": "allpairs(Dataset(numpy X)) returning a freshly allocated numpy result"}
+            wall_s = []
+            for _ in range(e2e_steps):
+                torch.cuda.synchronize()
+                barrier()
+                a = time.perf_counter()
+                api_split()
+                wall_s.append(time.perf_counter() - a)
+            e2e_split = max_over_ranks(statistics.median(wall_s))
+            split_mode["e2e"] = {"value": total_pairs / e2e_split, "unit": "pairs/s", "ms_per_step": e2e_split * 1e3,
+                                 "steps": e2e_steps, "h2d_bytes_per_step": n * l * 8, "d2h_bytes_per_step": total_pairs * 8}
 
     # ---- CPU baseline (rank 0, N=1 only): the reference itself (paircorr from
     # baseline/_ref, stock allpairs path, all host threads) on a ~12 s tile
@@ -836,7 +838,10 @@ def run_b200(args, rank: int, world: int, local_rank: int) -> None:
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": {"value": total_pairs / e2e_s, "unit": "pairs/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3, "steps": e2e_steps},
+                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3, "steps": e2e_steps,
+                    "what": "allpairs(Dataset(pinned X), out=pinned host result): upload, K1, K2 and download "
+                            "streamed and overlapped (stream.py), wall clock per call, median",
+                    "clocks": clock_e2e},
             "gpu_launches": launches,
             "exact_mode": exact_mode,
             "split_mode": split_mode,
