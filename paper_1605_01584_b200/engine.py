@@ -20,6 +20,7 @@ PAPER.md:235-287) with the device array as the staging buffer.
 
 from __future__ import annotations
 
+import os
 from pathlib import Path
 
 import numpy as np
@@ -62,8 +63,6 @@ def _device_result_budget(device: torch.device, n: int, l: int, method: str = "t
     """Bytes the packed result may take on ``device``: free memory minus X, U
     (plus the split method's digit planes) and a margin
     (``PCC_DEVICE_RESULT_BUDGET`` overrides, for tests)."""
-    import os
-
     env = os.environ.get("PCC_DEVICE_RESULT_BUDGET")
     if env:
         return int(env)
@@ -150,7 +149,10 @@ def _allpairs_one_device(dataset: Dataset, device: torch.device, keep_on_device:
 
         total = sym_job_count(n)
         T = int(L.pcc_gpu_tile_count(n))
-        budget = _device_result_budget(device, n, l, method)
+        # cudaMemGetInfo costs ~0.2 ms: only results that could approach the
+        # device's capacity are checked against the free memory
+        check = total * 8 > (1 << 30) or "PCC_DEVICE_RESULT_BUDGET" in os.environ
+        budget = _device_result_budget(device, n, l, method) if check else total * 8
         if not keep_on_device and total * 8 > budget:
             # the packed result does not fit the device next to X and U: bounded
             # device windows, each pass downloaded into the host result
