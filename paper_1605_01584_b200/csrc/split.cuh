@@ -328,9 +328,13 @@ __global__ void __launch_bounds__(SplitCfg::kThreads, 1)
                 mbar_arrive(full_bar(stage, sl));
                 continue;
               }
-              mbar_arrive_expect_tx(full_bar(stage, sl), 2u * C::kSliceBytes);
-              tma_load_3d(a + sl * C::kSliceBytes, &map1, 0, (int32_t)(Y * kTile), kb * C::kSlices + sl,
-                          full_bar(stage, sl));
+              // dbg 5 (timing experiment, wrong results): every other A slice is
+              // not loaded -- the L2 traffic a 2-CTA multicast of A would save
+              const bool skip_a = dbg == 5 && (sl & 1);
+              mbar_arrive_expect_tx(full_bar(stage, sl), (skip_a ? 1u : 2u) * C::kSliceBytes);
+              if (!skip_a)
+                tma_load_3d(a + sl * C::kSliceBytes, &map1, 0, (int32_t)(Y * kTile), kb * C::kSlices + sl,
+                            full_bar(stage, sl));
               tma_load_3d(a + C::kOpBytes + sl * C::kSliceBytes, &map1, 0, (int32_t)(X * kTile),
                           kb * C::kSlices + sl, full_bar(stage, sl));
             }
