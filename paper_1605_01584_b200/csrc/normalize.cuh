@@ -187,8 +187,9 @@ normalize_rows_kernel(const double *__restrict__ x, int64_t ldx, double *__restr
 
 // Shared-memory-staged variant (default whenever a row fits): X is read from
 // HBM exactly once.
-//   1. the CTA streams its R rows into shared memory with 8-byte cp.async
-//      (any l / ldx alignment, many copies in flight per thread);
+//   1. the CTA stages its R rows into shared memory with one bulk copy per
+//      row (any l / ldx alignment: the 16-byte-aligned interior by TMA, an
+//      unaligned first / last element by plain loads);
 //   2. 8 threads per row run the reference's lane chains (sum + constancy,
 //      then ssd) out of shared memory and finish with the shuffle tree;
 //   3. all threads write u = (x - mean) / scale (or the zero row) back with
@@ -198,9 +199,6 @@ normalize_rows_kernel(const double *__restrict__ x, int64_t ldx, double *__restr
 // normalize_rows_kernel, bit for bit.
 constexpr int kNormSmemMaxRows = 8;  // rows per CTA (one 8-lane group each; 64 or 128 threads)
 
-__device__ __forceinline__ void cp_async_8(uint32_t dst, const void *src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src));
-}
 
 #ifdef PCC_K1_PHASES
 // tools/k1_phases.cu: per-phase clock totals of normalize_rows_smem_kernel
@@ -247,10 +245,11 @@ template <int kNormSmemThreads, int MODE = kNormLocal>
 __global__ void __launch_bounds__(kNormSmemThreads)
 normalize_rows_smem_kernel(const double *__restrict__ x, int64_t ldx, double *__restrict__ u, int64_t ldu,
                            uint8_t *__restrict__ zero_variance, int64_t l, int64_t row_lo, int64_t row_hi,
-                           int rows_per_cta, NormDests dests) {
-  extern __shared__ __align__(16) double srow[];  // [rows_per_cta][l]
+                           int rows_per_cta, int64_t lds, NormDests dests) {
+  extern __shared__ __align__(16) double srow[];  // [rows_per_cta][lds]
   __shared__ double s_mean[kNormSmemMaxRows], s_scale[kNormSmemMaxRows];
   __shared__ int s_zero[kNormSmemMaxRows];
+  __shared__ int64_t s_base[kNormSmemMaxRows];  // row r's element 0 is srow[s_base[r]]
   const int tid = threadIdx.x;
   const int64_t r0 = row_lo + (int64_t)blockIdx.x * rows_per_cta;
   const int rows = (int)((row_hi - r0) < (int64_t)rows_per_cta ? (row_hi - r0) : (int64_t)rows_per_cta);
@@ -259,41 +258,37 @@ normalize_rows_smem_kernel(const double *__restrict__ x, int64_t ldx, double *__
   long long k1_t_ = clock64();
 #endif
 
-  // 1. stage the rows: one 1-D bulk copy per row (cp.async.bulk, thread 0,
-  //    byte-counted mbarrier) when every row start is 16-byte aligned and l
-  //    is even; else 16-byte (or 8-byte) cp.async pieces by all threads
+  // 1. stage the rows: per row one 1-D bulk copy (cp.async.bulk, byte-counted
+  //    mbarrier) of its 16-byte-aligned interior, issued by its own thread
+  //    (bulk copies issued by one thread complete one after another,
+  //    tools/bulk_bw.cu), plus plain loads of an unaligned first and last
+  //    element -- any l and ldx, and nothing outside the rows is read.  The
+  //    smem row starts 8 bytes into its slot when the row's first element is
+  //    misaligned, so the interior lands 16-byte aligned (slot stride lds).
   __shared__ __align__(8) uint64_t s_bar;
-  const bool bulk = (((reinterpret_cast<uintptr_t>(x) | (uintptr_t)(ldx * 8)) & 15) == 0) && (l % 2 == 0);
-  if (bulk) {
-    // one issuing thread per row: bulk copies issued by one thread complete
-    // one after another (tools/bulk_bw.cu), so the rows go out in parallel
-    const uint32_t bar = smem_u32(&s_bar);
-    if (tid == 0) {
-      mbar_init(bar, (uint32_t)rows);
-      mbar_fence_init();
-    }
-    __syncthreads();
-    if (tid < rows) {
-      mbar_arrive_expect_tx(bar, (uint32_t)(l * sizeof(double)));
-      bulk_copy_row(sbase + (uint32_t)(tid * l * sizeof(double)), x + (r0 + tid) * ldx, (uint32_t)(l * sizeof(double)),
+  const uint32_t bar = smem_u32(&s_bar);
+  if (tid == 0) {
+    mbar_init(bar, (uint32_t)rows);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (tid < rows) {
+    const double *xr = x + (r0 + tid) * ldx;
+    const int pre = (int)((reinterpret_cast<uintptr_t>(xr) >> 3) & 1);  // first element misaligned
+    const int64_t base = (int64_t)tid * lds + pre;
+    s_base[tid] = base;
+    const int64_t body = (l - pre) & ~(int64_t)1;  // aligned interior [pre, pre + body)
+    if (pre) srow[base] = xr[0];
+    if (pre + body < l) srow[base + l - 1] = xr[l - 1];
+    if (body > 0) {
+      mbar_arrive_expect_tx(bar, (uint32_t)(body * sizeof(double)));
+      bulk_copy_row(sbase + (uint32_t)((base + pre) * sizeof(double)), xr + pre, (uint32_t)(body * sizeof(double)),
                     bar);
-    }
-    if (tid == 0) mbar_wait(bar, 0);
-  }
-  for (int r = 0; r < rows && !bulk; ++r) {
-    const double *xr = x + (r0 + r) * ldx;
-    const uint32_t sr = sbase + (uint32_t)(r * l * sizeof(double));
-    if (((reinterpret_cast<uintptr_t>(xr) | sr) & 15) == 0) {
-      const int64_t pairs = l >> 1;
-      for (int64_t k = tid; k < pairs; k += kNormSmemThreads)
-        cp_async_16(sr + (uint32_t)(k * 2 * sizeof(double)), xr + 2 * k);
-      if ((l & 1) && tid == 0) cp_async_8(sr + (uint32_t)((l - 1) * sizeof(double)), xr + l - 1);
     } else {
-      for (int64_t k = tid; k < l; k += kNormSmemThreads) cp_async_8(sr + (uint32_t)(k * sizeof(double)), xr + k);
+      mbar_arrive(bar);
     }
   }
-  cp_async_commit();
-  cp_async_wait<0>();
+  if (tid == 0) mbar_wait(bar, 0);
   __syncthreads();
   K1_MARK(0);
 
@@ -311,7 +306,7 @@ normalize_rows_smem_kernel(const double *__restrict__ x, int64_t ldx, double *__
   if (MODE == kNormDigits && (tid >> 5) >= chain_warps) {
     const int fw = (tid >> 5) - chain_warps, nfw = kWarps - chain_warps;
     for (int r = 0; r < rows; ++r) {
-      const double *ds = srow + (int64_t)r * l;
+      const double *ds = srow + s_base[r];
       double lo = ds[0], hi = ds[0];
       for (int64_t k = fw * 32 + (tid & 31); k < l; k += nfw * 32) {
         lo = fmin(lo, ds[k]);
@@ -331,7 +326,7 @@ normalize_rows_smem_kernel(const double *__restrict__ x, int64_t ldx, double *__
   const int lane8 = tid & 7;
   const int row = tid >> 3;
   const bool active = row < rows;
-  const double *sr = srow + (int64_t)(active ? row : 0) * l;
+  const double *sr = srow + s_base[active ? row : 0];
   const int64_t nsteps = (l - lane8 + 7) >> 3;
   bool varies = false;
   double s = active ? lane_chain<false, 8>(sr + lane8, nsteps, sr[0], varies) : 0.0;
@@ -375,7 +370,7 @@ normalize_rows_smem_kernel(const double *__restrict__ x, int64_t ldx, double *__
     const int nfw = kWarps - chain_warps;
     if (nfw == 0) {  // every warp ran chains: min / max now, by all threads
       for (int r = 0; r < rows; ++r) {
-        const double *ds = srow + (int64_t)r * l;
+        const double *ds = srow + s_base[r];
         double lo = ds[0], hi = ds[0];
         for (int64_t k = tid; k < l; k += kNormSmemThreads) {
           lo = fmin(lo, ds[k]);
@@ -395,7 +390,7 @@ normalize_rows_smem_kernel(const double *__restrict__ x, int64_t ldx, double *__
     }
     const int w0 = nfw == 0 ? 0 : chain_warps, w1 = kWarps;
     for (int r = 0; r < rows; ++r) {
-      const double *ds = srow + (int64_t)r * l;
+      const double *ds = srow + s_base[r];
       const bool zero = s_zero[r] != 0;
       const double m0 = s_mean[r], sc = s_scale[r];
       double lo = s_min[w0][r], hi = s_max[w0][r];
@@ -416,8 +411,17 @@ normalize_rows_smem_kernel(const double *__restrict__ x, int64_t ldx, double *__
       for (int64_t k = 4 * (int64_t)tid; k < kpad; k += 4 * kNormSmemThreads) {
         uint32_t packed[7] = {};
         if (m > 0.0) {
+          double v4[4];
+          if (k + 3 < l && (s_base[r] & 1) == 0) {  // 16-byte aligned: two LDS.128
+            const double2 a = *reinterpret_cast<const double2 *>(ds + k);
+            const double2 b = *reinterpret_cast<const double2 *>(ds + k + 2);
+            v4[0] = a.x, v4[1] = a.y, v4[2] = b.x, v4[3] = b.y;
+          } else {
 #pragma unroll
-          for (int j = 0; j < 4; ++j) split_digits7((k + j < l) ? div_rn(__dsub_rn(ds[k + j], m0), dv) * pw : 0.0, j, packed);
+            for (int j = 0; j < 4; ++j) v4[j] = (k + j < l) ? ds[k + j] : 0.0;
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) split_digits7((k + j < l) ? div_rn(__dsub_rn(v4[j], m0), dv) * pw : 0.0, j, packed);
         }
         int8_t *dst = dests.slices + (k / W) * 7 * plane + (r0 + r) * W + (k % W);
 #pragma unroll
@@ -438,7 +442,7 @@ normalize_rows_smem_kernel(const double *__restrict__ x, int64_t ldx, double *__
         u[off + k] = v;
       }
     };
-    const double *ds = srow + (int64_t)r * l;
+    const double *ds = srow + s_base[r];
     if (s_zero[r]) {
       for (int64_t k = tid; k < ldu; k += kNormSmemThreads) put(k, 0.0);
     } else {

@@ -415,7 +415,11 @@ template <int MODE>
 int launch_normalize_staged(const double *x, int64_t ldx, double *u, int64_t ldu, uint8_t *zero_variance, int64_t l,
                             int64_t row_lo, int64_t row_hi, const pcc::NormDests &dests, cudaStream_t stream) {
   const uint64_t rows = (uint64_t)(row_hi - row_lo);
-  const int64_t row_bytes = l * (int64_t)sizeof(double);
+  // shared-memory row stride: l when every row starts 16-byte aligned and l
+  // is even, else room for the 8-byte shift of a misaligned row
+  const bool aligned_rows = (((reinterpret_cast<uintptr_t>(x) | (uintptr_t)(ldx * 8)) & 15) == 0) && (l % 2 == 0);
+  const int64_t lds = aligned_rows ? l : ((l + 3) & ~(int64_t)1);
+  const int64_t row_bytes = lds * (int64_t)sizeof(double);
   constexpr int64_t kSmPerSmem = kNormSmemPerSm;
   const DeviceConfig *dc = nullptr;
   const int cfg_rc = device_config(&dc);  // smem opt-in + register count of this device
@@ -462,13 +466,13 @@ int launch_normalize_staged(const double *x, int64_t ldx, double *u, int64_t ldu
   if (grid > 0x7FFFFFFFull) return fail(PCC_EINVAL, "too many rows");
   if (threads == 256)
     pcc::normalize_rows_smem_kernel<256, MODE><<<(unsigned)grid, 256, smem, stream>>>(
-        x, ldx, u, ldu, zero_variance, l, row_lo, row_hi, per_cta, dests);
+        x, ldx, u, ldu, zero_variance, l, row_lo, row_hi, per_cta, lds, dests);
   else if (threads == 128)
     pcc::normalize_rows_smem_kernel<128, MODE><<<(unsigned)grid, 128, smem, stream>>>(
-        x, ldx, u, ldu, zero_variance, l, row_lo, row_hi, per_cta, dests);
+        x, ldx, u, ldu, zero_variance, l, row_lo, row_hi, per_cta, lds, dests);
   else
     pcc::normalize_rows_smem_kernel<64, MODE><<<(unsigned)grid, 64, smem, stream>>>(
-        x, ldx, u, ldu, zero_variance, l, row_lo, row_hi, per_cta, dests);
+        x, ldx, u, ldu, zero_variance, l, row_lo, row_hi, per_cta, lds, dests);
   PCC_CUDA(cudaGetLastError(), "normalize_rows_smem_kernel launch");
   return PCC_OK;
 }

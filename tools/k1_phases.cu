@@ -20,7 +20,7 @@ void run(const double *x, double *u, uint8_t *f, long n, long l, long ldu, int r
     cudaEvent_t a, b;
     cudaEventCreate(&a); cudaEventCreate(&b);
     cudaEventRecord(a);
-    pcc::normalize_rows_smem_kernel<T><<<grid, T, smem>>>(x, l, u, ldu, f, l, 0, n, rows_per_cta);
+    pcc::normalize_rows_smem_kernel<T><<<grid, T, smem>>>(x, l, u, ldu, f, l, 0, n, rows_per_cta, l, pcc::NormDests{});
     cudaEventRecord(b);
     cudaEventSynchronize(b);
     float ms; cudaEventElapsedTime(&ms, a, b);
