@@ -382,6 +382,39 @@ def test_normalize_long_rows_bit_exact(n, l):
     assert np.array_equal(zv.cpu().numpy().astype(bool), zv_ref)
 
 
+@pytest.mark.parametrize("l,ldx,offset", [(1531, 1531, 0), (1531, 1531, 1), (64, 65, 1), (64, 67, 0), (2, 3, 1),
+                                          (3, 3, 1), (77, 80, 1), (2048, 2049, 1)])
+def test_normalize_any_row_alignment_bit_exact(l, ldx, offset):
+    """K1 stages rows by bulk copies of their 16-byte-aligned interior plus
+    plain loads of an unaligned first / last element: rows of any length,
+    any row stride and an 8-byte-misaligned base pointer (a view one element
+    into a buffer), over sub-ranges of rows -- bit-exact to the reference,
+    flags included, and every U row outside the range untouched."""
+    rng = np.random.default_rng(l * 7 + ldx + offset)
+    n = 37
+    buf = rng.standard_normal(offset + n * ldx + 5)
+    x = np.lib.stride_tricks.as_strided(buf[offset:], shape=(n, l), strides=(8 * ldx, 8)).copy()
+    x[3] = -1.25  # a constant row
+    for i in range(n):  # the same values inside the strided buffer
+        buf[offset + i * ldx: offset + i * ldx + l] = x[i]
+    u_ref, zv_ref = oracle.normalize(x)
+    L = _lib.lib()
+    bd = torch.from_numpy(buf).cuda()
+    ldu = int(L.pcc_ldu(l))
+    s = torch.cuda.current_stream().cuda_stream
+    for lo, hi in ((0, n), (1, n - 1), (5, 6), (n - 1, n)):
+        u = torch.full((n, ldu), float("nan"), dtype=torch.float64, device="cuda")
+        zv = torch.full((n,), 7, dtype=torch.uint8, device="cuda")
+        _lib.check(L.pcc_normalize_rows_f64(bd.data_ptr() + 8 * offset, ldx, u.data_ptr(), ldu, zv.data_ptr(), l,
+                                            lo, hi, s))
+        torch.cuda.synchronize()
+        got = u.cpu().numpy()
+        assert np.array_equal(got[lo:hi, :l], u_ref[lo:hi]), (lo, hi)
+        assert np.all(got[lo:hi, l:] == 0.0)
+        assert np.isnan(got[:lo]).all() and np.isnan(got[hi:]).all()
+        assert np.array_equal(zv.cpu().numpy()[lo:hi].astype(bool), zv_ref[lo:hi])
+
+
 @pytest.mark.parametrize("name", ["c2", "c4", "c5"])
 def test_full_size_configs_sampled_rows_and_properties(name):
     """BASELINE configs at full size: U bit-exact; sampled packed rows (tile
