@@ -55,6 +55,7 @@ __all__ = [
     "row_slices",
     "exchange_rows",
     "exchange_normalize",
+    "clear_exchange_cache",
 ]
 
 BACKENDS = ("in_process", "subprocess", "cuda")
@@ -501,14 +502,60 @@ def exchange_rows(u: torch.Tensor, flags: torch.Tensor, S: int, rank: int, world
 EXCHANGES = ("p2p", "collective")
 
 
+# Exchange buffers and peer mappings of the last p2p exchange, reused while
+# the shape, rank layout and group stay the same (cudaMalloc of U and 2 (p-1)
+# cudaIpcOpenMemHandle calls per allpairs call would otherwise cost several
+# ms each time).  One entry; ``clear_exchange_cache()`` releases it.
+_P2P_CACHE: dict = {}
+
+
+def clear_exchange_cache() -> None:
+    """Release the cached p2p exchange buffers and peer mappings."""
+    for entry in _P2P_CACHE.values():
+        for pu, pf in entry["peers"].values():
+            pu.close()
+            pf.close()
+    _P2P_CACHE.clear()
+
+
+def _p2p_buffers(n: int, ldu: int, S: int, rank: int, world: int, device: torch.device, group):
+    import torch.distributed as dist
+
+    key = (n, ldu, S, rank, world, device.index, id(group))
+    entry = _P2P_CACHE.get(key)
+    if entry is not None:
+        return entry
+    clear_exchange_cache()
+    L = _lib.lib()
+    s = stream_handle()
+    ubuf = _lib.DeviceBuffer(world * S * ldu * 8)
+    fbuf = _lib.DeviceBuffer(world * S)
+    u = ubuf.tensor((world * S, ldu), "<f8")
+    flags = fbuf.tensor((world * S,), "|u1")
+    # rows past n are written by nobody: each rank zeroes its own buffer's once
+    _lib.check(L.pcc_zero_rows_f64(ptr(u), ldu, n, world * S, s), "pad rows")
+    flags[n:].zero_()
+    handles = [None] * world
+    dist.all_gather_object(handles, (ubuf.ipc_handle(), fbuf.ipc_handle()), group=group)
+    peers = {q: (_lib.DeviceBuffer(handle=hu), _lib.DeviceBuffer(handle=hf))
+             for q, (hu, hf) in enumerate(handles) if q != rank}
+    us = [ubuf.address if q == rank else peers[q][0].address for q in range(world)]
+    fs = [fbuf.address if q == rank else peers[q][1].address for q in range(world)]
+    entry = {"ubuf": ubuf, "fbuf": fbuf, "u": u, "flags": flags, "peers": peers, "us": us, "fs": fs}
+    _P2P_CACHE[key] = entry
+    return entry
+
+
 def _exchange_normalize_p2p(x_host, n: int, l: int, rank: int, world: int, device: torch.device, group):
     """K1 fused with the all-gather of U over peer memory: every rank maps
-    every other rank's U (CUDA IPC handles swapped over ``group``) and one
-    broadcast K1 kernel (``pcc_normalize_rows_bcast_f64``) stores each
-    normalised row of this rank's block into all ``p`` buffers -- over NVLink
-    when the ranks sit on different GPUs of one node.  Two ``group``
-    barriers bracket the writes (buffers mapped and pad rows zeroed before,
-    every rank's rows landed after); no kernel ever waits on another rank."""
+    every other rank's U (CUDA IPC handles swapped over ``group``, cached
+    across calls) and one broadcast K1 kernel (``pcc_normalize_rows_bcast_f64``)
+    stores each normalised row of this rank's block into all ``p`` buffers --
+    over NVLink when the ranks sit on different GPUs of one node.  Two
+    ``group`` barriers bracket the writes (every rank done with the previous
+    use of its U before, every rank's rows landed after); no kernel ever
+    waits on another rank.  The returned ``u`` is the cached buffer: the
+    next exchange of the same shape overwrites it."""
     import torch.distributed as dist
 
     L = _lib.lib()
@@ -517,38 +564,22 @@ def _exchange_normalize_p2p(x_host, n: int, l: int, rank: int, world: int, devic
     ldu = int(L.pcc_ldu(l))
     with torch.cuda.device(device):
         s = stream_handle()
-        ubuf = _lib.DeviceBuffer(world * S * ldu * 8)
-        fbuf = _lib.DeviceBuffer(world * S)
-        u = ubuf.tensor((world * S, ldu), "<f8")
-        flags = fbuf.tensor((world * S,), "|u1")
-        # rows past n are written by nobody: each rank zeroes its own buffer's
-        _lib.check(L.pcc_zero_rows_f64(ptr(u), ldu, n, world * S, s), "pad rows")
-        flags[n:].zero_()
-        mine = (ubuf.ipc_handle(), fbuf.ipc_handle())
-        handles = [None] * world
-        dist.all_gather_object(handles, mine, group=group)
-        peers = {}
-        for q, (hu, hf) in enumerate(handles):
-            if q != rank:
-                peers[q] = (_lib.DeviceBuffer(handle=hu), _lib.DeviceBuffer(handle=hf))
-        torch.cuda.current_stream().synchronize()
-        dist.barrier(group=group)  # every buffer mapped and zero-padded
+        e = _p2p_buffers(n, ldu, S, rank, world, device, group)
+        xd = None
         if r1 > r0:
             xh = x_host if isinstance(x_host, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x_host))
             xd = torch.empty((r1 - r0, l), dtype=torch.float64, device=device)
             xd.copy_(xh[r0:r1], non_blocking=xh.is_pinned())
-            us = [ubuf.address if q == rank else peers[q][0].address for q in range(world)]
-            fs = [fbuf.address if q == rank else peers[q][1].address for q in range(world)]
-            uarr = (ctypes.c_void_p * world)(*[a + 8 * r0 * ldu for a in us])
-            farr = (ctypes.c_void_p * world)(*[a + r0 for a in fs])
+        torch.cuda.current_stream().synchronize()
+        dist.barrier(group=group)  # every rank is done with the previous use of its U; buffers mapped
+        if r1 > r0:
+            uarr = (ctypes.c_void_p * world)(*[a + 8 * r0 * ldu for a in e["us"]])
+            farr = (ctypes.c_void_p * world)(*[a + r0 for a in e["fs"]])
             _lib.check(L.pcc_normalize_rows_bcast_f64(ptr(xd), l, uarr, farr, world, ldu, l, 0, r1 - r0, s),
                        f"rank {rank} normalize+broadcast")
         torch.cuda.current_stream().synchronize()
         dist.barrier(group=group)  # every rank's rows have landed everywhere
-        for pu, pf in peers.values():
-            pu.close()
-            pf.close()
-    return u, flags
+    return e["u"], e["flags"]
 
 
 def exchange_normalize(x_host, n: int, l: int, rank: int, world: int, device: torch.device, group=None,

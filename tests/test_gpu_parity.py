@@ -315,10 +315,15 @@ def _exchange_rank(rank, world, port, x, q, exchange="collective", method="tenso
         lo_t, hi_t = partition(mg * (mg + 1) // 2, world)[rank]
         lo, hi = shard_span(n, lo_t, hi_t)
         host = torch.full((max(1, hi - lo),), float("nan"), dtype=torch.float64).pin_memory()
-        sh = compute_worker(pc.Dataset(values=torch.from_numpy(x).pin_memory()), world, rank, 0, out=host,
-                            group=dist.group.WORLD, exchange=exchange, method=method)
-        q.put((rank, [(a, b, host[a - lo:b - lo].numpy().copy()) for a, b in owned_runs(n, lo_t, hi_t)],
-               sorted(sh.zero_variance)))
+        ds = pc.Dataset(values=torch.from_numpy(x).pin_memory())
+        sh = compute_worker(ds, world, rank, 0, out=host, group=dist.group.WORLD, exchange=exchange, method=method)
+        first = host.clone()
+        # a second call reuses the cached exchange buffers / peer mappings (p2p)
+        host.fill_(float("nan"))
+        sh = compute_worker(ds, world, rank, 0, out=host, group=dist.group.WORLD, exchange=exchange, method=method)
+        runs = owned_runs(n, lo_t, hi_t)
+        same = all(torch.equal(first[a - lo:b - lo], host[a - lo:b - lo]) for a, b in runs)
+        q.put((rank, [(a, b, host[a - lo:b - lo].numpy().copy()) for a, b in runs], sorted(sh.zero_variance), same))
     finally:
         dist.destroy_process_group()
 
@@ -351,7 +356,8 @@ def test_exchange_mode_workers_match_single(world, n, l, exchange, method):
         p_.join(timeout=120)
         assert p_.exitcode == 0
     packed = np.full(ref.size, np.nan)
-    for _, runs, zvs in got:
+    for _, runs, zvs, same in got:
+        assert same, "second exchange call differs from the first"
         assert zvs == sorted(np.flatnonzero(zv).tolist())
         for a, b, v in runs:
             packed[a:b] = v
