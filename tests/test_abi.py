@@ -90,7 +90,7 @@ def test_sass_is_sm100a_and_uses_dmma():
     assert "DMMA.8x8x4" in sass          # FP64 tensor pipe in the contraction
     assert "UTMALDG.2D" in sass          # TMA operand staging (production contraction)
     assert "SYNCS" in sass               # mbarrier ring
-    assert "LDGSTS" in sass              # cp.async staging (K1, exact mode)
+    assert "UBLKCP" in sass              # 1-D bulk-copy staging (K1, exact mode)
     assert "DMUL" in sass and "DADD" in sass  # exact mode / K1 chains (no FMA contraction)
     assert "UTCIMMA" in sass             # split mode: tcgen05.mma kind::i8 (int8 tensor cores, TMEM)
     assert "UTMALDG.3D" in sass          # split mode: per-slice TMA boxes of the digit planes
