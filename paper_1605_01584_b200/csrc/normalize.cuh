@@ -111,6 +111,60 @@ __device__ __forceinline__ double lane_sum(const double *p, int nsteps) {
   return s;
 }
 
+// One reference lane chain over a whole shared-memory row (stride 8),
+// straight-line in 64-step blocks with the loads two 8-step batches ahead of
+// the dependent adds (~14.7 cycles per step on B200 vs ~17 for the
+// software-pipelined loop above, tools/k1s2_probe.cu EXP 9):
+//   SSD = false: s += x (sum8 lane);  SSD = true: d = x - ref (the mean),
+//   s += RN(d * d) (ssd8 lane).  The constancy test is not on this chain.
+template <bool SSD, bool CONST = false>
+__device__ __forceinline__ void chain64(double &s, const double *p, double ref, bool &varies) {
+  double v[3][8];
+#pragma unroll
+  for (int b = 0; b < 2; ++b)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[b][i] = p[8 * (8 * b + i)];
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    if (b + 2 < 8) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[(b + 2) % 3][i] = p[8 * (8 * (b + 2) + i)];
+    }
+    const double *cur = v[b % 3];
+    if (SSD) {
+      double d[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) d[i] = __dsub_rn(cur[i], ref);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) s = __dadd_rn(s, __dmul_rn(d[i], d[i]));
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        s = __dadd_rn(s, cur[i]);
+        if (CONST) varies |= cur[i] != ref;
+      }
+    }
+  }
+}
+// CONST (sum chain only): also the exact constancy test x != ref (= x[0]).
+template <bool SSD, bool CONST = false>
+__device__ __forceinline__ double row_chain(const double *p, int nsteps, double ref, bool &varies) {
+  double s = 0.0;
+  int t = 0;
+  for (; t + 64 <= nsteps; t += 64) chain64<SSD, CONST>(s, p + 8 * t, ref, varies);
+  for (; t < nsteps; ++t) {
+    const double v = p[8 * t];
+    if (SSD) {
+      const double d = __dsub_rn(v, ref);
+      s = __dadd_rn(s, __dmul_rn(d, d));
+    } else {
+      s = __dadd_rn(s, v);
+      if (CONST) varies |= v != ref;
+    }
+  }
+  return s;
+}
+
 // u = a / b bit-identical to IEEE division (__ddiv_rn), one FMA correction
 // instead of a full division per element: with y = RN(1/b) (one __drcp_rn
 // per row) and q0 = RN(a y), q = RN(q0 + (a - b q0) y) is the correctly rounded
@@ -293,22 +347,23 @@ normalize_rows_smem_kernel(const double *__restrict__ x, int64_t ldx, double *__
   K1_MARK(0);
 
   // 2. the 8 lanes of each row run the reference's chains back to back out
-  //    of shared memory: sum8 with the exact constancy test folded in
-  //    (every element vs the first; OR of the 8 lanes), the mean, then ssd8
-  //    with the centring d = x - mean inline (the subtract and square are off
-  //    the dependent add chain).  No CTA barrier between the phases.
-  // Digit planes need max |x - mean| per row = max(RN(xmax - mean), RN(mean -
-  // xmin)) (RN is monotone and odd), so the row's min and max -- order-free --
-  // are taken by the warps that run no lane chains, while the chains run.
+  //    of shared memory: sum8, the mean, then ssd8 with the centring d = x -
+  //    mean inline (the subtract and square are off the dependent add chain).
+  //    The reference's exact constancy test (every x == x[0],
+  //    _kernels.py:209-223) is row min == row max, and the row's min and max
+  //    -- order-free -- are taken by the warps that run no lane chains while
+  //    the chains run (after them, by every thread, when every warp runs
+  //    chains).  Digit planes need them too: max |x - mean| = max(RN(xmax -
+  //    mean), RN(mean - xmin)) (RN is monotone and odd).
   constexpr int kWarps = kNormSmemThreads / 32;
   __shared__ double s_min[kWarps][kNormSmemMaxRows], s_max[kWarps][kNormSmemMaxRows];
   const int chain_warps = (rows * 8 + 31) / 32;
-  if (MODE == kNormDigits && (tid >> 5) >= chain_warps) {
-    const int fw = (tid >> 5) - chain_warps, nfw = kWarps - chain_warps;
+  const int nfw = kWarps - chain_warps;
+  auto row_minmax = [&](int w, int nw) {  // this warp is w of nw warps sharing the rows
     for (int r = 0; r < rows; ++r) {
       const double *ds = srow + s_base[r];
       double lo = ds[0], hi = ds[0];
-      for (int64_t k = fw * 32 + (tid & 31); k < l; k += nfw * 32) {
+      for (int64_t k = w * 32 + (tid & 31); k < l; k += nw * 32) {
         lo = fmin(lo, ds[k]);
         hi = fmax(hi, ds[k]);
       }
@@ -322,40 +377,69 @@ normalize_rows_smem_kernel(const double *__restrict__ x, int64_t ldx, double *__
         s_max[tid >> 5][r] = hi;
       }
     }
-  }
+  };
+  // U modes: the constancy test rides on the sum chain (x != x[0]); digit
+  // planes: it is row min == row max, the min / max the digits need anyway,
+  // taken by the warps that run no chains while the chains run
+  constexpr bool kMinMax = MODE == kNormDigits;
+  if (kMinMax && (tid >> 5) >= chain_warps) row_minmax((tid >> 5) - chain_warps, nfw);
   const int lane8 = tid & 7;
   const int row = tid >> 3;
   const bool active = row < rows;
-  const double *sr = srow + s_base[active ? row : 0];
-  const int64_t nsteps = (l - lane8 + 7) >> 3;
-  bool varies = false;
-  double s = active ? lane_chain<false, 8>(sr + lane8, nsteps, sr[0], varies) : 0.0;
-  s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 1));
-  s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 2));
-  s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 4));
-  const unsigned vb = __ballot_sync(0xffffffffu, varies);
-  const bool constant = (vb & (0xffu << (tid & 24))) == 0u;
-  double q = 0.0, mean = 0.0;
-  if (active && !constant) {  // uniform within the 8-lane group
-    mean = __ddiv_rn(s, (double)l);
-    bool unused = false;
-    q = lane_chain<true, 8>(sr + lane8, nsteps, mean, unused);
-  }
-  q = __dadd_rn(q, __shfl_xor_sync(0xffffffffu, q, 1));
-  q = __dadd_rn(q, __shfl_xor_sync(0xffffffffu, q, 2));
-  q = __dadd_rn(q, __shfl_xor_sync(0xffffffffu, q, 4));
-  if (active && lane8 == 0) {
-    const bool zero = constant || q == 0.0;
-    s_zero[row] = zero;
-    s_mean[row] = mean;
-    s_scale[row] = zero ? 0.0 : __dsqrt_rn(q);
-    if (MODE == kNormBcast) {
-      for (int d = 0; d < dests.n; ++d) dests.flags[d][r0 + row] = zero ? 1 : 0;
-    } else {
-      zero_variance[r0 + row] = zero ? 1 : 0;
+  if ((tid >> 5) < chain_warps) {
+    const double *sr = srow + s_base[active ? row : 0];
+    const int nsteps = (int)((l - lane8 + 7) >> 3);
+    bool varies = false;
+    double s = active ? row_chain<false, !kMinMax>(sr + lane8, nsteps, sr[0], varies) : 0.0;
+    s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 1));
+    s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 2));
+    s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 4));
+    const unsigned vb = __ballot_sync(0xffffffffu, varies);
+    const bool constant = !kMinMax && (vb & (0xffu << (tid & 24))) == 0u;  // uniform within the 8-lane group
+    const double mean = constant ? 0.0 : __ddiv_rn(s, (double)l);
+    double q = (active && !constant) ? row_chain<true>(sr + lane8, nsteps, mean, varies) : 0.0;
+    q = __dadd_rn(q, __shfl_xor_sync(0xffffffffu, q, 1));
+    q = __dadd_rn(q, __shfl_xor_sync(0xffffffffu, q, 2));
+    q = __dadd_rn(q, __shfl_xor_sync(0xffffffffu, q, 4));
+    if (active && lane8 == 0) {
+      s_mean[row] = mean;
+      s_scale[row] = q;  // ssd for now (digit planes: the zero rule needs the min / max)
+      s_zero[row] = constant || q == 0.0;
+      if (!kMinMax) {
+        const bool zero = constant || q == 0.0;
+        s_scale[row] = zero ? 0.0 : __dsqrt_rn(q);
+        if (MODE == kNormBcast) {
+          for (int d = 0; d < dests.n; ++d) dests.flags[d][r0 + row] = zero ? 1 : 0;
+        } else {
+          zero_variance[r0 + row] = zero ? 1 : 0;
+        }
+      }
     }
   }
   __syncthreads();
+  if (kMinMax) {
+    if (nfw == 0) {  // every warp ran chains: min / max now, by all threads
+      row_minmax(tid >> 5, kWarps);
+      __syncthreads();
+    }
+    const int w0 = nfw == 0 ? 0 : chain_warps;
+    if (tid < rows) {
+      const int r = tid;
+      double lo = s_min[w0][r], hi = s_max[w0][r];
+      for (int w = w0 + 1; w < kWarps; ++w) {
+        lo = fmin(lo, s_min[w][r]);
+        hi = fmax(hi, s_max[w][r]);
+      }
+      s_min[0][r] = lo;  // the row's min / max (digit planes)
+      s_max[0][r] = hi;
+      const double q = s_scale[r];
+      const bool zero = lo == hi || q == 0.0;  // constant (x == x[0] everywhere), or zero ssd
+      s_zero[r] = zero;
+      s_scale[r] = zero ? 0.0 : __dsqrt_rn(q);
+      zero_variance[r0 + r] = zero ? 1 : 0;
+    }
+    __syncthreads();
+  }
   K1_MARK(1);
 
   if (MODE == kNormDigits) {
@@ -367,37 +451,11 @@ normalize_rows_smem_kernel(const double *__restrict__ x, int64_t ldx, double *__
     constexpr int W = 64;  // SplitCfg::kRowBytes
     const int64_t kpad = (l + W - 1) / W * W;
     const int64_t plane = dests.rows_total * W;
-    const int nfw = kWarps - chain_warps;
-    if (nfw == 0) {  // every warp ran chains: min / max now, by all threads
-      for (int r = 0; r < rows; ++r) {
-        const double *ds = srow + s_base[r];
-        double lo = ds[0], hi = ds[0];
-        for (int64_t k = tid; k < l; k += kNormSmemThreads) {
-          lo = fmin(lo, ds[k]);
-          hi = fmax(hi, ds[k]);
-        }
-#pragma unroll
-        for (int o = 16; o; o >>= 1) {
-          lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-          hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-        }
-        if ((tid & 31) == 0) {
-          s_min[tid >> 5][r] = lo;
-          s_max[tid >> 5][r] = hi;
-        }
-      }
-      __syncthreads();
-    }
-    const int w0 = nfw == 0 ? 0 : chain_warps, w1 = kWarps;
     for (int r = 0; r < rows; ++r) {
       const double *ds = srow + s_base[r];
       const bool zero = s_zero[r] != 0;
       const double m0 = s_mean[r], sc = s_scale[r];
-      double lo = s_min[w0][r], hi = s_max[w0][r];
-      for (int w = w0 + 1; w < w1; ++w) {
-        lo = fmin(lo, s_min[w][r]);
-        hi = fmax(hi, s_max[w][r]);
-      }
+      const double lo = s_min[0][r], hi = s_max[0][r];
       const double dm = fmax(__dsub_rn(hi, m0), __dsub_rn(m0, lo));  // = max_k |RN(x_k - mean)|
       const double m = zero ? 0.0 : __ddiv_rn(dm, sc);
       int e = 0;
