@@ -338,6 +338,12 @@ __global__ void __launch_bounds__(SplitCfg::kThreads, 1)
               tma_load_3d(a + C::kOpBytes + sl * C::kSliceBytes, &map1, 0, (int32_t)(X * kTile),
                           kb * C::kSlices + sl, full_bar(stage, sl));
             }
+            // slices this pass does not load: their barriers still complete a
+            // phase, so every slice barrier of a stage stays in step with the
+            // stage's phase (a stage is reused by passes of 7 and of 3 / 4
+            // slices; a barrier left a phase behind would let a later wait on
+            // it return before its data lands)
+            for (int sl = n_sl; sl < C::kSlices; ++sl) mbar_arrive(full_bar(stage, sl));
             if (++stage == C::kStages) stage = 0, phase ^= 1;
           }
         }

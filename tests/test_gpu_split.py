@@ -271,6 +271,21 @@ def test_split_full_c2_vs_fp64_tensor_path():
     torch.cuda.empty_cache()
 
 
+@pytest.mark.parametrize("l", [96, 128, 192, 320])
+def test_split_many_tiles_per_cta_short_k_vs_oracle(l):
+    """More tiles than resident CTAs (each CTA walks 2-3 tiles) with 2-5 K
+    blocks: a ring stage is reused by passes that load different numbers of
+    digit slices, so every slice barrier must advance in step with its stage
+    (regression: the unused slices' barriers fell a phase behind)."""
+    r = np.random.default_rng(l)
+    n = 128 * 25 + 7  # 26 tile rows: 351 GPU tiles
+    x = r.standard_normal((n, l))
+    x[300:340, 3] += 300.0  # one tile row at full depth: both pass-1 slice counts
+    ref, _ = oracle.allpairs(x, t=4)
+    got = pc.allpairs(pc.Dataset(values=x), **SPLIT).packed
+    assert float(np.abs(got - ref).max()) <= TOL
+
+
 def test_split_mixed_depth_tiles_vs_oracle():
     """Adaptive depth decided per tile pair: spiky rows (max|u| near 1) in one
     GPU tile row force full depth (34 products) on every tile touching it,
