@@ -19,6 +19,7 @@ p.add_argument("--config", default="c1")
 p.add_argument("--reps", type=int, default=3)
 p.add_argument("--skip-dmma", action="store_true")
 p.add_argument("--sustain", type=int, default=0, help="also time N back-to-back split launches with clock sampling")
+p.add_argument("--hash", action="store_true", help="print the sha256 of the split result (A/B bit-identity checks)")
 a = p.parse_args()
 L = _lib.lib()
 x = torch.from_numpy(make_config(a.config)).cuda()
@@ -58,6 +59,9 @@ prod = _lib.split_products(scale, n, l, 0, tiles)
 print(f"{a.config}: products per tile {prod / tiles:.2f} (34 = full depth, 28 = adaptive depth everywhere)")
 print(f"{a.config}: n={n} l={l}  split_rows {t_split_rows:.3f} ms  split syrk {t_split:.3f} ms "
       f"({flops / t_split / 1e9:.1f} TFLOP/s-equivalent n^2 l/t)", flush=True)
+if a.hash:
+    import hashlib
+    print(f"  split result sha256 {hashlib.sha256(out_s.cpu().numpy().tobytes()).hexdigest()[:24]}", flush=True)
 if not a.skip_dmma:
     t_d = timed(lambda: _lib.check(L.pcc_syrk_f64(u.data_ptr(), n, l, ldu, 0, tiles, _lib.LAYOUT_PACKED,
                                                   out_d.data_ptr(), 0, 0, 0, 0, 0, s0), "syrk"))
