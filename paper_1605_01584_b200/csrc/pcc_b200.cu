@@ -49,7 +49,6 @@ struct DeviceConfig {
   int quad_ctas = 0;
   int exact_ctas = 0;
   int split_ctas = 0;
-  int split_mc_clusters = 0;  // resident 2-CTA clusters of the CTA-pair split kernel
   int norm_regs[3] = {0, 0, 0};  // registers of normalize_rows_smem_kernel<256, MODE>
 #ifdef PCC_TUNING_VARIANTS
   int variant_ctas[16] = {0};
@@ -180,42 +179,12 @@ int configure_split_one(int *ctas) {
   return PCC_OK;
 }
 
-// CTA-pair split kernel: shared-memory opt-in and how many 2-CTA clusters
-// can be resident at once (cluster placement is per GPC, so not always
-// sm_count / 2).
-template <int LAYOUT>
-int configure_split_mc_one(int *clusters) {
-  using C = pcc::SplitCfg;
-  PCC_CUDA(cudaFuncSetAttribute(pcc::syrk_split_mc_kernel<LAYOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                C::kSmemBytes),
-           "cudaFuncSetAttribute(split mc smem)");
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(2, 1, 1);
-  cfg.blockDim = dim3(C::kThreads, 1, 1);
-  cfg.dynamicSmemBytes = C::kSmemBytes;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  PCC_CUDA(cudaOccupancyMaxActiveClusters(clusters, pcc::syrk_split_mc_kernel<LAYOUT>, &cfg),
-           "cudaOccupancyMaxActiveClusters(split mc)");
-  return PCC_OK;
-}
-
-int configure_split(int *ctas, int *mc_clusters) {
+int configure_split(int *ctas) {
   int c0 = 0, c1 = 0, c2 = 0;
   int rc = configure_split_one<pcc::kLayoutPacked>(&c0);
   if (rc == PCC_OK) rc = configure_split_one<pcc::kLayoutDense>(&c1);
   if (rc == PCC_OK) rc = configure_split_one<pcc::kLayoutTiles>(&c2);
   *ctas = c0 < c1 ? (c0 < c2 ? c0 : c2) : (c1 < c2 ? c1 : c2);
-  int m0 = 0, m1 = 0, m2 = 0;
-  if (rc == PCC_OK) rc = configure_split_mc_one<pcc::kLayoutPacked>(&m0);
-  if (rc == PCC_OK) rc = configure_split_mc_one<pcc::kLayoutDense>(&m1);
-  if (rc == PCC_OK) rc = configure_split_mc_one<pcc::kLayoutTiles>(&m2);
-  *mc_clusters = m0 < m1 ? (m0 < m2 ? m0 : m2) : (m1 < m2 ? m1 : m2);
   return rc;
 }
 
@@ -275,7 +244,7 @@ int device_config(const DeviceConfig **out, int device = -1) {
     if (rc == PCC_OK) rc = configure_tma_variant<V0, false>(&c.syrk_id_ctas);
     if (rc == PCC_OK) rc = configure_tma_variant<VQ>(&c.quad_ctas);
     if (rc == PCC_OK) rc = configure_exact(&c.exact_ctas);
-    if (rc == PCC_OK) rc = configure_split(&c.split_ctas, &c.split_mc_clusters);
+    if (rc == PCC_OK) rc = configure_split(&c.split_ctas);
     if (rc == PCC_OK) rc = configure_normalize<pcc::kNormLocal>(&c.norm_regs[pcc::kNormLocal]);
     if (rc == PCC_OK) rc = configure_normalize<pcc::kNormBcast>(&c.norm_regs[pcc::kNormBcast]);
     if (rc == PCC_OK) rc = configure_normalize<pcc::kNormDigits>(&c.norm_regs[pcc::kNormDigits]);
@@ -401,35 +370,6 @@ int launch_split(const int8_t *slices, const double *scale, int64_t n, int64_t l
   const unsigned grid = (unsigned)(tiles < resident ? tiles : resident);
   uint32_t group = 1;
   while ((uint64_t)(group + 1) * (group + 1) <= grid) ++group;
-  static const int mc_knob = [] {  // PCC_SPLIT_MC=0: the one-CTA kernel (A/B knob)
-    const char *e = getenv("PCC_SPLIT_MC");
-    return e ? atoi(e) : 1;
-  }();
-  if (mc_knob != 0 && split_dbg == 0 && dc->split_mc_clusters > 0 && tiles >= 2) {
-    // CTA pairs take consecutive schedule entries; an even group height keeps
-    // the pairs inside one column of the grouped order (shared B band)
-    const uint64_t pairs = (tiles + 1) / 2;
-    const uint64_t clusters = pairs < (uint64_t)dc->split_mc_clusters ? pairs : (uint64_t)dc->split_mc_clusters;
-    uint32_t g = 2;
-    while ((uint64_t)(g + 2) * (g + 2) <= 2 * clusters) g += 2;
-    const pcc::TileOrder mc_order = pcc::make_tile_order(m_g, tb, te, g);
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(2 * clusters), 1, 1);
-    cfg.blockDim = dim3(C::kThreads, 1, 1);
-    cfg.dynamicSmemBytes = C::kSmemBytes;
-    cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    PCC_CUDA(cudaLaunchKernelEx(&cfg, pcc::syrk_split_mc_kernel<LAYOUT>, map1, scale, n, l, (int)k_blocks, m_g,
-                                mc_order, ep),
-             "syrk_split_mc_kernel launch");
-    return PCC_OK;
-  }
   const pcc::TileOrder order = pcc::make_tile_order(m_g, tb, te, group);
   pcc::syrk_split_kernel<LAYOUT><<<grid, C::kThreads, C::kSmemBytes, stream>>>(map1, scale, n, l,
                                                                                (int)k_blocks, m_g, order, ep, split_dbg);

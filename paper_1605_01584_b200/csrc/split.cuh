@@ -269,55 +269,6 @@ __global__ void __launch_bounds__(256) split_rows_kernel(const double *__restric
   }
 }
 
-// One epilogue thread's row segment of a finished tile: cells (y, x) for x
-// in [X*128 + 64*half, +64), scaled by scale_y * scale_x, through the packed
-// / dense / reference-tile epilogues (only y <= x < n).
-template <int LAYOUT>
-__device__ __forceinline__ void split_store_row(const Epilogue &ep, const double *__restrict__ scale,
-                                                const double (&t)[64], uint64_t y, uint64_t X, int half,
-                                                uint64_t un) {
-  const double sy = scale[y];
-  const uint64_t prb = (LAYOUT == kLayoutPacked) ? row_prefix(un, y) - y - ep.out_base : 0;
-  const uint64_t x0 = X * kTile + 64 * half;
-  if (LAYOUT == kLayoutPacked) {
-    // the row's cells [max(x0, y), min(x0 + 64, n)) are contiguous in the
-    // packed triangle: 16-byte stores (two cells per request) on the
-    // aligned pairs, single cells at the ends
-    const uint64_t xa = x0 > y ? x0 : y, xb = x0 + 64 < un ? x0 + 64 : un;
-    if (xa < xb) {
-      const int ja = (int)(xa - x0), jb = (int)(xb - x0);
-      double *row = ep.out + prb + x0;
-      auto cell = [&](int j) { return t[j] * sy * __ldg(scale + x0 + j); };
-      auto one = [&](int j) {
-        if (j >= ja && j < jb) __stcs(row + j, cell(j));
-      };
-      auto pair = [&](int j) {
-        if (j >= ja && j + 1 < jb) {
-          __stcs(reinterpret_cast<double2 *>(row + j), make_double2(cell(j), cell(j + 1)));
-        } else {
-          one(j);
-          one(j + 1);
-        }
-      };
-      if (((prb + x0) & 1) == 0) {
-#pragma unroll
-        for (int j = 0; j < 64; j += 2) pair(j);
-      } else {
-        one(0);
-#pragma unroll
-        for (int j = 1; j < 63; j += 2) pair(j);
-        one(63);
-      }
-    }
-  } else {
-#pragma unroll
-    for (int j = 0; j < 64; ++j) {
-      const uint64_t x = x0 + j;
-      if (x >= y && x < un) store_cell<LAYOUT>(ep, y, x, prb, t[j] * sy * __ldg(scale + x));
-    }
-  }
-}
-
 // ---- the contraction ----------------------------------------------------
 template <int LAYOUT>
 __global__ void __launch_bounds__(SplitCfg::kThreads, 1)
@@ -365,21 +316,18 @@ __global__ void __launch_bounds__(SplitCfg::kThreads, 1)
       uint64_t Y, X;
       tile_at(order, m_g, s, Y, X);
       const bool drop = split_drop_top(scale, Y, X, lane, l_f, sqrt_l);  // whole warp
-      // lane sl issues digit slice sl of both operands: a thread's TMA
-      // copies complete one after another (tools/tma_issue_bw.cu), so the 14
-      // slice loads of a stage go out from 7 lanes instead of one
-      for (int pass = 0; pass < 2; ++pass) {
-        // pass 0 reads all digit slices; pass 1 slices 0..3 (full depth) or 0..2 (adaptive)
-        const int n_sl = pass == 0 ? C::kSlices : (drop ? 3 : 4);
-        for (int kb = 0; kb < k_blocks; ++kb) {
-          if (lane == 0) mbar_wait(empty_bar(stage), phase ^ 1);
-          __syncwarp();
-          const uint32_t a = ring + stage * C::kStageBytes;
-          const int sl = lane;
-          if (sl < n_sl) {
-            if (dbg == 1 || dbg == 3) {
-              mbar_arrive(full_bar(stage, sl));
-            } else {
+      if (lane == 0) {
+        for (int pass = 0; pass < 2; ++pass) {
+          // pass 0 reads all digit slices; pass 1 slices 0..3 (full depth) or 0..2 (adaptive)
+          const int n_sl = pass == 0 ? C::kSlices : (drop ? 3 : 4);
+          for (int kb = 0; kb < k_blocks; ++kb) {
+            mbar_wait(empty_bar(stage), phase ^ 1);
+            const uint32_t a = ring + stage * C::kStageBytes;
+            for (int sl = 0; sl < n_sl; ++sl) {  // slice by slice, in the order the MMAs need them
+              if (dbg == 1 || dbg == 3) {
+                mbar_arrive(full_bar(stage, sl));
+                continue;
+              }
               // dbg 5 (timing experiment, wrong results): every other A slice is
               // not loaded -- the L2 traffic a 2-CTA multicast of A would save
               const bool skip_a = dbg == 5 && (sl & 1);
@@ -390,15 +338,14 @@ __global__ void __launch_bounds__(SplitCfg::kThreads, 1)
               tma_load_3d(a + C::kOpBytes + sl * C::kSliceBytes, &map1, 0, (int32_t)(X * kTile),
                           kb * C::kSlices + sl, full_bar(stage, sl));
             }
-          } else if (sl < C::kSlices) {
             // slices this pass does not load: their barriers still complete a
             // phase, so every slice barrier of a stage stays in step with the
             // stage's phase (a stage is reused by passes of 7 and of 3 / 4
             // slices; a barrier left a phase behind would let a later wait on
             // it return before its data lands)
-            mbar_arrive(full_bar(stage, sl));
+            for (int sl = n_sl; sl < C::kSlices; ++sl) mbar_arrive(full_bar(stage, sl));
+            if (++stage == C::kStages) stage = 0, phase ^= 1;
           }
-          if (++stage == C::kStages) stage = 0, phase ^= 1;
         }
       }
       __syncwarp();
@@ -478,210 +425,53 @@ __global__ void __launch_bounds__(SplitCfg::kThreads, 1)
         if (lane == 0) mbar_arrive(tempty);
       }
       const uint64_t y = Y * kTile + 32 * quad + lane;
-      if (y < un && dbg < 3) split_store_row<LAYOUT>(ep, scale, t, y, X, half, un);
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem, C::kTmemCols);
-}
-
-
-// ---- the contraction, CTA-pair variant (B band multicast) ---------------
-// Two CTAs of a cluster take consecutive schedule entries 2p, 2p + 1; in the
-// grouped order those are mostly the tiles (Y, X) and (Y + 1, X) of one
-// column, which read the same B band (digit slices of the X rows).  Then each
-// CTA loads its own A slices and half of the B slices (even / odd), each B
-// slice multicast into both CTAs' rings -- a quarter less L2 -> SMEM traffic
-// (the split contraction's loads are L2-bandwidth-bound, DESIGN.md §3 K2s).
-// A pair that does not share X loads like the one-CTA kernel.  Every stage is
-// released by both CTAs' MMA commits (multicast arrivals, empty count 2),
-// since either CTA may write into the other's ring.  An odd last entry is
-// computed by both CTAs, the duplicate without stores.  The per-tile MMA
-// schedules, epilogue and adaptive-depth rule are those of syrk_split_kernel,
-// so every coefficient is bitwise the same.
-__device__ __forceinline__ uint32_t cluster_ctarank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-}
-__device__ __forceinline__ void tma_load_3d_mc(uint32_t dst, const CUtensorMap *map, int32_t c0, int32_t c1,
-                                               int32_t c2, uint32_t bar, uint16_t mask) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%2, "
-      "%3, %4}], [%5], %6;\n" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar), "h"(mask)
-      : "memory");
-}
-__device__ __forceinline__ void umma_commit_mc(uint32_t bar, uint16_t mask) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::
-                   "r"(bar),
-               "h"(mask)
-               : "memory");
-}
-
-template <int LAYOUT>
-__global__ void __launch_bounds__(SplitCfg::kThreads, 1)
-    syrk_split_mc_kernel(const __grid_constant__ CUtensorMap map1, const double *__restrict__ scale, int64_t n,
-                         int64_t l, int k_blocks, uint64_t m_g, TileOrder order, Epilogue ep) {
-  using C = SplitCfg;
-  extern __shared__ uint8_t smem_raw[];
-  const uint32_t raw = smem_u32(smem_raw);
-  const uint32_t ring = (raw + 1023u) & ~1023u;
-  const uint32_t bars = ring + C::kStages * C::kStageBytes;
-  auto full_bar = [&](int s, int sl) { return bars + 8u * (s * C::kSlices + sl); };
-  auto empty_bar = [&](int s) { return bars + 8u * (C::kStages * C::kSlices + s); };
-  const uint32_t tfull = bars + 8u * (C::kStages * C::kSlices + C::kStages);
-  const uint32_t tempty = tfull + 8u;
-  const uint32_t tmem_slot = tempty + 8u;
-  uint32_t *tmem_slot_ptr = reinterpret_cast<uint32_t *>(smem_raw + (tmem_slot - raw));
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_ctarank();
-  const uint64_t pair0 = blockIdx.x >> 1, pairs_step = gridDim.x >> 1;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < C::kStages; ++s) {
-      for (int sl = 0; sl < C::kSlices; ++sl) mbar_init(full_bar(s, sl), 1);
-      mbar_init(empty_bar(s), 2);  // both CTAs' MMA commits
-    }
-    mbar_init(tfull, 1);
-    mbar_init(tempty, C::kEpiWarps);
-    mbar_fence_init();
-    tma_prefetch_desc(&map1);
-  }
-  if (warp == 1) tmem_alloc(tmem_slot, C::kTmemCols);
-  tc_fence_before();
-  cluster_sync_all();  // the peer's barriers are initialised before any multicast
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot_ptr;
-  const uint64_t count = order.total;
-  const double l_f = (double)l, sqrt_l = sqrt((double)l);
-  // entry of CTA r in pair p (an odd last entry is duplicated)
-  auto entry = [&](uint64_t p, uint32_t r) { return 2 * p + r < count ? 2 * p + r : 2 * p; };
-
-  if (warp == 0) {
-    // ---------------- TMA producer ----------------
-    int stage = 0;
-    uint32_t phase = 0;
-    for (uint64_t p = pair0; 2 * p < count; p += pairs_step) {
-      uint64_t Y, X, Yo, Xo;
-      tile_at(order, m_g, entry(p, rank), Y, X);
-      tile_at(order, m_g, entry(p, rank ^ 1u), Yo, Xo);
-      const bool drop = split_drop_top(scale, Y, X, lane, l_f, sqrt_l);  // whole warp
-      const bool drop_o = split_drop_top(scale, Yo, Xo, lane, l_f, sqrt_l);
-      const bool share = X == Xo;
-      // lane sl issues digit slice sl (one lane per slice: a thread's TMA
-      // copies complete one after another, tools/tma_issue_bw.cu)
-      for (int pass = 0; pass < 2; ++pass) {
-        const int n_a = pass == 0 ? C::kSlices : (drop ? 3 : 4);  // slices this CTA's MMAs read
-        const int n_b = !share ? n_a : (pass == 0 ? C::kSlices : ((drop && drop_o) ? 3 : 4));
-        for (int kb = 0; kb < k_blocks; ++kb) {
-          if (lane == 0) mbar_wait(empty_bar(stage), phase ^ 1);  // both CTAs are done with this stage
-          __syncwarp();
-          const uint32_t a = ring + stage * C::kStageBytes;
-          const int sl = lane;
-          if (sl < C::kSlices) {
-            const uint32_t bytes =
-                (sl < n_a ? (uint32_t)C::kSliceBytes : 0u) + (sl < n_b ? (uint32_t)C::kSliceBytes : 0u);
-            if (bytes)
-              mbar_arrive_expect_tx(full_bar(stage, sl), bytes);
-            else
-              mbar_arrive(full_bar(stage, sl));  // keep the slice barrier in step with its stage
-            if (sl < n_a)
-              tma_load_3d(a + sl * C::kSliceBytes, &map1, 0, (int32_t)(Y * kTile), kb * C::kSlices + sl,
-                          full_bar(stage, sl));
-            if (sl < n_b) {
-              if (!share)
-                tma_load_3d(a + C::kOpBytes + sl * C::kSliceBytes, &map1, 0, (int32_t)(X * kTile),
-                            kb * C::kSlices + sl, full_bar(stage, sl));
-              else if ((uint32_t)(sl & 1) == rank)
-                tma_load_3d_mc(a + C::kOpBytes + sl * C::kSliceBytes, &map1, 0, (int32_t)(X * kTile),
-                               kb * C::kSlices + sl, full_bar(stage, sl), (uint16_t)3);
+      if (y < un && dbg < 3) {
+        const double sy = scale[y];
+        const uint64_t prb = (LAYOUT == kLayoutPacked) ? row_prefix(un, y) - y - ep.out_base : 0;
+        const uint64_t x0 = X * kTile + 64 * half;
+        if (LAYOUT == kLayoutPacked) {
+          // the row's cells [max(x0, y), min(x0 + 64, n)) are contiguous in the
+          // packed triangle: 16-byte stores (two cells per request) on the
+          // aligned pairs, single cells at the ends
+          const uint64_t xa = x0 > y ? x0 : y, xb = x0 + 64 < un ? x0 + 64 : un;
+          if (xa < xb) {
+            const int ja = (int)(xa - x0), jb = (int)(xb - x0);
+            double *row = ep.out + prb + x0;
+            auto cell = [&](int j) { return t[j] * sy * __ldg(scale + x0 + j); };
+            auto one = [&](int j) {
+              if (j >= ja && j < jb) __stcs(row + j, cell(j));
+            };
+            auto pair = [&](int j) {
+              if (j >= ja && j + 1 < jb) {
+                __stcs(reinterpret_cast<double2 *>(row + j), make_double2(cell(j), cell(j + 1)));
+              } else {
+                one(j);
+                one(j + 1);
+              }
+            };
+            if (((prb + x0) & 1) == 0) {
+#pragma unroll
+              for (int j = 0; j < 64; j += 2) pair(j);
+            } else {
+              one(0);
+#pragma unroll
+              for (int j = 1; j < 63; j += 2) pair(j);
+              one(63);
             }
           }
-          if (++stage == C::kStages) stage = 0, phase ^= 1;
-        }
-      }
-      __syncwarp();
-    }
-  } else if (warp == 1) {
-    // ---------------- MMA issuer ----------------
-    int stage = 0;
-    uint32_t phase = 0, use = 0;
-    for (uint64_t p = pair0; 2 * p < count; p += pairs_step) {
-      uint64_t Y, X;
-      tile_at(order, m_g, entry(p, rank), Y, X);
-      const bool drop = split_drop_top(scale, Y, X, lane, l_f, sqrt_l);
-      if (lane == 0) {
-        for (int pass = 0; pass < 2; ++pass, ++use) {
-          mbar_wait(tempty, (use & 1) ^ 1);
-          tc_fence_after();
-          for (int kb = 0; kb < k_blocks; ++kb) {
-            const uint32_t a = ring + stage * C::kStageBytes, b = a + C::kOpBytes;
-            const bool first_k = kb == 0;
-            if (pass == 0 && !drop)
-              issue_stage<1>(tmem, a, b, first_k, full_bar(stage, 0), phase);
-            else if (pass == 0)
-              issue_stage<3>(tmem, a, b, first_k, full_bar(stage, 0), phase);
-            else if (!drop)
-              issue_stage<0>(tmem, a, b, first_k, full_bar(stage, 0), phase);
-            else
-              issue_stage<2>(tmem, a, b, first_k, full_bar(stage, 0), phase);
-            umma_commit_mc(empty_bar(stage), (uint16_t)3);  // release the stage in both CTAs
-            if (++stage == C::kStages) stage = 0, phase ^= 1;
-          }
-          umma_commit(tfull);
-        }
-      } else {
-        use += 2;
-      }
-      __syncwarp();
-    }
-  } else {
-    // ---------------- epilogue ----------------
-    const int quad = warp & 3;
-    const int half = (warp - 2) >> 2;
-    const uint32_t lane_base = (uint32_t)(32 * quad) << 16;
-    const uint64_t un = (uint64_t)n;
-    uint32_t use = 0;
-    for (uint64_t p = pair0; 2 * p < count; p += pairs_step) {
-      const bool dup = 2 * p + rank >= count;  // duplicate of the partner's tile: no stores
-      uint64_t Y, X;
-      tile_at(order, m_g, entry(p, rank), Y, X);
-      const int top1 = split_drop_top(scale, Y, X, lane, l_f, sqrt_l) ? 2 : 3;
-      double t[64];
+        } else {
 #pragma unroll
-      for (int pass = 0; pass < 2; ++pass, ++use) {
-        mbar_wait(tfull, use & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-#pragma unroll
-          for (int q = 3; q >= 0; --q) {
-            if (pass == 1 && q > top1) continue;
-            int32_t v[16];
-            tmem_ld16(tmem + lane_base + 128u * q + (uint32_t)(64 * half + 16 * c), v);
-            tmem_ld_wait();
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-              t[16 * c + j] = (pass == 0 && q == 3) ? (double)v[j] : fma(t[16 * c + j], 0.0078125, (double)v[j]);
+          for (int j = 0; j < 64; ++j) {
+            const uint64_t x = x0 + j;
+            if (x >= y && x < un) store_cell<LAYOUT>(ep, y, x, prb, t[j] * sy * __ldg(scale + x));
           }
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(tempty);
       }
-      const uint64_t y = Y * kTile + 32 * quad + lane;
-      if (y < un && !dup) split_store_row<LAYOUT>(ep, scale, t, y, X, half, un);
     }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc(tmem, C::kTmemCols);
-  cluster_sync_all();  // no CTA leaves while its peer may still write into its ring or barriers
 }
 
 }  // namespace pcc
