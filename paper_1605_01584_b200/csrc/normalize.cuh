@@ -165,6 +165,24 @@ __device__ __forceinline__ double row_chain(const double *p, int nsteps, double 
   return s;
 }
 
+// The same lane chain continued from s over nsteps more elements (chunked
+// kernel: a row's chain runs across shared-memory chunks).
+template <bool SSD, bool CONST = false>
+__device__ __forceinline__ void row_chain_more(double &s, const double *p, int nsteps, double ref, bool &varies) {
+  int t = 0;
+  for (; t + 64 <= nsteps; t += 64) chain64<SSD, CONST>(s, p + 8 * t, ref, varies);
+  for (; t < nsteps; ++t) {
+    const double v = p[8 * t];
+    if (SSD) {
+      const double d = __dsub_rn(v, ref);
+      s = __dadd_rn(s, __dmul_rn(d, d));
+    } else {
+      s = __dadd_rn(s, v);
+      if (CONST) varies |= v != ref;
+    }
+  }
+}
+
 // u = a / b bit-identical to IEEE division (__ddiv_rn), one FMA correction
 // instead of a full division per element: with y = RN(1/b) (one __drcp_rn
 // per row) and q0 = RN(a y), q = RN(q0 + (a - b q0) y) is the correctly rounded
@@ -185,6 +203,19 @@ __device__ __forceinline__ double div_rn(double a, const RowDiv &d) {
     return __fma_rn(__fma_rn(-q0, d.b, a), d.y, q0);
   }
   return __ddiv_rn(a, d.b);
+}
+// The same quotient without the per-element branch (the branch and the
+// inlined IEEE fallback made the output loops ~2.5x slower, tools/
+// k1c_probe.cu): the guard is tested on the bits of a and collected in
+// `bad` -- +0 is exact here, -0 and |a| < 2^-520 (subnormals included) are
+// not -- and a caller whose `bad` is set anywhere writes its block again with
+// __ddiv_rn.  Rows whose scale fails the range test (!d.fast) take __ddiv_rn
+// throughout.
+__device__ __forceinline__ double div_fast(double a, const RowDiv &d, bool &bad) {
+  const double q0 = __dmul_rn(a, d.y);
+  const int hi = __double2hiint(a), lo = __double2loint(a);
+  bad |= ((hi & 0x7fffffff) < ((1023 - 520) << 20)) & ((hi | lo) != 0);
+  return __fma_rn(__fma_rn(-q0, d.b, a), d.y, q0);
 }
 
 constexpr int kNormThreads = 256;
@@ -466,25 +497,31 @@ normalize_rows_smem_kernel(const double *__restrict__ x, int64_t ldx, double *__
       if (tid == 0) dests.scale[r0 + r] = m > 0.0 ? ldexp(1.0, e - 7) : 0.0;
       const double pw = m > 0.0 ? ldexp(1.0, 7 - e) : 0.0;  // 7 - e <= 14 for unit-norm rows
       const RowDiv dv = row_div(sc);
-      for (int64_t k = 4 * (int64_t)tid; k < kpad; k += 4 * kNormSmemThreads) {
-        uint32_t packed[7] = {};
-        if (m > 0.0) {
-          double v4[4];
-          if (k + 3 < l && (s_base[r] & 1) == 0) {  // 16-byte aligned: two LDS.128
-            const double2 a = *reinterpret_cast<const double2 *>(ds + k);
-            const double2 b = *reinterpret_cast<const double2 *>(ds + k + 2);
-            v4[0] = a.x, v4[1] = a.y, v4[2] = b.x, v4[3] = b.y;
-          } else {
+      auto emit = [&](bool exact) {
+        bool bad = false;
+        auto dq = [&](double a) { return exact ? __ddiv_rn(a, dv.b) : div_fast(a, dv, bad); };
+        for (int64_t k = 4 * (int64_t)tid; k < kpad; k += 4 * kNormSmemThreads) {
+          uint32_t packed[7] = {};
+          if (m > 0.0) {
+            double v4[4];
+            if (k + 3 < l && (s_base[r] & 1) == 0) {  // 16-byte aligned: two LDS.128
+              const double2 a = *reinterpret_cast<const double2 *>(ds + k);
+              const double2 b = *reinterpret_cast<const double2 *>(ds + k + 2);
+              v4[0] = a.x, v4[1] = a.y, v4[2] = b.x, v4[3] = b.y;
+            } else {
 #pragma unroll
-            for (int j = 0; j < 4; ++j) v4[j] = (k + j < l) ? ds[k + j] : 0.0;
+              for (int j = 0; j < 4; ++j) v4[j] = (k + j < l) ? ds[k + j] : 0.0;
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) split_digits7((k + j < l) ? dq(__dsub_rn(v4[j], m0)) * pw : 0.0, j, packed);
           }
+          int8_t *dst = dests.slices + (k / W) * 7 * plane + (r0 + r) * W + (k % W);
 #pragma unroll
-          for (int j = 0; j < 4; ++j) split_digits7((k + j < l) ? div_rn(__dsub_rn(v4[j], m0), dv) * pw : 0.0, j, packed);
+          for (int i = 0; i < 7; ++i) *reinterpret_cast<uint32_t *>(dst + i * plane) = packed[i];
         }
-        int8_t *dst = dests.slices + (k / W) * 7 * plane + (r0 + r) * W + (k % W);
-#pragma unroll
-        for (int i = 0; i < 7; ++i) *reinterpret_cast<uint32_t *>(dst + i * plane) = packed[i];
-      }
+        return bad;
+      };
+      if (__syncthreads_or(emit(!dv.fast) ? 1 : 0)) emit(true);
     }
     return;
   }
@@ -507,22 +544,249 @@ normalize_rows_smem_kernel(const double *__restrict__ x, int64_t ldx, double *__
       const double m = s_mean[r];
       const RowDiv dv = row_div(s_scale[r]);
       // u = (x - mean) / scale; four independent divisions per iteration keep
-      // more of their latency in flight
+      // more of their latency in flight; the IEEE fallback (div_fast) rewrites
+      // the row in the rare case that any element needs it
       constexpr int64_t T = kNormSmemThreads;
-      int64_t k = tid;
-      for (; k + 3 * T < l; k += 4 * T) {
-        const double q0 = div_rn(__dsub_rn(ds[k], m), dv), q1 = div_rn(__dsub_rn(ds[k + T], m), dv);
-        const double q2 = div_rn(__dsub_rn(ds[k + 2 * T], m), dv), q3 = div_rn(__dsub_rn(ds[k + 3 * T], m), dv);
-        put(k, q0);
-        put(k + T, q1);
-        put(k + 2 * T, q2);
-        put(k + 3 * T, q3);
-      }
-      for (; k < l; k += T) put(k, div_rn(__dsub_rn(ds[k], m), dv));
-      for (k = l + tid; k < ldu; k += kNormSmemThreads) put(k, 0.0);
+      auto emit = [&](bool exact) {
+        bool bad = false;
+        auto dq = [&](double a) { return exact ? __ddiv_rn(a, dv.b) : div_fast(a, dv, bad); };
+        int64_t k = tid;
+        for (; k + 3 * T < l; k += 4 * T) {
+          const double q0 = dq(__dsub_rn(ds[k], m)), q1 = dq(__dsub_rn(ds[k + T], m));
+          const double q2 = dq(__dsub_rn(ds[k + 2 * T], m)), q3 = dq(__dsub_rn(ds[k + 3 * T], m));
+          put(k, q0);
+          put(k + T, q1);
+          put(k + 2 * T, q2);
+          put(k + 3 * T, q3);
+        }
+        for (; k < l; k += T) put(k, dq(__dsub_rn(ds[k], m)));
+        return bad;
+      };
+      if (__syncthreads_or(emit(!dv.fast) ? 1 : 0)) emit(true);
+      for (int64_t k = l + tid; k < ldu; k += kNormSmemThreads) put(k, 0.0);
     }
   }
   K1_MARK(2);
+}
+
+// Chunked K1 for long rows (host dispatch: rows 16-byte aligned, l even,
+// l >= kChunkMinL).  One row per 64-thread CTA, never resident: the row
+// streams through two shared-memory chunk buffers three times -- sum pass,
+// ssd pass, output pass -- one bulk copy per chunk, the next chunk landing
+// while the current one is consumed.  The staged kernel holds a whole row for
+// its ~2 l/8 dependent adds, so at l = 8192 only 3 rows fit an SM; here a row
+// occupies 2 chunks, and the rows in flight per SM are set by the host to
+// what L2 can hold between the passes (the second and third reads of a row
+// are L2 hits: DRAM traffic stays one read of X plus one write).  Lanes 0..7
+// of warp 0 ARE the reference's lanes (same chains, same tree, same IEEE
+// operations as normalize_rows_smem_kernel); warp 1 takes the row's min / max
+// in the digit-plane mode; both warps write the output.
+constexpr int kChunkThreads = 64;
+#ifdef PCC_K1C_PROBE
+// tools/k1c_probe.cu: clock64 totals (thread 0 of each CTA) -- [0..2] time in
+// passes 0 / 1 / 2 (sum, ssd, output), [3] time waiting for chunks
+__device__ unsigned long long g_k1c_probe[8];
+#endif
+template <int MODE>
+__global__ void __launch_bounds__(kChunkThreads)
+normalize_rows_chunked_kernel(const double *__restrict__ x, int64_t ldx, double *__restrict__ u, int64_t ldu,
+                              uint8_t *__restrict__ zero_variance, int64_t l, int64_t row_lo, int ch,
+                              NormDests dests) {
+  extern __shared__ __align__(16) double cbuf[];  // [2][ch]
+  __shared__ __align__(8) uint64_t s_bar[2];
+  __shared__ double s_mean, s_scale, s_pw, s_lo, s_hi;
+  __shared__ int s_zero;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int64_t row = row_lo + blockIdx.x;
+  const double *xr = x + row * ldx;
+  const int nc = (int)((l + ch - 1) / ch);
+  const int items = 3 * nc;  // (pass, chunk): sum, ssd, output
+  if (tid == 0) {
+    mbar_init(smem_u32(&s_bar[0]), 1);
+    mbar_init(smem_u32(&s_bar[1]), 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  auto issue = [&](int it) {  // chunk it % nc into buffer it & 1
+    const int64_t k0 = (int64_t)(it % nc) * ch;
+    const uint32_t bytes = (uint32_t)((l - k0 < ch ? l - k0 : ch) * sizeof(double));
+    const uint32_t bar = smem_u32(&s_bar[it & 1]);
+    mbar_arrive_expect_tx(bar, bytes);
+    bulk_copy_row(smem_u32(cbuf + (it & 1) * ch), xr + k0, bytes, bar);
+  };
+  // buffer b's chunks are issued by thread 32 b: a thread's bulk copies
+  // complete one after another (tools/tma_issue_bw.cu), so the two buffers'
+  // copies come from different threads
+  if (tid == 0) issue(0);
+  constexpr bool kMinMax = MODE == kNormDigits;  // constancy = (min == max) there
+  double s = 0.0, q = 0.0, ref = 0.0, mean = 0.0, lo = 0.0, hi = 0.0;
+  bool varies = false;
+  constexpr int W = 64;  // digit-plane K block = SplitCfg::kRowBytes
+  const int64_t kend = MODE == kNormDigits ? (l + W - 1) / W * W : ldu;  // outputs incl. padding
+  for (int it = 0; it < items; ++it) {
+#ifdef PCC_K1C_PROBE
+    const long long t_item = clock64();
+#endif
+    if (tid == 32 * ((it + 1) & 1) && it + 1 < items) issue(it + 1);  // its buffer was released by item it - 1
+    mbar_wait(smem_u32(&s_bar[it & 1]), (uint32_t)((it >> 1) & 1));
+#ifdef PCC_K1C_PROBE
+    if (tid == 0) atomicAdd(&g_k1c_probe[3], (unsigned long long)(clock64() - t_item));
+#endif
+    const int pass = it / nc, c = it % nc;
+    const int64_t k0 = (int64_t)c * ch;
+    const int cnt = (int)(l - k0 < ch ? l - k0 : ch);
+    const double *p = cbuf + (it & 1) * ch;
+    if (pass < 2 && tid < 8) {
+      // the reference's lane tid over this chunk (chunks are multiples of 8)
+      const int nsteps = (cnt - tid + 7) >> 3;
+      if (pass == 0) {
+        if (c == 0) ref = p[0];
+        row_chain_more<false, !kMinMax>(s, p + tid, nsteps, ref, varies);
+      } else {
+        row_chain_more<true>(q, p + tid, nsteps, mean, varies);
+      }
+      if (c == nc - 1) {
+        if (pass == 0) {  // tree ((s0+s1)+(s2+s3))+((s4+s5)+(s6+s7)), mean
+          s = __dadd_rn(s, __shfl_xor_sync(0xffu, s, 1));
+          s = __dadd_rn(s, __shfl_xor_sync(0xffu, s, 2));
+          s = __dadd_rn(s, __shfl_xor_sync(0xffu, s, 4));
+          const bool constant = !kMinMax && __ballot_sync(0xffu, varies) == 0u;
+          mean = __ddiv_rn(s, (double)l);
+          if (tid == 0) s_zero = constant ? 1 : 0;
+        } else {
+          q = __dadd_rn(q, __shfl_xor_sync(0xffu, q, 1));
+          q = __dadd_rn(q, __shfl_xor_sync(0xffu, q, 2));
+          q = __dadd_rn(q, __shfl_xor_sync(0xffu, q, 4));
+          if (tid == 0) {
+            const bool zero = (kMinMax ? s_lo == s_hi : s_zero != 0) || q == 0.0;
+            const double sc = zero ? 0.0 : __dsqrt_rn(q);
+            s_zero = zero ? 1 : 0;
+            s_mean = mean;
+            s_scale = sc;
+            if (MODE == kNormBcast) {
+              for (int d = 0; d < dests.n; ++d) dests.flags[d][row] = zero ? 1 : 0;
+            } else {
+              zero_variance[row] = zero ? 1 : 0;
+            }
+            if (MODE == kNormDigits) {
+              // exact max |u| = RN(max |x - mean| / scale) (RN is monotone and odd)
+              const double dm = fmax(__dsub_rn(s_hi, mean), __dsub_rn(mean, s_lo));
+              const double m = zero ? 0.0 : __ddiv_rn(dm, sc);
+              int e = 0;
+              if (m > 0.0) {
+                frexp(m, &e);
+                if (ldexp(m, 7 - e) >= 127.5) ++e;  // keep the leading digit within [-127, 127]
+              }
+              dests.scale[row] = m > 0.0 ? ldexp(1.0, e - 7) : 0.0;
+              s_pw = m > 0.0 ? ldexp(1.0, 7 - e) : 0.0;
+            }
+          }
+        }
+      }
+    } else if (pass == 0 && kMinMax && tid >= 32) {
+      // warp 1: the row's min / max (order-free), for the digits and the
+      // constancy test min == max
+      if (c == 0) lo = hi = p[0];
+      for (int k = lane; k < cnt; k += 32) {
+        lo = fmin(lo, p[k]);
+        hi = fmax(hi, p[k]);
+      }
+      if (c == nc - 1) {
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+          hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        }
+        if (lane == 0) {
+          s_lo = lo;
+          s_hi = hi;
+        }
+      }
+    } else if (pass == 2) {
+      // output of this chunk (+ the K padding after the last one)
+      const bool zero = s_zero != 0;
+      const double m0 = s_mean;
+      const RowDiv dv = row_div(zero ? 1.0 : s_scale);
+      const int64_t kb = k0 + (c == nc - 1 ? (kend - k0) : ch);  // this chunk's outputs: [k0, kb)
+      if (MODE == kNormDigits) {
+        const double pw = s_pw;
+        const int64_t plane = dests.rows_total * W;
+        auto emit = [&](bool exact) {
+          bool bad = false;
+          auto dq = [&](double a) { return exact ? __ddiv_rn(a, dv.b) : div_fast(a, dv, bad); };
+          for (int64_t k = k0 + 4 * tid; k < kb; k += 4 * kChunkThreads) {
+            uint32_t packed[7] = {0u, 0u, 0u, 0u, 0u, 0u, 0u};
+            if (pw > 0.0) {
+              double v4[4];
+              if (k + 3 < l) {
+                const double2 a = *reinterpret_cast<const double2 *>(p + (k - k0));
+                const double2 b = *reinterpret_cast<const double2 *>(p + (k - k0) + 2);
+                v4[0] = a.x, v4[1] = a.y, v4[2] = b.x, v4[3] = b.y;
+              } else {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) v4[j] = (k + j < l) ? p[k - k0 + j] : 0.0;
+              }
+#pragma unroll
+              for (int j = 0; j < 4; ++j)
+                split_digits7((k + j < l) ? __dmul_rn(dq(__dsub_rn(v4[j], m0)), pw) : 0.0, j, packed);
+            }
+            int8_t *dst = dests.slices + (k / W) * 7 * plane + row * W + (k % W);
+#pragma unroll
+            for (int i = 0; i < 7; ++i) *reinterpret_cast<uint32_t *>(dst + i * plane) = packed[i];
+          }
+          return bad;
+        };
+        if (__syncthreads_or(emit(!dv.fast) ? 1 : 0)) emit(true);
+      } else {
+        const int64_t off = row * ldu;
+        auto put = [&](int64_t k, double2 v) {
+          if (MODE == kNormBcast) {
+            for (int d = 0; d < dests.n; ++d) *reinterpret_cast<double2 *>(dests.u[d] + off + k) = v;
+          } else {
+            __stcs(reinterpret_cast<double2 *>(u + off + k), v);
+          }
+        };
+        auto emit = [&](bool exact) {
+          bool bad = false;
+          auto dq = [&](double a) { return exact ? __ddiv_rn(a, dv.b) : div_fast(a, dv, bad); };
+          int64_t k = k0 + 2 * tid;
+          if (!zero) {
+            // four independent pairs per thread in flight (the quotients are
+            // latency chains of 4 FP64 operations)
+            constexpr int S = 2 * kChunkThreads;
+            const int64_t kl = kb < l ? kb : l;
+            for (; k + 3 * S < kl; k += 4 * S) {
+              double2 xv[4], v[4];
+#pragma unroll
+              for (int i = 0; i < 4; ++i) xv[i] = *reinterpret_cast<const double2 *>(p + (k + i * S - k0));
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                v[i].x = dq(__dsub_rn(xv[i].x, m0));
+                v[i].y = dq(__dsub_rn(xv[i].y, m0));
+              }
+#pragma unroll
+              for (int i = 0; i < 4; ++i) put(k + i * S, v[i]);
+            }
+          }
+          for (; k < kb; k += 2 * kChunkThreads) {  // l, ldu even: pairs never straddle
+            double2 v = make_double2(0.0, 0.0);
+            if (!zero && k < l) {
+              const double2 xv = *reinterpret_cast<const double2 *>(p + (k - k0));
+              v.x = dq(__dsub_rn(xv.x, m0));
+              v.y = dq(__dsub_rn(xv.y, m0));
+            }
+            put(k, v);
+          }
+          return bad;
+        };
+        if (__syncthreads_or(emit(!dv.fast) ? 1 : 0)) emit(true);
+      }
+    }
+    __syncthreads();  // the buffer is free for item it + 2; s_* written above are visible
+#ifdef PCC_K1C_PROBE
+    if (tid == 0) atomicAdd(&g_k1c_probe[pass], (unsigned long long)(clock64() - t_item));
+#endif
+  }
 }
 
 }  // namespace pcc

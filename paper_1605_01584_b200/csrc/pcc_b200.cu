@@ -203,6 +203,9 @@ int configure_normalize(int *regs) {
   cudaFuncAttributes fa;
   PCC_CUDA(cudaFuncGetAttributes(&fa, pcc::normalize_rows_smem_kernel<256, MODE>), "cudaFuncGetAttributes(normalize)");
   *regs = fa.numRegs;
+  PCC_CUDA(cudaFuncSetAttribute(pcc::normalize_rows_chunked_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                kNormSmemPerSm),
+           "cudaFuncSetAttribute(normalize chunked smem)");
   return PCC_OK;
 }
 
@@ -411,6 +414,43 @@ int launch_syrk(const double *u, int64_t n, int64_t l, int64_t ldu, uint64_t tb,
 // Shared-memory-staged K1 launch (the default whenever a row fits), single
 // destination or broadcast to dests; kNotStaged if the row is too long.
 constexpr int kNotStaged = -1;
+// Chunked K1 (normalize_rows_chunked_kernel) for long rows: eligible when
+// every row starts 16-byte aligned and l is even (bulk copies), chosen from
+// kChunkMinL samples on (measured, DESIGN.md §3 K1).  Rows in flight per SM =
+// what ~60 MB of L2 holds (each row is read three times: HBM, then L2 twice),
+// set through the CTA's shared-memory footprint.  Knobs: PCC_K1_CHUNK = 0
+// (never) / 1 (whenever eligible); PCC_K1_CHUNK_CTAS = rows in flight per SM.
+constexpr int64_t kChunkMinL = 8192;
+template <int MODE>
+int launch_normalize_chunked(const double *x, int64_t ldx, double *u, int64_t ldu, uint8_t *zero_variance, int64_t l,
+                             int64_t row_lo, int64_t row_hi, const pcc::NormDests &dests, cudaStream_t stream,
+                             const DeviceConfig *dc) {
+  static const int knob = [] {
+    const char *e = getenv("PCC_K1_CHUNK");
+    return e ? atoi(e) : -1;
+  }();
+  static const int ctas_knob = [] {
+    const char *e = getenv("PCC_K1_CHUNK_CTAS");
+    return e ? atoi(e) : 0;
+  }();
+  const bool aligned_rows = (((reinterpret_cast<uintptr_t>(x) | (uintptr_t)(ldx * 8)) & 15) == 0) && (l % 2 == 0);
+  if (!aligned_rows || knob == 0 || (knob < 0 && l < kChunkMinL)) return kNotStaged;
+  if (MODE != pcc::kNormDigits && (ldu & 1)) return kNotStaged;
+  const uint64_t rows = (uint64_t)(row_hi - row_lo);
+  if (rows > 0x7FFFFFFFull) return fail(PCC_EINVAL, "too many rows");
+  int k = (int)(60.0e6 / ((double)dc->sm_count * (double)l * 8.0));
+  k = k < 3 ? 3 : (k > 16 ? 16 : k);
+  if (ctas_knob > 0) k = ctas_knob;
+  const int budget = kNormSmemPerSm / k - 1024;  // shared memory per CTA for k CTAs per SM
+  int ch = 2048;
+  while (ch > 256 && 2 * ch * (int)sizeof(double) > budget) ch /= 2;
+  const size_t smem = (size_t)(budget > 2 * ch * (int)sizeof(double) ? budget : 2 * ch * (int)sizeof(double));
+  pcc::normalize_rows_chunked_kernel<MODE><<<(unsigned)rows, pcc::kChunkThreads, smem, stream>>>(
+      x, ldx, u, ldu, zero_variance, l, row_lo, ch, dests);
+  PCC_CUDA(cudaGetLastError(), "normalize_rows_chunked_kernel launch");
+  return PCC_OK;
+}
+
 template <int MODE>
 int launch_normalize_staged(const double *x, int64_t ldx, double *u, int64_t ldu, uint8_t *zero_variance, int64_t l,
                             int64_t row_lo, int64_t row_hi, const pcc::NormDests &dests, cudaStream_t stream) {
@@ -424,6 +464,10 @@ int launch_normalize_staged(const double *x, int64_t ldx, double *u, int64_t ldu
   const DeviceConfig *dc = nullptr;
   const int cfg_rc = device_config(&dc);  // smem opt-in + register count of this device
   if (cfg_rc) return cfg_rc;
+  {
+    const int crc = launch_normalize_chunked<MODE>(x, ldx, u, ldu, zero_variance, l, row_lo, row_hi, dests, stream, dc);
+    if (crc != kNotStaged) return crc;
+  }
   // Shared-memory staging in natural order: as many CTAs per SM as rows allow
   // (4, 3, 2, then 1 CTA/SM), up to 8 rows per CTA.
   int per_cta = 0;
