@@ -375,9 +375,10 @@ def test_streamed_upload_from_pageable_and_device_inputs(rng):
 
 @pytest.mark.parametrize("n,l", [(3, 12_801), (2, 20_000), (1, 1_000_000), (40, 12_800), (33, 4_096)])
 def test_normalize_long_rows_bit_exact(n, l):
-    """Rows beyond the shared-memory budget take the three-pass global kernel;
-    both paths must equal the reference's normalize_rows bit for bit
-    (the reference tests a 10^6-sample row, test_transform.py:91-97)."""
+    """Rows beyond the shared-memory budget take the chunked kernel (even l,
+    aligned rows) or the three-pass global kernel (odd l); every path must
+    equal the reference's normalize_rows bit for bit (the reference tests a
+    10^6-sample row, test_transform.py:91-97)."""
     rng = np.random.default_rng(l)
     x = rng.random((n, l))
     if n > 1:
@@ -385,6 +386,27 @@ def test_normalize_long_rows_bit_exact(n, l):
     u, zv = _abi_normalize(x)
     u_ref, zv_ref = oracle.normalize(x)
     assert np.array_equal(u.cpu().numpy()[:n, :l], u_ref)
+    assert np.array_equal(zv.cpu().numpy().astype(bool), zv_ref)
+
+
+@pytest.mark.parametrize("l", [4096, 8192, 12_288])
+def test_normalize_signed_zero_quotients_bit_exact(l):
+    """Integer rows summing to exactly 0 (mean +0) with -0.0 entries: x - mean
+    = -0 there, which the one-FMA-correction quotient would turn into +0, so
+    those blocks must be written again with IEEE division -- staged (l = 4096)
+    and chunked (l >= 8192) kernels, bit for bit with the reference."""
+    rng = np.random.default_rng(l + 3)
+    n = 24
+    x = rng.integers(-9, 10, size=(n, l)).astype(np.float64)
+    x[:, 5] = -0.0
+    x[:, 77] = -0.0
+    x[:, -1] -= x.sum(axis=1)  # every row sums to 0 exactly
+    x[7] = -0.0  # a constant (all -0) row
+    u, zv = _abi_normalize(x)
+    u_ref, zv_ref = oracle.normalize(x)
+    got = u.cpu().numpy()[:n, :l]
+    assert np.array_equal(got.view(np.uint64), u_ref.view(np.uint64))  # signs of zeros included
+    assert np.signbit(got[0, 5])
     assert np.array_equal(zv.cpu().numpy().astype(bool), zv_ref)
 
 
