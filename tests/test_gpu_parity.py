@@ -373,7 +373,8 @@ def test_streamed_upload_from_pageable_and_device_inputs(rng):
         _assert_parity(res.packed, ref, frozenset(np.flatnonzero(zv).tolist()), 900)
 
 
-@pytest.mark.parametrize("n,l", [(3, 12_801), (2, 20_000), (1, 1_000_000), (40, 12_800), (33, 4_096)])
+@pytest.mark.parametrize("n,l", [(3, 12_801), (2, 20_000), (1, 1_000_000), (40, 12_800), (33, 4_096), (5, 8_194),
+                                 (3, 16_386)])
 def test_normalize_long_rows_bit_exact(n, l):
     """Rows beyond the shared-memory budget take the chunked kernel (even l,
     aligned rows) or the three-pass global kernel (odd l); every path must
@@ -814,13 +815,15 @@ def test_allpairs_property_vs_oracle(n, l, seed, dist):
     assert split.zero_variance == fast.zero_variance
 
 
-def test_normalize_broadcast_writes_every_destination(rng):
+@pytest.mark.parametrize("n,l", [(300, 77), (40, 8194)])
+def test_normalize_broadcast_writes_every_destination(rng, n, l):
     """pcc_normalize_rows_bcast_f64: one K1 launch stores each row into all
     destinations (the fused normalise + all-gather of the p2p exchange),
-    bit-identical to the single-destination K1."""
+    bit-identical to the single-destination K1 -- staged rows and chunked
+    rows (l >= 8192, a partial last chunk)."""
     import ctypes
 
-    x = torch.from_numpy(random_values(rng, 300, 77, special_rows=True)).cuda()
+    x = torch.from_numpy(random_values(rng, n, l, special_rows=True)).cuda()
     n, l = x.shape
     L = _lib.lib()
     ldu = int(L.pcc_ldu(l))
