@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <vector>
 
 #include "common.cuh"
@@ -287,10 +288,51 @@ void run_peak(const int8_t *src, int32_t *sink, int sms, int zero) {
   CK(cudaFree(cyc));
 }
 
-int main() {
+// Sustained rate: back-to-back launches of the M128 N256 random-operand
+// kernel for `seconds`; the median over the launches after the first second
+// (the power-capped steady state the split contraction runs in, bench.py).
+void run_sustained(const int8_t *src, int32_t *sink, int sms, double seconds) {
+  constexpr int N = 256;
+  const size_t smem = 1024 + 7 * (128 + N) * 32;
+  CK(cudaFuncSetAttribute(peak_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int iters = 20000;
+  long long *cyc;
+  CK(cudaMalloc(&cyc, sms * sizeof(long long)));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0), cudaEventCreate(&e1);
+  std::vector<double> tops, mhz;
+  double elapsed = 0.0;
+  while (elapsed < seconds * 1e3) {
+    cudaEventRecord(e0);
+    peak_kernel<N><<<sms, 128, smem>>>(src, iters, sink, cyc, 0);
+    cudaEventRecord(e1);
+    CK(cudaEventSynchronize(e1));
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    std::vector<long long> c(sms);
+    CK(cudaMemcpy(c.data(), cyc, sms * sizeof(long long), cudaMemcpyDeviceToHost));
+    long long cmax = 0;
+    for (auto v : c) cmax = v > cmax ? v : cmax;
+    const double ops = 2.0 * 128 * N * 32 * 34.0 * iters * sms;
+    if (elapsed >= 1000.0) {
+      tops.push_back(ops / ms / 1e9);
+      mhz.push_back(cmax / (ms * 1e3));
+    }
+    elapsed += ms;
+  }
+  std::sort(tops.begin(), tops.end());
+  std::sort(mhz.begin(), mhz.end());
+  printf("SUSTAINED M=128 N=256 K=32 random, %.1f s back to back: median %.1f TOPS (min %.1f, max %.1f) over %zu "
+         "launches, median clock %.0f MHz\n",
+         seconds, tops[tops.size() / 2], tops.front(), tops.back(), tops.size(), mhz[mhz.size() / 2]);
+  CK(cudaFree(cyc));
+}
+
+int main(int argc, char **argv) {
   cudaDeviceProp p;
   CK(cudaGetDeviceProperties(&p, 0));
   printf("%s, %d SMs\n", p.name, p.multiProcessorCount);
+  const bool sustain_only = argc > 1 && strcmp(argv[1], "sustain") == 0;
   // (1) correctness, 1..4 accumulated K steps
   srand(7);
   std::vector<int8_t> a(4 * 128 * 32), b(4 * 64 * 32);
@@ -328,6 +370,10 @@ int main() {
   CK(cudaMalloc(&src, r.size()));
   CK(cudaMalloc(&sink, 4096));
   CK(cudaMemcpy(src, r.data(), r.size(), cudaMemcpyHostToDevice));
+  if (sustain_only) {
+    run_sustained(src, sink, p.multiProcessorCount, argc > 2 ? atof(argv[2]) : 5.0);
+    return bad_total ? 1 : 0;
+  }
   run_peak_pair<128>(src, p.multiProcessorCount);
   run_peak_pair<256>(src, p.multiProcessorCount);
   run_peak_ts<64>(src, sink, p.multiProcessorCount);
