@@ -9,7 +9,8 @@
 
 template <int T>
 void run(const double *x, double *u, uint8_t *f, long n, long l, long ldu, int rows_per_cta) {
-  const size_t smem = (size_t)rows_per_cta * l * sizeof(double);
+  const long lds = (l % 2) ? ((l + 3) & ~1L) : l;  // the host's slot stride for odd / misaligned rows
+  const size_t smem = (size_t)rows_per_cta * lds * sizeof(double);
   cudaFuncSetAttribute(pcc::normalize_rows_smem_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pcc::normalize_rows_smem_kernel<T>, T, smem);
@@ -20,7 +21,7 @@ void run(const double *x, double *u, uint8_t *f, long n, long l, long ldu, int r
     cudaEvent_t a, b;
     cudaEventCreate(&a); cudaEventCreate(&b);
     cudaEventRecord(a);
-    pcc::normalize_rows_smem_kernel<T><<<grid, T, smem>>>(x, l, u, ldu, f, l, 0, n, rows_per_cta, l, pcc::NormDests{});
+    pcc::normalize_rows_smem_kernel<T><<<grid, T, smem>>>(x, l, u, ldu, f, l, 0, n, rows_per_cta, lds, pcc::NormDests{});
     cudaEventRecord(b);
     cudaEventSynchronize(b);
     float ms; cudaEventElapsedTime(&ms, a, b);
@@ -45,11 +46,13 @@ int main(int argc, char **argv) {
   double *x, *u; uint8_t *f;
   cudaMalloc(&x, n * l * 8); cudaMalloc(&u, n * ldu * 8); cudaMalloc(&f, n);
   cudaMemcpy(x, h.data(), n * l * 8, cudaMemcpyHostToDevice);
-  run<64>(x, u, f, n, l, ldu, 1);
-  run<128>(x, u, f, n, l, ldu, 1);
-  run<256>(x, u, f, n, l, ldu, 1);
-  run<128>(x, u, f, n, l, ldu, 2);
-  run<256>(x, u, f, n, l, ldu, 2);
+  const int rows_list[] = {1, 2, 3, 4, 8};
+  for (int r : rows_list) {
+    if ((long)r * l * 8 > 200 * 1024) continue;
+    run<64>(x, u, f, n, l, ldu, r);
+    run<128>(x, u, f, n, l, ldu, r);
+    run<256>(x, u, f, n, l, ldu, r);
+  }
   printf("%s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
 }
