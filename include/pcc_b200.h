@@ -98,7 +98,8 @@ int pcc_normalize_rows_f64(const double *x, int64_t ldx, double *u, int64_t ldu,
  * pcc_ipc_open_handle -- normalisation fused with the all-gather of U in
  * the multi-GPU exchange (distributed.exchange_normalize, mode "p2p").
  * Replaces normalize_rows (_kernels.py:226-252) + the worker model's
- * per-worker normalisation (worker.py:68-80).  Rows up to 110 KB. */
+ * per-worker normalisation (worker.py:68-80).  Rows up to 110 KB, or of any
+ * length when 16-byte aligned with even l (the chunked kernel). */
 int pcc_normalize_rows_bcast_f64(const double *x, int64_t ldx, double *const *u, uint8_t *const *zero_variance,
                                  int32_t n_dest, int64_t ldu, int64_t l, int64_t row_lo, int64_t row_hi,
                                  void *stream);

@@ -612,7 +612,8 @@ int pcc_normalize_rows_bcast_f64(const double *x, int64_t ldx, double *const *u,
   const int rc = launch_normalize_staged<pcc::kNormBcast>(x, ldx, nullptr, ldu, nullptr, l, row_lo, row_hi, d,
                                                 (cudaStream_t)stream);
   if (rc == kNotStaged)
-    return fail(PCC_EINVAL, "rows of %lld samples are too long for the broadcast normaliser", (long long)l);
+    return fail(PCC_EINVAL, "rows of %lld samples are too long for the broadcast normaliser (unless 16-byte aligned "
+                "with even l)", (long long)l);
   return rc;
 }
 
