@@ -641,7 +641,11 @@ normalize_rows_chunked_kernel(const double *__restrict__ x, int64_t ldx, double 
       const int nsteps = (cnt - tid + 7) >> 3;
       if (pass == 0) {
         if (c == 0) ref = p[0];
+#if defined(PCC_K1C_EXP) && (PCC_K1C_EXP & 2)  // probe experiment: no constancy compare on the chain
+        row_chain_more<false, false>(s, p + tid, nsteps, ref, varies);
+#else
         row_chain_more<false, !kMinMax>(s, p + tid, nsteps, ref, varies);
+#endif
       } else {
         row_chain_more<true>(q, p + tid, nsteps, mean, varies);
       }
@@ -702,7 +706,11 @@ normalize_rows_chunked_kernel(const double *__restrict__ x, int64_t ldx, double 
           s_hi = hi;
         }
       }
-    } else if (pass == 2) {
+    } else if (pass == 2
+#if defined(PCC_K1C_EXP) && (PCC_K1C_EXP & 1)  // probe experiment: no output pass work
+               && false
+#endif
+    ) {
       // output of this chunk (+ the K padding after the last one)
       const bool zero = s_zero != 0;
       const double m0 = s_mean;
